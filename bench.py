@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the emulated complex GEMM (Ozaki-II / CRT on INT8 tcgen05).
+
+Workload (BASELINE.json metric "emulated ZGEMM/CGEMM TFLOPS at m=n=k=16384 vs
+cuBLAS native"): ZGEMM m=n=k=16384 per GPU, fast mode, N=14 moduli, phi=0.5
+synthetic inputs (configs[2]).  A "step" is one full emulated product
+C = A @ B: scaling + residues + 3N tcgen05 INT8 GEMMs + CRT.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+
+Multi-GPU: weak scaling by output tiles — rank r owns an A row-block and a B
+column-block (R x C grid) of a (16384 R) x (16384 C) x 16384 product and
+computes its C tile; fast mode needs no collective on the data path.
+
+`--impl reference` times the reference algorithm's CPU implementation (the
+numpy port in oracle/, float64-BLAS "INT8 engine" like the reference) on a
+bounded row/column-local sample of the same product on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "emulated ZGEMM TFLOPS (8mnk/t) at m=n=k=16384 per GPU, fast mode, 14 moduli"
+UNIT = "TFLOPS"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--m", type=int, default=16384)
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--k", type=int, default=16384)
+    ap.add_argument("--moduli", type=int, default=14)
+    ap.add_argument("--mode", choices=("fast", "accurate"), default="fast")
+    ap.add_argument("--precision", choices=("double", "single"), default="double")
+    ap.add_argument("--phi", type=float, default=0.5)
+    ap.add_argument("--n-block", type=int, default=8192)
+    ap.add_argument("--no-native", action="store_true", help="skip the cuBLAS native timing")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-sample", type=int, default=128,
+                    help="rows/cols of the CPU sample block (k kept full)")
+    return ap.parse_args()
+
+
+def workload_name(a) -> str:
+    kind = "zgemm" if a.precision == "double" else "cgemm"
+    return f"{kind}_{a.m}x{a.n}x{a.k}_{a.mode}_N{a.moduli}"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- helpers
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p.get("bf16_tflops", 1590.0), p.get("hbm_gbs", 6650.0), "measured"
+    except Exception:
+        return 1590.0, 6650.0, "fallback"
+
+
+def profile_traffic():
+    """Per-launch DRAM bytes of the GEMM from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def synth(torch, rows, cols, phi, seed, dtype, dev):
+    """(u - 0.5) * exp(z * phi) per part, the reference generator's distribution
+    (bench.py:50-54 there), drawn on the device."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    real = torch.float64 if dtype == torch.complex128 else torch.float32
+    parts = []
+    for _ in range(2):
+        u = torch.rand((rows, cols), generator=g, device=dev, dtype=real)
+        z = torch.randn((rows, cols), generator=g, device=dev, dtype=real)
+        parts.append((u - 0.5) * torch.exp(z * phi))
+    return torch.complex(parts[0], parts[1]).to(dtype)
+
+
+# --------------------------------------------------------------------------- CPU leg
+def cpu_sample(a, reps: int = 1):
+    """The reference algorithm on the host cores (oracle port, float64-BLAS INT8
+    engine): a row/column-local block `s x s x k` of the same product."""
+    from oracle import ozaki2 as orc
+    s = min(a.cpu_sample, a.m, a.n)
+    prec = a.precision
+    A = orc.gen_matrix(s, a.k, a.phi, 11, prec)
+    B = orc.gen_matrix(a.k, s, a.phi, 12, prec)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        orc.emulate_complex(A, B, a.moduli, a.mode, prec)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": 8.0 * s * s * a.k / t / 1e12, "unit": UNIT, "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": f"{s}x{s}x{a.k} block of the {a.m}x{a.n}x{a.k} product "
+                      f"({a.mode}, N={a.moduli}, phi={a.phi}), median of {reps}, "
+                      f"{t:.2f} s each, numpy+OpenBLAS on {os.cpu_count()} threads"}
+
+
+def run_reference(a, rank: int):
+    if rank != 0:
+        return
+    base = cpu_sample(a, reps=1)  # warm numpy/BLAS
+    vals = []
+    for _ in range(max(0, a.warmup - 1)):
+        cpu_sample(a)
+    for _ in range(a.steps):
+        vals.append(cpu_sample(a)["value"])
+    v = statistics.median(vals)
+    s = min(a.cpu_sample, a.m, a.n)
+    ms = 8.0 * s * s * a.k / (v * 1e12) * 1e3
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if a.precision == "double" else "f32",
+            "data": "synthetic (reference generator, Philox + ndtri)",
+            "config": {"workload": workload_name(a), "m": a.m, "n": a.n, "k": a.k,
+                       "num_moduli": a.moduli, "mode": a.mode, "precision": a.precision,
+                       "phi": a.phi},
+            "impl": "reference",
+            "cpu_baseline": {**base, "value": v},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU leg
+def run_ours(a, rank: int, world: int, local_rank: int):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_08321_b200 as crt
+    from paper_2512_08321_b200 import _native as nat
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    # 2-D grid of output tiles for weak scaling
+    R = 1 << (int(math.log2(world)) // 2)
+    Cc = world // R
+    r_i, c_i = rank // Cc, rank % Cc
+
+    cdt = torch.complex128 if a.precision == "double" else torch.complex64
+    A = synth(torch, a.m, a.k, a.phi, 1000 + r_i, cdt, dev)
+    B = synth(torch, a.k, a.n, a.phi, 2000 + c_i, cdt, dev)
+    cfg = crt.EmuConfig(precision=a.precision, domain="complex", mode=a.mode,
+                        num_moduli=a.moduli, n_block=a.n_block)
+    ws = None
+    out = torch.empty((a.m, a.n), dtype=cdt, device=dev)
+
+    def step():
+        crt.run_complex(A, B, cfg, None, dev, sync_check=False, ws=ws_holder[0], out=out)
+
+    ws_holder = [None]
+    lib = nat.load()
+    need = lib.crtg_workspace_size((1 if a.precision == "single" else 0)
+                                   | (16 if cdt == torch.complex64 else 0),
+                                   0 if a.mode == "fast" else 1, a.m, a.n, a.k, a.moduli,
+                                   a.n_block)
+    ws_holder[0] = torch.empty(need, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        step()
+    barrier()
+    nat.profile_enable(True)
+    nat.profile_read()  # clear
+    launches0 = nat.launch_count()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    launches = nat.launch_count() - launches0
+    stage_ms, stage_n = nat.profile_read()
+    nat.profile_enable(False)
+    ms_total = e0.elapsed_time(e1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / a.steps
+    flops_step = 8.0 * a.m * a.n * a.k * world
+    value = flops_step / (ms_step * 1e-3) / 1e12
+
+    # roofline of the dominant kernel (K3 tcgen05 GEMM): algorithmic INT8 ops per
+    # launch = 6 * N * m * n_block * k (3 GEMMs x 2 ops/MAC x N moduli)
+    bf16, hbm, src = peaks()
+    gemm_ms = stage_ms["gemm"] / max(1, stage_n["gemm"])
+    nblocks = math.ceil(a.n / min(a.n, -(-a.n_block // 256) * 256))
+    ops_launch = 6.0 * a.moduli * a.m * (a.n / nblocks) * a.k
+    achieved = ops_launch / (gemm_ms * 1e-3) / 1e12
+    peak_int8 = 2.0 * bf16
+    traffic = profile_traffic()
+    roof = {"bound": "tensor", "kernel": "k_gemm_i8<EPI_KARATSUBA>", "achieved": achieved,
+            "peak": peak_int8, "unit": "TOPS", "frac": achieved / peak_int8,
+            "peak_note": f"INT8 dense = 2 x {src} bf16 ({bf16} TF/s, MEASURED_PEAKS.json); "
+                         "spec 4500 TOPS",
+            "frac_of_spec": achieved / 4500.0,
+            "ops_per_launch": ops_launch, "ms_per_launch": gemm_ms,
+            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None}
+    stages = {k: v / a.steps for k, v in stage_ms.items()}
+
+    result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+              "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
+              "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+              "dtype": "int8 tensor / f64" if a.precision == "double" else "int8 tensor / f32",
+              "data": "synthetic (u-0.5)*exp(z*phi), drawn on device",
+              "config": {"workload": workload_name(a), "m": a.m, "n": a.n, "k": a.k,
+                         "num_moduli": a.moduli, "mode": a.mode, "precision": a.precision,
+                         "phi": a.phi, "n_block": a.n_block, "grid": f"{R}x{Cc}",
+                         "parallelism": f"output-tile x{world}",
+                         "l2": "inputs (4 GiB each) exceed L2; no flush"},
+              "stage_ms_per_step": stages, "gpu_launches": int(launches),
+              "roofline": roof, "clocks": clocks}
+
+    # cuBLAS native baseline on the same device (rank 0)
+    if rank == 0 and not a.no_native:
+        torch.backends.cuda.matmul.allow_tf32 = False
+        for _ in range(2):
+            torch.matmul(A, B, out=out)
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        reps = 3
+        f0.record(stream)
+        for _ in range(reps):
+            torch.matmul(A, B, out=out)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        nat_ms = f0.elapsed_time(f1) / reps
+        nat_tf = 8.0 * a.m * a.n * a.k / (nat_ms * 1e-3) / 1e12
+        result["native_cublas"] = {"op": "torch.matmul " + str(cdt).replace("torch.", ""),
+                                   "ms": nat_ms, "tflops": nat_tf,
+                                   "speedup_per_gpu": (value / world) / nat_tf}
+
+    # end to end through the public API with host buffers (rank 0 shape per rank)
+    if not a.no_e2e:
+        hA = A.cpu().pin_memory()
+        hB = B.cpu().pin_memory()
+        hC = torch.empty((a.m, a.n), dtype=cdt).pin_memory()
+        cfg_e = crt.EmuConfig(precision=a.precision, domain="complex", mode=a.mode,
+                              num_moduli=a.moduli, n_block=a.n_block)
+
+        def e2e_step():
+            c = crt.emulate_gemm_complex(hA, hB, cfg_e)
+            hC.copy_(c)
+            return c
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        reps = max(1, min(a.steps, 3))
+        for _ in range(reps):
+            e2e_step()
+        barrier()
+        dt = (time.perf_counter() - t0) / reps
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        result["e2e"] = {"value": flops_step / dt / 1e12, "unit": UNIT,
+                         "h2d_bytes_per_step": int(hA.numel() * hA.element_size()
+                                                   + hB.numel() * hB.element_size()),
+                         "d2h_bytes_per_step": int(hC.numel() * hC.element_size()),
+                         "ms_per_step": dt * 1e3,
+                         "api": "paper_2512_08321_b200.emulate_gemm_complex(pinned host tensors)"}
+
+    if rank == 0 and world == 1 and not a.no_cpu:
+        result["cpu_baseline"] = cpu_sample(a, reps=1)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus if a.gpus == 1 else 1)))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank)
+        return
+    run_ours(a, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,175 @@
+/*
+ * crtg.h — C-ABI of the B200 (sm_100a) Ozaki-II / CRT complex GEMM emulation.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * `crtgemm.emulate_gemm_complex` (/root/reference/pkg/src/crtgemm/emulate.py:193-240)
+ * and its BLAS-style wrapper `crtgemm.gemm` (emulate.py:256-278).  The reference
+ * is a pure-Python package, so "the reference FFI for this path" is its Python
+ * call surface; every entry point below replaces one reference function and is
+ * bound with ctypes by `paper_2512_08321_b200/_native.py`.
+ *
+ * Conventions
+ *   - All matrix pointers are DEVICE pointers; `stream` is a cudaStream_t (NULL =
+ *     legacy default stream).  Every launch is stream-ordered; no call allocates
+ *     memory: scratch comes from the caller-owned workspace `ws`.
+ *   - Complex matrices are interleaved (re, im) pairs, row-major, with a row
+ *     stride `ld*` counted in complex elements.  Inputs are complex128, or
+ *     complex64 with CRTG_IN_C64 (upcast exactly, emulate.py:159-166); the
+ *     result is complex128 (CRTG_DOUBLE) or complex64 (CRTG_SINGLE).
+ *   - Return value: CRTG_OK or one of the CRTG_ERR_* codes; crtg_last_error()
+ *     returns a thread-local message.  The Python layer maps
+ *     CONFIG->ConfigError, DIMENSION->DimensionError, DOMAIN->DomainError
+ *     (reference errors.py:4-13).
+ *   - Data-dependent domain errors (non-finite input, |a'| >= 2^90 after
+ *     scaling) are detected on the device and reported through `diag`
+ *     (device uint64[CRTG_DIAG_LEN]); with sync_check != 0 the call synchronizes
+ *     the stream and returns CRTG_ERR_DOMAIN itself.
+ */
+#ifndef CRTG_H
+#define CRTG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CRTG_MAX_MODULI 20
+
+enum crtg_status {
+  CRTG_OK = 0,
+  CRTG_ERR_CONFIG = 1,     /* ConfigError     */
+  CRTG_ERR_DIMENSION = 2,  /* DimensionError  */
+  CRTG_ERR_DOMAIN = 3,     /* DomainError     */
+  CRTG_ERR_CUDA = 4,       /* launch / device failure */
+  CRTG_ERR_WORKSPACE = 5,  /* ws too small */
+  CRTG_ERR_ARITH = 6       /* ArithmeticError (int32 accumulator bound) */
+};
+
+/* precision argument: low bit = result precision (double -> complex128 result
+ * and the double-double CRT path; single -> complex64 result and the plain-f64
+ * CRT path, crt.py:246-258).  OR in CRTG_IN_C64 when the inputs are complex64
+ * (read and upcast exactly on the device); otherwise inputs are complex128. */
+enum crtg_precision { CRTG_DOUBLE = 0, CRTG_SINGLE = 1, CRTG_IN_C64 = 16 };
+enum crtg_mode { CRTG_FAST = 0, CRTG_ACCURATE = 1 };
+
+/* diag[] slots (device uint64) */
+enum crtg_diag {
+  CRTG_DIAG_CLAMPED_MU = 0,  /* scaling.py:165-171 key "clamped_mu" */
+  CRTG_DIAG_CLAMPED_NU = 1,  /* key "clamped_nu" */
+  CRTG_DIAG_NONFINITE_A = 2, /* emulate.py:163-165 */
+  CRTG_DIAG_NONFINITE_B = 3,
+  CRTG_DIAG_OVERFLOW_A = 4,  /* scaling.py:290-292, crt.py:209-210 */
+  CRTG_DIAG_OVERFLOW_B = 5,
+  CRTG_DIAG_LEN = 8
+};
+
+/*
+ * Modulus-set constants.  Built on the host from exact big-integer arithmetic
+ * (reference crt.py:52-110 `ModulusSet.from_moduli`, scaling.py:100-115
+ * `ScalingConstants.from_product`) — the Python layer fills it.
+ */
+typedef struct crtg_consts {
+  int32_t num_moduli;                  /* N in 1..20 */
+  int32_t moduli[CRTG_MAX_MODULI];     /* descending, pairwise coprime, <= 256 */
+  double coeff_hi[CRTG_MAX_MODULI];    /* crt.py:84-86 */
+  double coeff_lo[CRTG_MAX_MODULI];
+  double p_hi;                         /* float(P)           crt.py:163 */
+  double p_lo;                         /* float(P - int(p_hi)) crt.py:164 */
+  float p_fast;                        /* ScalingConstants.p_fast */
+  float p_accu;                        /* ScalingConstants.p_accu */
+  float delta;                         /* ScalingConstants.delta  */
+  int32_t reserved;
+} crtg_consts;
+
+/* library identity / errors */
+const char* crtg_version(void);
+const char* crtg_last_error(void);
+/* 0 if `device` is an sm_100 part the kernels were built for, else CRTG_ERR_CUDA */
+int crtg_device_check(int device);
+
+/*
+ * Bytes of scratch `crtg_gemm_complex` needs.  n_block bounds the number of B
+ * columns processed per pass (reference kernel.py:15 DEFAULT_N_BLOCK, used here
+ * as a working-set bound only — results are bitwise independent of it).
+ */
+size_t crtg_workspace_size(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                           int num_moduli, int64_t n_block);
+
+/*
+ * C = A @ B emulated with N moduli (replaces emulate_gemm_complex,
+ * emulate.py:193-240).  A: m x k, B: k x n, C: m x n.  mu_out / nu_out
+ * (device int32[m] / int32[n], may be NULL) receive the scaling exponents.
+ */
+int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                      const void* A, int64_t lda, const void* B, int64_t ldb,
+                      void* C, int64_t ldc, const crtg_consts* K, int64_t n_block,
+                      void* ws, size_t ws_bytes, int32_t* mu_out, int32_t* nu_out,
+                      uint64_t* diag, int sync_check, void* stream);
+
+/* ---- parity hooks: each reuses the production kernels of one stage ---- */
+
+/* Scaling vectors only (fast_scaling scaling.py:198-213 / accurate_scaling
+ * scaling.py:229-274).  Workspace: crtg_workspace_size(...). */
+int crtg_scaling(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                 const void* A, int64_t lda, const void* B, int64_t ldb,
+                 const crtg_consts* K, void* ws, size_t ws_bytes,
+                 int32_t* mu_out, int32_t* nu_out, uint64_t* diag, void* stream);
+
+/* quantize (scaling.py:277-293) + residue_decompose (crt.py:199-218) with
+ * injected exponents.  operand 0: X is the left operand (rows x kdim, exps per
+ * row); operand 1: X is the right operand (kdim x rows, exps per column).
+ * out: int8 [N][3][rows][kdim] with planes (re, im, mod(re+im)) — the third is
+ * the Karatsuba sum of kernel.py:101-103.  Workspace: packed tiles,
+ * 3*N*round_up(rows,256)*round_up(kdim,128) bytes. */
+int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim,
+                  const void* X, int64_t ldx, const int32_t* exps,
+                  const crtg_consts* K, int8_t* out, void* ws, size_t ws_bytes,
+                  uint64_t* diag, void* stream);
+
+/* Exact int8 x int8 -> int32 on tcgen05 (replaces gemm_i8_i32,
+ * kernel.py:20-35).  A: m x k row-major, B: k x n row-major, C: m x n. */
+size_t crtg_i8_workspace_size(int64_t m, int64_t n, int64_t k, int nplanes);
+int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A,
+                     const int8_t* B, int32_t* C, void* ws, size_t ws_bytes,
+                     void* stream);
+
+/* Modular complex product on residue operands, Karatsuba form (replaces
+ * complex_gemm_mod, kernel.py:70-120): e_re = ar br - ai bi, e_im = ar bi +
+ * ai br (mod p), symmetric int8.  Inputs row-major: ar, ai m x k; br, bi k x n.
+ * Workspace: crtg_i8_workspace_size(m, n, k, 3). */
+int crtg_complex_gemm_mod(int64_t m, int64_t n, int64_t k, const int8_t* ar,
+                          const int8_t* ai, const int8_t* br, const int8_t* bi,
+                          int p, int8_t* e_re, int8_t* e_im, void* ws,
+                          size_t ws_bytes, void* stream);
+
+/* CRT accumulate + reduce + inverse scale + complex assembly (crt.py:221-258,
+ * emulate.py:135-144, 234-240).  e_re / e_im: int8 [N][m][n]. */
+int crtg_crt_reconstruct(int precision, int64_t m, int64_t n, const int8_t* e_re,
+                         const int8_t* e_im, const int32_t* mu, const int32_t* nu,
+                         const crtg_consts* K, void* C, int64_t ldc, void* stream);
+
+/* ---- instrumentation (bench.py) ---- */
+/* total kernels this library has launched in the process */
+uint64_t crtg_launch_count(void);
+/* stage ids for the per-stage device timers */
+enum crtg_stage {
+  CRTG_STAGE_SCALING = 0, /* K1 (+ bound GEMM in accurate mode) */
+  CRTG_STAGE_RESIDUE_A = 1,
+  CRTG_STAGE_RESIDUE_B = 2,
+  CRTG_STAGE_GEMM = 3, /* K3 Karatsuba tcgen05 GEMM (all moduli of a block) */
+  CRTG_STAGE_CRT = 4,
+  CRTG_STAGE_COUNT = 5
+};
+/* enable (1) / disable (0) CUDA-event timing of every stage launch, recorded
+ * on the launching stream */
+int crtg_profile_enable(int on);
+/* synchronize the recorded events and return, per stage, the summed device
+ * milliseconds (ms[CRTG_STAGE_COUNT]) and launch counts; clears the record */
+int crtg_profile_read(double* ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CRTG_H */

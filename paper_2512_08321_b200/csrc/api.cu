@@ -1,0 +1,696 @@
+// api.cu — the C-ABI (include/crtg.h): argument checks, workspace planning and the
+// stream-ordered launch sequence of the complex Ozaki-II pipeline.
+//
+// Pipeline of crtg_gemm_complex (reference emulate.py:193-240):
+//   K1   scaling: fast (row pairwise / column sequential sums of squares) or
+//        accurate (bound operands + tcgen05 bound GEMM + row/col maxima)
+//   K2   quantize + residues of A, packed for tcgen05 (once)
+//   for each column block of B (n_block, bitwise-neutral working-set bound):
+//     K2 quantize + residues of the B block (transposed into K-major tiles)
+//     K3 Karatsuba INT8 GEMMs for all N moduli, modular epilogue -> int8 planes
+//     K4 CRT + inverse scaling -> C block
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/crtg.h"
+#include "common.cuh"
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+using namespace crtg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_check(int err, const char* where) {
+  if (err == 0) return CRTG_OK;
+  return fail(CRTG_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(cudaError_t(err)));
+}
+
+#define CRTG_TRY(expr, where)                    \
+  do {                                           \
+    const int _e = (expr);                       \
+    if (_e) return cuda_check(_e, where);        \
+  } while (0)
+
+// ---- instrumentation: launch counter and per-stage CUDA-event timers ----
+std::atomic<uint64_t> g_launches{0};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+struct ProfRec {
+  int stage;
+  cudaEvent_t a, b;
+};
+std::vector<ProfRec> g_prof;
+
+struct StageTimer {
+  int stage;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  int kernels;
+  StageTimer(int st, cudaStream_t str, int nkernels) : stage(st), s(str), kernels(nkernels) {
+    if (g_prof_on) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~StageTimer() {
+    g_launches += uint64_t(kernels);
+    if (a) {
+      cudaEventRecord(b, s);
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      g_prof.push_back({stage, a, b});
+    }
+  }
+};
+
+int sm_count() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (n <= 0) n = 148;
+  cache[dev] = n;
+  return n;
+}
+
+int check_consts(const crtg_consts* K, int* n_out) {
+  if (!K) return fail(CRTG_ERR_CONFIG, "modulus constants are required");
+  const int n = K->num_moduli;
+  if (n < 1 || n > CRTG_MAX_MODULI) return fail(CRTG_ERR_CONFIG, "num_moduli must be in 1..20");
+  for (int l = 0; l < n; ++l)
+    if (K->moduli[l] < 2 || K->moduli[l] > 256)
+      return fail(CRTG_ERR_CONFIG, "modulus outside [2, 256]");
+  *n_out = n;
+  return CRTG_OK;
+}
+
+ModConst make_mod(int p) {
+  ModConst c{};
+  c.p = p;
+  c.is_pow2 = (p & (p - 1)) == 0;
+  int sh = 0;
+  while ((2 << sh) <= p) ++sh;  // floor(log2 p)
+  c.shift = sh;
+  if (!c.is_pow2) {
+    const unsigned __int128 num = (unsigned __int128)1 << (32 + sh);
+    c.magic = uint32_t((num + p - 1) / p);
+  }
+  c.half = (p + 1) / 2;
+  c.c16 = uint32_t((1u << 16) % p);
+  c.c32 = uint32_t((uint64_t(1) << 32) % p);
+  const int64_t q = ((int64_t(1) << 30) + p - 1) / p;
+  c.bias = int32_t(q * p);
+  return c;
+}
+
+DevConsts make_dev(const crtg_consts& K) {
+  DevConsts d{};
+  d.n = K.num_moduli;
+  for (int l = 0; l < d.n; ++l) {
+    const int p = K.moduli[l];
+    d.mc[l] = make_mod(p);
+    uint32_t v = 1 % p;
+    for (int s = 0; s < 40; ++s) {
+      d.pow2mod[l][s] = uint16_t(v);
+      v = (v * 2) % p;
+    }
+    d.coeff_hi[l] = K.coeff_hi[l];
+    d.coeff_lo[l] = K.coeff_lo[l];
+  }
+  d.p_hi = K.p_hi;
+  d.p_lo = K.p_lo;
+  d.p_fast = K.p_fast;
+  d.p_accu = K.p_accu;
+  d.delta = K.delta;
+  return d;
+}
+
+// ---- numpy pairwise-sum tree of one row (see kernels.cuh PwTree) ----
+struct HostTree {
+  std::vector<int2> leaves;
+  std::vector<int2> nodes;  // sorted by height
+  std::vector<int> level_start;
+};
+
+const HostTree& pairwise_tree(int64_t n) {
+  static std::mutex mu;
+  static std::map<int64_t, HostTree> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(n);
+  if (it != cache.end()) return it->second;
+  HostTree t;
+  struct Raw {
+    int left, right, height;  // child ids: >= 0 leaf index, < 0 -> ~node index
+  };
+  std::vector<Raw> raw;
+  // returns id: leaf index >= 0, or ~node index
+  struct Rec {
+    HostTree& t;
+    std::vector<Raw>& raw;
+    int go(int64_t start, int64_t len, int* height) {
+      if (len <= 128) {
+        t.leaves.push_back(make_int2(int(start), int(len)));
+        *height = 0;
+        return int(t.leaves.size()) - 1;
+      }
+      int64_t h = len / 2;
+      h -= h % 8;
+      int hl, hr;
+      const int l = go(start, h, &hl);
+      const int r = go(start + h, len - h, &hr);
+      *height = std::max(hl, hr) + 1;
+      raw.push_back({l, r, *height});
+      return ~int(raw.size() - 1);
+    }
+  } rec{t, raw};
+  int hroot = 0;
+  rec.go(0, n, &hroot);
+  const int nl = int(t.leaves.size());
+  // order nodes by height; slot of node = nl + sorted position
+  std::vector<int> order(raw.size());
+  for (size_t i = 0; i < raw.size(); ++i) order[i] = int(i);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int a, int b) { return raw[a].height < raw[b].height; });
+  std::vector<int> pos(raw.size());
+  for (size_t i = 0; i < order.size(); ++i) pos[order[i]] = int(i);
+  auto slot = [&](int id) { return id >= 0 ? id : nl + pos[~id]; };
+  for (int idx : order) t.nodes.push_back(make_int2(slot(raw[idx].left), slot(raw[idx].right)));
+  t.level_start.push_back(0);
+  for (int h = 1; h <= hroot; ++h) {
+    int cnt = 0;
+    for (auto& r : raw) cnt += r.height == h;
+    t.level_start.push_back(t.level_start.back() + cnt);
+  }
+  return cache.emplace(n, std::move(t)).first->second;
+}
+
+size_t tree_bytes(int64_t k) { return size_t(16) * (k / 64 + 4) + 4 * 64 + 256; }
+
+// ---- workspace plan ----
+struct Region {
+  size_t off = 0, bytes = 0;
+};
+struct Plan {
+  int64_t m, n, k, N, nb, m_pad, n_pad, nb_pad, k_pad;
+  Region diag, mu, nu, rowabs, colabs, colsq, tree, bar_mu, bar_nu, rowmax, colmax, a_pack,
+      b_pack, e_re, e_im, a_bars, b_bars;
+  size_t total = 0;
+};
+
+void add(Plan& p, Region& r, size_t bytes) {
+  r.off = p.total;
+  r.bytes = bytes;
+  p.total += (bytes + 255) & ~size_t(255);
+}
+
+Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_block) {
+  Plan p{};
+  p.m = m;
+  p.n = n;
+  p.k = k;
+  p.N = N;
+  p.m_pad = round_up(std::max<int64_t>(m, 1), 128);
+  p.n_pad = round_up(std::max<int64_t>(n, 1), 256);
+  p.k_pad = round_up(std::max<int64_t>(k, 1), 128);
+  int64_t nb = n_block < 1 ? n : n_block;
+  nb = std::min(round_up(nb, 256), p.n_pad);
+  p.nb = nb;
+  p.nb_pad = nb;
+  add(p, p.diag, 8 * CRTG_DIAG_LEN);
+  add(p, p.mu, 4 * p.m_pad);
+  add(p, p.nu, 4 * p.n_pad);
+  add(p, p.rowabs, 8 * p.m_pad);
+  add(p, p.colabs, 8 * p.n_pad);
+  add(p, p.colsq, 16 * p.n_pad);
+  add(p, p.tree, tree_bytes(k));
+  add(p, p.a_pack, size_t(3 * N) * p.m_pad * p.k_pad);
+  add(p, p.b_pack, size_t(3 * N) * p.nb_pad * p.k_pad);
+  add(p, p.e_re, size_t(N) * m * p.nb_pad);
+  add(p, p.e_im, size_t(N) * m * p.nb_pad);
+  if (mode == CRTG_ACCURATE) {
+    add(p, p.bar_mu, 4 * p.m_pad);
+    add(p, p.bar_nu, 4 * p.n_pad);
+    add(p, p.rowmax, 4 * p.m_pad);
+    add(p, p.colmax, 4 * p.n_pad);
+    add(p, p.a_bars, size_t(3) * p.m_pad * p.k_pad);
+    add(p, p.b_bars, size_t(3) * p.n_pad * p.k_pad);
+  }
+  return p;
+}
+
+template <typename T>
+T* at(void* ws, const Region& r) {
+  return reinterpret_cast<T*>(static_cast<char*>(ws) + r.off);
+}
+
+int check_dims(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_t ldc,
+               int64_t max_k = 65536) {
+  if (m < 1 || n < 1 || k < 1) return fail(CRTG_ERR_DIMENSION, "m, n, k must be positive");
+  if (k > max_k)
+    return fail(CRTG_ERR_DIMENSION,
+                "inner dimension " + std::to_string(k) + " exceeds " + std::to_string(max_k));
+  if (lda < k || ldb < n || ldc < n) return fail(CRTG_ERR_DIMENSION, "leading dimension too small");
+  if (m > (int64_t(1) << 31) || n > (int64_t(1) << 31))
+    return fail(CRTG_ERR_DIMENSION, "dimension too large");
+  return CRTG_OK;
+}
+
+// exponents (fast or accurate) into mu / nu of the plan
+int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t lda,
+                const void* B, int64_t ldb, const DevConsts& dc, void* ws,
+                unsigned long long* diag, cudaStream_t s) {
+  const bool single = (precision & CRTG_IN_C64) != 0;  // input element type
+  int32_t* mu = at<int32_t>(ws, P.mu);
+  int32_t* nu = at<int32_t>(ws, P.nu);
+  double* rowabs = at<double>(ws, P.rowabs);
+  double* colabs = at<double>(ws, P.colabs);
+  CRTG_TRY(cudaMemsetAsync(colabs, 0, P.colabs.bytes, s), "memset");
+  PwTree tree{};
+  if (mode == CRTG_FAST) {
+    const HostTree& ht = pairwise_tree(P.k);
+    char* tb = at<char>(ws, P.tree);
+    const size_t lb = ht.leaves.size() * sizeof(int2), nb = ht.nodes.size() * sizeof(int2),
+                 sb = ht.level_start.size() * sizeof(int);
+    if (lb + nb + sb + 64 > P.tree.bytes) return fail(CRTG_ERR_WORKSPACE, "tree region too small");
+    CRTG_TRY(cudaMemcpyAsync(tb, ht.leaves.data(), lb, cudaMemcpyHostToDevice, s), "tree copy");
+    if (nb) CRTG_TRY(cudaMemcpyAsync(tb + lb, ht.nodes.data(), nb, cudaMemcpyHostToDevice, s), "tree copy");
+    CRTG_TRY(cudaMemcpyAsync(tb + lb + nb, ht.level_start.data(), sb, cudaMemcpyHostToDevice, s),
+             "tree copy");
+    tree.nleaves = int(ht.leaves.size());
+    tree.nnodes = int(ht.nodes.size());
+    tree.nlevels = int(ht.level_start.size()) - 1;
+    tree.leaves = reinterpret_cast<const int2*>(tb);
+    tree.nodes = reinterpret_cast<const int2*>(tb + lb);
+    tree.level_start = reinterpret_cast<const int*>(tb + lb + nb);
+    StageTimer timer(CRTG_STAGE_SCALING, s, 4);
+    CRTG_TRY(launch_row_stats(single, true, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu,
+                              rowabs, diag, s),
+             "row stats");
+    CRTG_TRY(launch_col_absmax(single, B, ldb, P.k, P.n, colabs, diag, s), "col absmax");
+    CRTG_TRY(launch_col_fast(single, B, ldb, P.k, P.n, colabs, at<double>(ws, P.colsq), dc.p_fast,
+                             dc.delta, nu, diag, s),
+             "col sumsq");
+    return CRTG_OK;
+  }
+  // accurate mode (scaling.py:229-274)
+  int32_t* bar_mu = at<int32_t>(ws, P.bar_mu);
+  int32_t* bar_nu = at<int32_t>(ws, P.bar_nu);
+  int32_t* rowmax = at<int32_t>(ws, P.rowmax);
+  int32_t* colmax = at<int32_t>(ws, P.colmax);
+  CRTG_TRY(cudaMemsetAsync(rowmax, 0, P.rowmax.bytes, s), "memset");
+  CRTG_TRY(cudaMemsetAsync(colmax, 0, P.colmax.bytes, s), "memset");
+  StageTimer timer(CRTG_STAGE_SCALING, s, 9);
+  CRTG_TRY(launch_row_stats(single, false, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu, rowabs,
+                            diag, s),
+           "row absmax");
+  CRTG_TRY(launch_bar(rowabs, P.m, bar_mu, s), "bar");
+  CRTG_TRY(launch_col_absmax(single, B, ldb, P.k, P.n, colabs, diag, s), "col absmax");
+  CRTG_TRY(launch_bar(colabs, P.n, bar_nu, s), "bar");
+  const int64_t a_plane = P.m_pad * P.k_pad, b_plane = P.n_pad * P.k_pad;
+  int8_t* abars = at<int8_t>(ws, P.a_bars);
+  int8_t* bbars = at<int8_t>(ws, P.b_bars);
+  CRTG_TRY(launch_pack(single, 0, PACK_BARS, A, lda, P.m, P.k, 0, bar_mu, dc, abars, a_plane,
+                       P.m_pad / 128, diag + CRTG_DIAG_OVERFLOW_A, s),
+           "bars A");
+  CRTG_TRY(launch_pack(single, 1, PACK_BARS, B, ldb, P.n, P.k, 0, bar_nu, dc, bbars, b_plane,
+                       P.n_pad / 128, diag + CRTG_DIAG_OVERFLOW_B, s),
+           "bars B");
+  GemmArgs g{};
+  g.a = abars;
+  g.b = bbars;
+  g.a_plane = a_plane;
+  g.b_plane = b_plane;
+  g.a_rb = int(P.m_pad / 128);
+  g.b_rb = int(P.n_pad / 128);
+  g.mt = int(P.m_pad / 128);
+  g.nt = int(P.n_pad / 256);
+  g.kb = int(P.k_pad / 128);
+  g.nl = 1;
+  g.planes_per_l = 3;
+  g.nphase = 3;
+  g.m = int(P.m);
+  g.n = int(P.n);
+  g.row_max = rowmax;
+  g.col_max = colmax;
+  CRTG_TRY(launch_gemm(EPI_BOUND, g, sm_count(), s), "bound gemm");
+  CRTG_TRY(launch_accurate_exps(rowmax, rowabs, bar_mu, P.m, dc.p_accu, dc.delta, mu,
+                                diag + CRTG_DIAG_CLAMPED_MU, s),
+           "accurate mu");
+  CRTG_TRY(launch_accurate_exps(colmax, colabs, bar_nu, P.n, dc.p_accu, dc.delta, nu,
+                                diag + CRTG_DIAG_CLAMPED_NU, s),
+           "accurate nu");
+  return CRTG_OK;
+}
+
+int check_diag(const unsigned long long* diag_dev, cudaStream_t s) {
+  unsigned long long h[CRTG_DIAG_LEN];
+  CRTG_TRY(cudaMemcpyAsync(h, diag_dev, sizeof(h), cudaMemcpyDeviceToHost, s), "diag copy");
+  CRTG_TRY(cudaStreamSynchronize(s), "sync");
+  if (h[CRTG_DIAG_NONFINITE_A]) return fail(CRTG_ERR_DOMAIN, "A contains non-finite entries");
+  if (h[CRTG_DIAG_NONFINITE_B]) return fail(CRTG_ERR_DOMAIN, "B contains non-finite entries");
+  if (h[CRTG_DIAG_OVERFLOW_A] || h[CRTG_DIAG_OVERFLOW_B])
+    return fail(CRTG_ERR_DOMAIN, "scaled magnitudes exceed the quantization budget");
+  return CRTG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* crtg_version(void) { return "crtg 0.1.0 (sm_100a tcgen05 int8)"; }
+
+const char* crtg_last_error(void) { return g_last_error.c_str(); }
+
+int crtg_device_check(int device) {
+  cudaDeviceProp prop;
+  const cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) return cuda_check(int(e), "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(CRTG_ERR_CUDA, std::string("device is sm_") + std::to_string(prop.major) +
+                                   std::to_string(prop.minor) + ", kernels are built for sm_100a");
+  return CRTG_OK;
+}
+
+size_t crtg_workspace_size(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                           int num_moduli, int64_t n_block) {
+  (void)precision;
+  return make_plan(mode, m, n, k, num_moduli, n_block).total;
+}
+
+int crtg_scaling(int precision, int mode, int64_t m, int64_t n, int64_t k, const void* A,
+                 int64_t lda, const void* B, int64_t ldb, const crtg_consts* K, void* ws,
+                 size_t ws_bytes, int32_t* mu_out, int32_t* nu_out, uint64_t* diag,
+                 void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if (mode != CRTG_FAST && mode != CRTG_ACCURATE) return fail(CRTG_ERR_CONFIG, "bad mode");
+  // fast_scaling itself has no k cap (scaling.py:198-213); the bound product does
+  if (int e = check_dims(m, n, k, lda, ldb, n, mode == CRTG_FAST ? (int64_t(1) << 18) : 65536))
+    return e;
+  const Plan P = make_plan(mode, m, n, k, N, n);
+  if (ws_bytes < P.total) return fail(CRTG_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
+                                : at<unsigned long long>(ws, P.diag);
+  CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
+  const DevConsts dc = make_dev(*K);
+  if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s)) return e;
+  if (mu_out)
+    CRTG_TRY(cudaMemcpyAsync(mu_out, at<int32_t>(ws, P.mu), 4 * m, cudaMemcpyDeviceToDevice, s), "copy");
+  if (nu_out)
+    CRTG_TRY(cudaMemcpyAsync(nu_out, at<int32_t>(ws, P.nu), 4 * n, cudaMemcpyDeviceToDevice, s), "copy");
+  return CRTG_OK;
+}
+
+int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, const void* A,
+                      int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                      const crtg_consts* K, int64_t n_block, void* ws, size_t ws_bytes,
+                      int32_t* mu_out, int32_t* nu_out, uint64_t* diag, int sync_check,
+                      void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if ((precision & ~(CRTG_SINGLE | CRTG_IN_C64)) != 0)
+    return fail(CRTG_ERR_CONFIG, "precision must be double or single");
+  if (mode != CRTG_FAST && mode != CRTG_ACCURATE) return fail(CRTG_ERR_CONFIG, "bad mode");
+  if (int e = check_dims(m, n, k, lda, ldb, ldc)) return e;
+  const Plan P = make_plan(mode, m, n, k, N, n_block);
+  if (!ws || ws_bytes < P.total)
+    return fail(CRTG_ERR_WORKSPACE, "workspace too small: need " + std::to_string(P.total));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool in32 = (precision & CRTG_IN_C64) != 0;
+  const bool single = (precision & CRTG_SINGLE) != 0;  // result type / CRT path
+  unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
+                                : at<unsigned long long>(ws, P.diag);
+  CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
+  const DevConsts dc = make_dev(*K);
+
+  if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s)) return e;
+  int32_t* mu = at<int32_t>(ws, P.mu);
+  int32_t* nu = at<int32_t>(ws, P.nu);
+
+  // K2: residues of A (once)
+  const int64_t a_plane = P.m_pad * P.k_pad;
+  int8_t* apack = at<int8_t>(ws, P.a_pack);
+  {
+    StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
+    CRTG_TRY(launch_pack(in32, 0, PACK_RESIDUE, A, lda, m, k, 0, mu, dc, apack, a_plane,
+                         P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s),
+             "residues A");
+  }
+
+  int8_t* bpack = at<int8_t>(ws, P.b_pack);
+  int8_t* ere = at<int8_t>(ws, P.e_re);
+  int8_t* eim = at<int8_t>(ws, P.e_im);
+  const size_t csz = single ? 8 : 16;
+  for (int64_t j0 = 0; j0 < n; j0 += P.nb) {
+    const int64_t w = std::min(P.nb, n - j0);
+    const int64_t w_pad = round_up(w, 256);
+    const int64_t b_plane = w_pad * P.k_pad;
+    {
+      StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
+      CRTG_TRY(launch_pack(in32, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack, b_plane,
+                           w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
+               "residues B");
+    }
+    GemmArgs g{};
+    g.a = apack;
+    g.b = bpack;
+    g.a_plane = a_plane;
+    g.b_plane = b_plane;
+    g.a_rb = int(P.m_pad / 128);
+    g.b_rb = int(w_pad / 128);
+    g.mt = int(P.m_pad / 128);
+    g.nt = int(w_pad / 256);
+    g.kb = int(P.k_pad / 128);
+    g.nl = N;
+    g.planes_per_l = 3;
+    g.nphase = 3;
+    g.m = int(m);
+    g.n = int(w);
+    g.e_re = ere;
+    g.e_im = eim;
+    g.e_ld = P.nb_pad;
+    g.e_plane = m * P.nb_pad;
+    for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
+    {
+      StageTimer timer(CRTG_STAGE_GEMM, s, 1);
+      CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
+    }
+    {
+      StageTimer timer(CRTG_STAGE_CRT, s, 1);
+      CRTG_TRY(launch_crt(single, m, w, ere, eim, g.e_plane, g.e_ld, mu, nu + j0, dc,
+                          static_cast<char*>(C) + j0 * csz, ldc, s),
+               "crt");
+    }
+  }
+  if (mu_out) CRTG_TRY(cudaMemcpyAsync(mu_out, mu, 4 * m, cudaMemcpyDeviceToDevice, s), "copy");
+  if (nu_out) CRTG_TRY(cudaMemcpyAsync(nu_out, nu, 4 * n, cudaMemcpyDeviceToDevice, s), "copy");
+  if (sync_check) return check_diag(dg, s);
+  return CRTG_OK;
+}
+
+int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim, const void* X,
+                  int64_t ldx, const int32_t* exps, const crtg_consts* K, int8_t* out, void* ws,
+                  size_t ws_bytes, uint64_t* diag, void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if (rows < 1 || kdim < 1) return fail(CRTG_ERR_DIMENSION, "empty operand");
+  const int64_t r_pad = round_up(rows, 256), k_pad = round_up(kdim, 128);
+  const int64_t plane = r_pad * k_pad;
+  if (ws_bytes < size_t(3 * N) * plane) return fail(CRTG_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const DevConsts dc = make_dev(*K);
+  int8_t* packed = static_cast<int8_t*>(ws);
+  unsigned long long* ovf = reinterpret_cast<unsigned long long*>(diag) +
+                            (operand == 0 ? CRTG_DIAG_OVERFLOW_A : CRTG_DIAG_OVERFLOW_B);
+  CRTG_TRY(launch_pack((precision & CRTG_IN_C64) != 0, operand, PACK_RESIDUE, X, ldx, rows, kdim, 0,
+                       exps, dc, packed, plane, r_pad / 128, ovf, s),
+           "residues");
+  g_launches += uint64_t(1 + 3 * N);
+  for (int q = 0; q < 3 * N; ++q)
+    CRTG_TRY(launch_unpack_i8(packed + q * plane, rows, kdim, r_pad / 128, out + q * rows * kdim, s),
+             "unpack");
+  return CRTG_OK;
+}
+
+size_t crtg_i8_workspace_size(int64_t m, int64_t n, int64_t k, int nplanes) {
+  const int64_t m_pad = round_up(m, 128), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
+  size_t t = 0;
+  t += round_up(size_t(nplanes) * m_pad * k_pad, 256);
+  t += round_up(size_t(nplanes) * n_pad * k_pad, 256);
+  t += round_up(size_t(m) * n_pad * 4, 256);
+  t += round_up(size_t(m) * n_pad * 2, 256);
+  t += round_up(size_t(m_pad) * k_pad + size_t(n_pad) * k_pad, 256);  // Karatsuba sums
+  return t;
+}
+
+int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A, const int8_t* B, int32_t* C,
+                     void* ws, size_t ws_bytes, void* stream) {
+  if (m < 1 || n < 1 || k < 1) return fail(CRTG_ERR_DIMENSION, "m, n, k must be positive");
+  if (k > 131072) return fail(CRTG_ERR_DIMENSION, "inner dimension exceeds 131072");
+  if (ws_bytes < crtg_i8_workspace_size(m, n, k, 1))
+    return fail(CRTG_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t m_pad = round_up(m, 128), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
+  int8_t* ap = static_cast<int8_t*>(ws);
+  int8_t* bp = ap + round_up(m_pad * k_pad, 256);
+  int32_t* raw = reinterpret_cast<int32_t*>(bp + round_up(n_pad * k_pad, 256));
+  g_launches += 3;
+  CRTG_TRY(launch_pack_i8(A, 0, m, k, ap, m_pad / 128, s), "pack A");
+  CRTG_TRY(launch_pack_i8(B, 1, n, k, bp, n_pad / 128, s), "pack B");
+  GemmArgs g{};
+  g.a = ap;
+  g.b = bp;
+  g.a_plane = m_pad * k_pad;
+  g.b_plane = n_pad * k_pad;
+  g.a_rb = int(m_pad / 128);
+  g.b_rb = int(n_pad / 128);
+  g.mt = int(m_pad / 128);
+  g.nt = int(n_pad / 256);
+  g.kb = int(k_pad / 128);
+  g.nl = 1;
+  g.planes_per_l = 1;
+  g.nphase = 1;
+  g.m = int(m);
+  g.n = int(n);
+  g.raw = raw;
+  g.raw_ld = n_pad;
+  g.raw_plane = m * n_pad;
+  CRTG_TRY(launch_gemm(EPI_RAW, g, sm_count(), s), "i8 gemm");
+  CRTG_TRY(cudaMemcpy2DAsync(C, n * 4, raw, n_pad * 4, n * 4, m, cudaMemcpyDeviceToDevice, s),
+           "copy out");
+  return CRTG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void k_mod_sum(const int8_t* __restrict__ x, const int8_t* __restrict__ y, int64_t count,
+                          ModConst mc, int8_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint32_t r = mod_i32(int32_t(x[i]) + int32_t(y[i]), mc);
+  out[i] = int8_t(to_sym(r, mc));
+}
+}  // namespace
+
+extern "C" int crtg_complex_gemm_mod(int64_t m, int64_t n, int64_t k, const int8_t* ar,
+                                     const int8_t* ai, const int8_t* br, const int8_t* bi, int p,
+                                     int8_t* e_re, int8_t* e_im, void* ws, size_t ws_bytes,
+                                     void* stream) {
+  if (m < 1 || n < 1 || k < 1) return fail(CRTG_ERR_DIMENSION, "m, n, k must be positive");
+  if (k > 65536) return fail(CRTG_ERR_DIMENSION, "inner dimension exceeds 65536");
+  if (p < 2 || p > 256) return fail(CRTG_ERR_DOMAIN, "modulus outside [2, 256]");
+  if (ws_bytes < crtg_i8_workspace_size(m, n, k, 3))
+    return fail(CRTG_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t m_pad = round_up(m, 128), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
+  const int64_t a_plane = m_pad * k_pad, b_plane = n_pad * k_pad;
+  int8_t* ap = static_cast<int8_t*>(ws);
+  int8_t* bp = ap + round_up(3 * a_plane, 256);
+  int8_t* eo = bp + round_up(3 * b_plane, 256);  // [2][m][n_pad]
+  int8_t* sums = eo + round_up(m * n_pad * 4, 256);
+  const ModConst mc = make_mod(p);
+  g_launches += 9;
+  // Karatsuba operand sums sa = sym(ar + ai), sb = sym(br + bi)  (kernel.py:101-103)
+  k_mod_sum<<<unsigned((m * k + 255) / 256), 256, 0, s>>>(ar, ai, m * k, mc, sums);
+  k_mod_sum<<<unsigned((k * n + 255) / 256), 256, 0, s>>>(br, bi, k * n, mc, sums + m * k);
+  CRTG_TRY(int(cudaGetLastError()), "mod sum");
+  CRTG_TRY(launch_pack_i8(ar, 0, m, k, ap, m_pad / 128, s), "pack");
+  CRTG_TRY(launch_pack_i8(ai, 0, m, k, ap + a_plane, m_pad / 128, s), "pack");
+  CRTG_TRY(launch_pack_i8(sums, 0, m, k, ap + 2 * a_plane, m_pad / 128, s), "pack");
+  CRTG_TRY(launch_pack_i8(br, 1, n, k, bp, n_pad / 128, s), "pack");
+  CRTG_TRY(launch_pack_i8(bi, 1, n, k, bp + b_plane, n_pad / 128, s), "pack");
+  CRTG_TRY(launch_pack_i8(sums + m * k, 1, n, k, bp + 2 * b_plane, n_pad / 128, s), "pack");
+  GemmArgs g{};
+  g.a = ap;
+  g.b = bp;
+  g.a_plane = a_plane;
+  g.b_plane = b_plane;
+  g.a_rb = int(m_pad / 128);
+  g.b_rb = int(n_pad / 128);
+  g.mt = int(m_pad / 128);
+  g.nt = int(n_pad / 256);
+  g.kb = int(k_pad / 128);
+  g.nl = 1;
+  g.planes_per_l = 3;
+  g.nphase = 3;
+  g.m = int(m);
+  g.n = int(n);
+  g.e_re = eo;
+  g.e_im = eo + m * n_pad;
+  g.e_ld = n_pad;
+  g.e_plane = 0;
+  g.mc[0] = mc;
+  CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
+  CRTG_TRY(cudaMemcpy2DAsync(e_re, n, g.e_re, n_pad, n, m, cudaMemcpyDeviceToDevice, s), "copy");
+  CRTG_TRY(cudaMemcpy2DAsync(e_im, n, g.e_im, n_pad, n, m, cudaMemcpyDeviceToDevice, s), "copy");
+  return CRTG_OK;
+}
+
+extern "C" int crtg_crt_reconstruct(int precision, int64_t m, int64_t n, const int8_t* e_re,
+                                    const int8_t* e_im, const int32_t* mu, const int32_t* nu,
+                                    const crtg_consts* K, void* C, int64_t ldc, void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if (m < 1 || n < 1 || ldc < n) return fail(CRTG_ERR_DIMENSION, "bad shape");
+  const DevConsts dc = make_dev(*K);
+  g_launches += 1;
+  CRTG_TRY(launch_crt((precision & CRTG_SINGLE) != 0, m, n, e_re, e_im, m * n, n, mu, nu, dc, C, ldc,
+                      static_cast<cudaStream_t>(stream)),
+           "crt");
+  return CRTG_OK;
+}
+
+extern "C" uint64_t crtg_launch_count(void) { return g_launches.load(); }
+
+extern "C" int crtg_profile_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+  return CRTG_OK;
+}
+
+extern "C" int crtg_profile_read(double* ms, uint64_t* launches) {
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    recs.swap(g_prof);
+  }
+  for (int i = 0; i < CRTG_STAGE_COUNT; ++i) {
+    if (ms) ms[i] = 0.0;
+    if (launches) launches[i] = 0;
+  }
+  int status = CRTG_OK;
+  for (auto& r : recs) {
+    float t = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess)
+      status = fail(CRTG_ERR_CUDA, "profile event failure");
+    if (r.stage >= 0 && r.stage < CRTG_STAGE_COUNT) {
+      if (ms) ms[r.stage] += t;
+      if (launches) launches[r.stage] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  return status;
+}

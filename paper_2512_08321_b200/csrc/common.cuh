@@ -1,0 +1,204 @@
+// common.cuh — shared device helpers for the sm_100a Ozaki-II / CRT kernels.
+//
+// Operand tile image ("packed") layout used by every producer kernel and read by
+// the tcgen05 GEMM with plain 1-D bulk copies (TMA engine, no tensor map):
+//   one plane  = residue (or bound) matrix of R rows x K bytes, K-major,
+//                R padded to 256, K padded to 128;
+//   block      = 128 rows x 128 K-bytes = 16 KiB, stored as the exact
+//                SWIZZLE_128B shared-memory image UMMA expects
+//                (8-row groups of 1 KiB; 16-byte chunk c of row r lands at chunk
+//                c ^ (r & 7));
+//   block order = [kb][rb] so one 128-byte K step of a 256-row B tile is one
+//                contiguous 32 KiB copy.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/crtg.h"
+
+namespace crtg {
+
+constexpr int kBlockRows = 128;
+constexpr int kBlockK = 128;                    // bytes
+constexpr int kBlockBytes = kBlockRows * kBlockK;  // 16 KiB
+constexpr int kRowPad = 256;                    // rows padded to the GEMM N tile
+
+__host__ __device__ inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// byte offset of element (r, kbyte) inside one packed plane with `rb_count`
+// 128-row blocks.
+__host__ __device__ inline int64_t pack_offset(int64_t r, int64_t kbyte, int64_t rb_count) {
+  const int64_t kb = kbyte >> 7, rb = r >> 7;
+  const int rr = int(r & 127), kin = int(kbyte & 127);
+  return (kb * rb_count + rb) * kBlockBytes + (rr >> 3) * 1024 + (rr & 7) * 128 +
+         ((((kin >> 4) ^ (rr & 7)) << 4) | (kin & 15));
+}
+
+// Per-modulus integer constants for exact residue arithmetic on 32-bit lanes.
+//   mod(u) = u - p * (umulhi(u, magic) >> shift)  exact for u < 2^31 when p is
+//   not a power of two (shift = floor(log2 p), magic = ceil(2^(32+shift)/p));
+//   p == 256 uses a mask.
+struct ModConst {
+  int32_t p;
+  uint32_t magic;
+  int32_t shift;
+  int32_t half;      // (p + 1) / 2 : symmetric residue r >= half -> r - p
+  uint32_t c16;      // 2^16 mod p
+  uint32_t c32;      // 2^32 mod p
+  int32_t bias;      // p * ceil(2^30 / p): makes |x| <= 2^30 non-negative
+  int32_t is_pow2;
+};
+
+struct DevConsts {
+  int32_t n;
+  ModConst mc[CRTG_MAX_MODULI];
+  uint16_t pow2mod[CRTG_MAX_MODULI][40];  // 2^s mod p, s < 40 (wide residues)
+  double coeff_hi[CRTG_MAX_MODULI];
+  double coeff_lo[CRTG_MAX_MODULI];
+  double p_hi, p_lo;
+  float p_fast, p_accu, delta;
+};
+
+__device__ __forceinline__ uint32_t mod_u31(uint32_t u, const ModConst& c) {
+  if (c.is_pow2) return u & uint32_t(c.p - 1);
+  const uint32_t q = __umulhi(u, c.magic) >> c.shift;
+  return u - q * uint32_t(c.p);
+}
+
+// residue in [0,p) of a signed 32-bit value with |x| <= 2^30
+__device__ __forceinline__ uint32_t mod_i32(int32_t x, const ModConst& c) {
+  if (c.is_pow2) return uint32_t(x) & uint32_t(c.p - 1);
+  return mod_u31(uint32_t(x + c.bias), c);
+}
+
+// symmetric representative of r in [0,p): [-floor(p/2), ceil(p/2)-1]
+__device__ __forceinline__ int32_t to_sym(uint32_t r, const ModConst& c) {
+  return int32_t(r) - (int32_t(r) >= c.half ? c.p : 0);
+}
+
+// np.ldexp(x, e): x * 2^e with a single rounding (CUDA's ldexp is exact /
+// correctly rounded, 0 ulp, like glibc scalbn).  When 2^e is representable a
+// single multiply gives the identical correctly-rounded result.
+__device__ __forceinline__ double ldexp_rn(double x, int e) {
+  if (e >= -1022 && e <= 1023) return __dmul_rn(x, __longlong_as_double(int64_t(e + 1023) << 52));
+  return ldexp(x, e);
+}
+
+// floor(log2|x|) of a positive finite double (frexp exponent - 1), subnormals too
+__device__ __forceinline__ int floor_log2(double x) { return ilogb(x); }
+
+// ---------------------------------------------------------------------------
+// PTX wrappers (mbarrier, bulk copy, tcgen05)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// 1-D bulk copy global -> shared, completion counted on an mbarrier (TMA engine)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+template <int kCols>
+__device__ __forceinline__ void tmem_alloc(uint32_t dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst_smem),
+               "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+
+template <int kCols>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+               : "memory");
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, s8 x s8 -> s32
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+
+// 32 lanes x 32 consecutive 32-bit columns: thread t of the warp gets row
+// (lane base + t), columns [col, col+32).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row groups 1 KiB apart.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t(1024 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+
+// Instruction descriptor: kind::i8, s8 x s8 -> s32, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+}  // namespace crtg

@@ -1,0 +1,343 @@
+// gemm_tc.cu — K3: INT8 residue GEMMs on 5th-gen tensor cores (tcgen05, sm_100a).
+//
+// Replaces the per-modulus loop of emulate_gemm_complex (reference
+// emulate.py:224-231) -> complex_gemm_mod (kernel.py:70-120) -> _karatsuba_block
+// (kernel.py:45-51) -> gemm_i8_i32 (kernel.py:20-35), and the bound product of
+// accurate_scaling (scaling.py:249-258).
+//
+// One persistent, warp-specialised kernel:
+//   warp 0 (lane 0)  producer: 1-D bulk copies (TMA engine) of pre-packed,
+//                    pre-swizzled 128x128-byte operand blocks into a 4-stage ring;
+//   warp 1 (lane 0)  MMA issuer: tcgen05.mma.kind::i8, M=128 N=256 K=32, s32
+//                    accumulators in TMEM (2 x 256 columns, double-buffered);
+//   warp 2           TMEM allocator;
+//   warps 4..7       epilogue: tcgen05.ld -> registers -> modular epilogue.
+// A tile (l, tm, tn) runs one "segment" per operand pair:
+//   EPI_KARATSUBA: D = Ar*Br, E = Ai*Bi, F = As*Bs (three sequential K loops into
+//     alternating TMEM buffers).  The epilogue keeps D mod p, then (D+E) mod p, as
+//     packed bytes in registers, and writes e_R = sym(D-E) and e_I = sym(F-D-E)
+//     as int8 — INT32 products never leave the SM.
+//   EPI_RAW: writes the int32 accumulators (parity hook for gemm_i8_i32).
+//   EPI_BOUND: cross = AI*BR + AR*BI (buffer 0) and diff = AD*BD (buffer 1);
+//     bound = max(cross+diff, cross); row / column maxima by atomicMax.
+#include <cstdio>
+
+#include "common.cuh"
+#include "gemm_tc.cuh"
+
+namespace crtg {
+
+namespace {
+
+constexpr uint32_t kStageA = 16384;  // 128 rows x 128 B
+constexpr uint32_t kStageB = 32768;  // 256 rows x 128 B
+constexpr uint32_t kStageBytes = kStageA + kStageB;
+constexpr int kStages = 4;
+constexpr int kTmemCols = 512;
+constexpr int kGroupM = 16;  // rasterisation: 16 row tiles share each column sweep
+
+struct Seg {
+  int a_plane, b_plane, buf, accumulate;
+};
+
+template <int MODE>
+__device__ __forceinline__ int num_segs(const GemmArgs& g) {
+  return MODE == EPI_BOUND ? 3 : g.nphase;
+}
+
+template <int MODE>
+__device__ __forceinline__ Seg seg_of(int s) {
+  if (MODE == EPI_BOUND) {
+    // cross = AI*BR + AR*BI -> buffer 0; diff = AD*BD -> buffer 1 (scaling.py:251-256)
+    if (s == 0) return {1, 0, 0, 0};
+    if (s == 1) return {0, 1, 0, 1};
+    return {2, 2, 1, 0};
+  }
+  return {s, s, -1, 0};
+}
+
+__device__ __forceinline__ void decode_tile(int t, const GemmArgs& g, int& l, int& tm, int& tn) {
+  const int per = g.mt * g.nt;
+  l = t / per;
+  const int r = t - l * per;
+  const int grp = r / (kGroupM * g.nt);
+  const int first = grp * kGroupM;
+  const int gm = min(kGroupM, g.mt - first);
+  const int in = r - grp * kGroupM * g.nt;
+  tm = first + in % gm;
+  tn = in / gm;
+}
+
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return (a & 0xFF) | ((b & 0xFF) << 8) | ((c & 0xFF) << 16) | (d << 24);
+}
+
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int i) { return (w >> (8 * i)) & 0xFF; }
+
+}  // namespace
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) k_gemm_i8(const __grid_constant__ GemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2];
+  __shared__ __align__(8) uint64_t tempty_bar[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  // 1024-byte aligned operand ring (SWIZZLE_128B atoms)
+  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull_bar[b]), 1);
+      mbar_init(smem_u32(&tempty_bar[b]), 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(&tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  const int total = g.nl * g.mt * g.nt;
+  const int nseg = num_segs<MODE>(g);
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer ----------------
+    uint32_t stage = 0, phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int l, tm, tn;
+      decode_tile(t, g, l, tm, tn);
+      for (int s = 0; s < nseg; ++s) {
+        const Seg sg = seg_of<MODE>(s);
+        const int8_t* a = g.a + (int64_t)(l * g.planes_per_l + sg.a_plane) * g.a_plane;
+        const int8_t* b = g.b + (int64_t)(l * g.planes_per_l + sg.b_plane) * g.b_plane;
+        for (int kb = 0; kb < g.kb; ++kb) {
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full_bar[stage]);
+          const uint32_t sa = smem_base + stage * kStageBytes;
+          mbar_expect_tx(fb, kStageBytes);
+          bulk_g2s(sa, a + ((int64_t)kb * g.a_rb + tm) * kBlockBytes, kStageA, fb);
+          bulk_g2s(sa + kStageA, b + ((int64_t)kb * g.b_rb + 2 * tn) * kBlockBytes, kStageB, fb);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_i8(128, 256);
+    uint32_t stage = 0, phase = 0, gslot = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      if (MODE == EPI_BOUND) {
+        const uint32_t par = ((gslot >> 1) & 1) ^ 1;
+        mbar_wait(smem_u32(&tempty_bar[0]), par);
+        mbar_wait(smem_u32(&tempty_bar[1]), par);
+        tc_fence_after();
+      }
+      for (int s = 0; s < nseg; ++s) {
+        const Seg sg = seg_of<MODE>(s);
+        uint32_t buf;
+        if (MODE == EPI_BOUND) {
+          buf = sg.buf;
+        } else {
+          buf = gslot & 1;
+          mbar_wait(smem_u32(&tempty_bar[buf]), ((gslot >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
+        const uint32_t d = tmem + buf * 256;
+        for (int kb = 0; kb < g.kb; ++kb) {
+          mbar_wait(smem_u32(&full_bar[stage]), phase);
+          tc_fence_after();
+          const uint32_t sa = smem_base + stage * kStageBytes;
+          const uint64_t ad = smem_desc_sw128(sa);
+          const uint64_t bd = smem_desc_sw128(sa + kStageA);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            // advance 32 bytes of K inside the 128-byte swizzle atom
+            mma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk | sg.accumulate) != 0);
+          }
+          mma_commit(smem_u32(&empty_bar[stage]));  // frees the smem slot when MMAs finish
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        if (MODE == EPI_BOUND) {
+          if (s == 1) mma_commit(smem_u32(&tfull_bar[0]));
+          if (s == 2) mma_commit(smem_u32(&tfull_bar[1]));
+        } else {
+          mma_commit(smem_u32(&tfull_bar[buf]));
+          ++gslot;
+        }
+      }
+      if (MODE == EPI_BOUND) gslot += 2;
+    }
+  } else if (warp >= 4) {
+    // ---------------- epilogue (128 threads, one TMEM lane each) ----------------
+    const int q = warp & 3;
+    const uint32_t lane_addr = tmem + (uint32_t(32 * q) << 16);
+    uint32_t gslot = 0;
+    uint32_t st[64];  // packed per-column state across the three Karatsuba phases
+#pragma unroll
+    for (int i = 0; i < 64; ++i) st[i] = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int l, tm, tn;
+      decode_tile(t, g, l, tm, tn);
+      const int row = tm * 128 + 32 * q + lane;
+      const bool row_ok = row < g.m;
+      const int col_base = tn * 256;
+      if (MODE == EPI_BOUND) {
+        const uint32_t par = (gslot >> 1) & 1;
+        mbar_wait(smem_u32(&tfull_bar[0]), par);
+        mbar_wait(smem_u32(&tfull_bar[1]), par);
+        tc_fence_after();
+        int32_t rmax = 0;
+#pragma unroll 1
+        for (int c = 0; c < 8; ++c) {
+          uint32_t cr[32], df[32];
+          tmem_ld32(lane_addr + c * 32, cr);
+          tmem_ld32(lane_addr + 256 + c * 32, df);
+          tmem_wait_ld();
+          int32_t mine = 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int32_t cross = int32_t(cr[i]);
+            const int32_t bnd = max(cross + int32_t(df[i]), cross);
+            rmax = max(rmax, bnd);
+            const int32_t cm = __reduce_max_sync(0xffffffffu, bnd);
+            if (lane == i) mine = cm;
+          }
+          atomicMax(g.col_max + col_base + c * 32 + lane, mine);
+        }
+        if (row_ok) atomicMax(g.row_max + row, rmax);
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty_bar[0]));
+        mbar_arrive(smem_u32(&tempty_bar[1]));
+        gslot += 2;
+        continue;
+      }
+      const ModConst mc = g.mc[l];
+      for (int s = 0; s < nseg; ++s) {
+        const uint32_t buf = gslot & 1;
+        mbar_wait(smem_u32(&tfull_bar[buf]), (gslot >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = lane_addr + buf * 256;
+        if (MODE == EPI_RAW) {
+#pragma unroll 1
+          for (int c = 0; c < 8; ++c) {
+            uint32_t v[32];
+            tmem_ld32(taddr + c * 32, v);
+            tmem_wait_ld();
+            if (row_ok) {
+              int32_t* dst = g.raw + (int64_t)s * g.raw_plane + (int64_t)row * g.raw_ld +
+                             col_base + c * 32;
+#pragma unroll
+              for (int w = 0; w < 8; ++w)
+                reinterpret_cast<uint4*>(dst)[w] =
+                    make_uint4(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]);
+            }
+          }
+        } else {
+          // EPI_KARATSUBA
+          int8_t* dst_base = nullptr;
+          if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+          if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint32_t v[32];
+            tmem_ld32(taddr + c * 32, v);
+            tmem_wait_ld();
+            uint32_t out[8];
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+              uint32_t r[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) r[j] = mod_i32(int32_t(v[4 * w + j]), mc);
+              if (s == 0) {
+                st[c * 8 + w] = pack4(r[0], r[1], r[2], r[3]);
+              } else if (s == 1) {
+                // e_R = sym(D - E); keep (D + E) mod p for the imaginary part
+                uint32_t o[4], keep[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  const int32_t dm = int32_t(byte_of(st[c * 8 + w], j));
+                  int32_t x = dm - int32_t(r[j]);
+                  x += (x < 0) ? mc.p : 0;
+                  o[j] = uint32_t(to_sym(uint32_t(x), mc));
+                  int32_t y = dm + int32_t(r[j]);
+                  y -= (y >= mc.p) ? mc.p : 0;
+                  keep[j] = uint32_t(y);
+                }
+                out[w] = pack4(o[0], o[1], o[2], o[3] & 0xFF);
+                st[c * 8 + w] = pack4(keep[0], keep[1], keep[2], keep[3]);
+              } else {
+                // e_I = sym(F - (D + E))
+                uint32_t o[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  int32_t x = int32_t(r[j]) - int32_t(byte_of(st[c * 8 + w], j));
+                  x += (x < 0) ? mc.p : 0;
+                  o[j] = uint32_t(to_sym(uint32_t(x), mc));
+                }
+                out[w] = pack4(o[0], o[1], o[2], o[3] & 0xFF);
+              }
+            }
+            if (s != 0 && row_ok) {
+              uint4* d4 = reinterpret_cast<uint4*>(dst_base + c * 32);
+              d4[0] = make_uint4(out[0], out[1], out[2], out[3]);
+              d4[1] = make_uint4(out[4], out[5], out[6], out[7]);
+            }
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty_bar[buf]));
+        ++gslot;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
+size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + 1024; }
+
+int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {
+  const int total = g.nl * g.mt * g.nt;
+  if (total <= 0) return 0;
+  const int grid = total < num_sms ? total : num_sms;
+  const size_t smem = gemm_smem_bytes();
+  cudaError_t err;
+  switch (mode) {
+    case EPI_KARATSUBA:
+      err = cudaFuncSetAttribute(k_gemm_i8<EPI_KARATSUBA>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (err != cudaSuccess) return int(err);
+      k_gemm_i8<EPI_KARATSUBA><<<grid, 256, smem, stream>>>(g);
+      break;
+    case EPI_RAW:
+      err = cudaFuncSetAttribute(k_gemm_i8<EPI_RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem));
+      if (err != cudaSuccess) return int(err);
+      k_gemm_i8<EPI_RAW><<<grid, 256, smem, stream>>>(g);
+      break;
+    default:
+      err = cudaFuncSetAttribute(k_gemm_i8<EPI_BOUND>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (err != cudaSuccess) return int(err);
+      k_gemm_i8<EPI_BOUND><<<grid, 256, smem, stream>>>(g);
+      break;
+  }
+  return int(cudaGetLastError());
+}
+
+}  // namespace crtg

@@ -1,0 +1,398 @@
+"""Drop-in complex GEMM emulation on B200 (reference emulate.py:193-278).
+
+`emulate_gemm_complex(a, b, cfg=None, diagnostics=None)` and the BLAS-style
+`gemm(...)` keep the reference's names, arguments, defaults, error classes and
+results (bit-for-bit, see tests/).  Everything below the argument checks runs in
+libcrtg.so on the GPU (include/crtg.h); there is no CPU path.
+
+Inputs may be numpy arrays (copied to the device, result returned as numpy —
+the reference's behaviour) or torch tensors (CUDA or CPU; if both inputs are
+torch tensors the result is a torch CUDA tensor on the same device).
+
+Lower-level GPU parity hooks mirror the reference's stage functions:
+`gemm_i8_i32` (kernel.py:20-35), `complex_gemm_mod` (kernel.py:70-120),
+`fast_scaling` / `accurate_scaling` (scaling.py:198-274), `quantized_residues`
+(quantize + residue_decompose, scaling.py:277-293 + crt.py:199-218) and
+`crt_reconstruct` (crt.py:221-258 + emulate.py:135-144).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .config import MAX_K_COMPLEX, MAX_K_REAL, STRATEGIES, EmuConfig
+from .errors import ConfigError, DimensionError, DomainError
+from .moduli import ModulusSet, ScalingConstants, device_constants, select_moduli
+
+__all__ = [
+    "ScalingVectors", "emulate_gemm_complex", "gemm", "gemm_i8_i32", "complex_gemm_mod",
+    "fast_scaling", "accurate_scaling", "quantized_residues", "crt_reconstruct",
+]
+
+
+@dataclass
+class ScalingVectors:
+    """mu = 2^mu_exp per row of A, nu = 2^nu_exp per column of B
+    (reference scaling.py:118-127)."""
+
+    mu_exp: np.ndarray
+    nu_exp: np.ndarray
+    bar_mu_exp: np.ndarray | None = None
+    bar_nu_exp: np.ndarray | None = None
+
+
+# ----------------------------------------------------------------------------
+# device plumbing
+# ----------------------------------------------------------------------------
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise nat.NativeError("no CUDA device: the B200 emulation has no CPU path")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    nat.check_device(dev.index)
+    return dev
+
+
+def _stream_ptr(dev) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _to_device_matrix(x, name: str, dev, complex_out: bool = True):
+    """-> (contiguous CUDA tensor, was_torch).  Mirrors _check_complex_input
+    (emulate.py:159-166): 2-D, cast to complex (complex64 kept, upcast exactly
+    on the device)."""
+    if isinstance(x, torch.Tensor):
+        t = x
+        if t.dim() != 2:
+            raise DimensionError(f"{name} must be 2-D")
+        if complex_out and not t.is_complex():
+            t = t.to(torch.complex128)
+        if complex_out and t.dtype not in (torch.complex64, torch.complex128):
+            t = t.to(torch.complex128)
+        return t.to(dev).contiguous(), True
+    arr = np.asarray(x)
+    if arr.ndim != 2:
+        raise DimensionError(f"{name} must be 2-D")
+    if complex_out and arr.dtype not in (np.complex64, np.complex128):
+        arr = arr.astype(np.complex128)
+    arr = np.ascontiguousarray(arr)
+    t = torch.from_numpy(arr)
+    if t.numel() * t.element_size() >= (1 << 20):
+        t = t.pin_memory()
+    return t.to(dev, non_blocking=True), False
+
+
+def _workspace(nbytes: int, dev) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+
+
+# ----------------------------------------------------------------------------
+# the hot path
+# ----------------------------------------------------------------------------
+def emulate_gemm_complex(a, b, cfg: EmuConfig | None = None,
+                         diagnostics: dict | None = None):
+    """Emulated complex matrix product A @ B (reference emulate.py:193-240)."""
+    cfg = cfg or EmuConfig(domain="complex")
+    if cfg.domain != "complex":
+        raise ConfigError("config domain must be 'complex'")
+    dev = _device()
+    at, a_torch = _to_device_matrix(a, "A", dev)
+    bt, b_torch = _to_device_matrix(b, "B", dev)
+    if at.shape[1] != bt.shape[0]:
+        raise DimensionError(f"inner dimensions differ: {tuple(at.shape)} x {tuple(bt.shape)}")
+    m, k = at.shape
+    n = bt.shape[1]
+    if k > MAX_K_COMPLEX:
+        raise DimensionError(f"inner dimension {k} exceeds {MAX_K_COMPLEX}")
+    out = run_complex(at, bt, cfg, diagnostics, dev)
+    if a_torch and b_torch:
+        return out
+    return out.cpu().numpy()
+
+
+def run_complex(at: torch.Tensor, bt: torch.Tensor, cfg: EmuConfig,
+                diagnostics: dict | None = None, dev=None, sync_check: bool = True,
+                ws: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                return_exponents: bool = False):
+    """Device-resident entry: contiguous CUDA complex tensors in, CUDA tensor out.
+    Used by the public API, the benchmark and the multi-GPU driver."""
+    dev = dev or at.device
+    if at.dtype != bt.dtype:  # mixed precision inputs: upcast the narrower one
+        at, bt = at.to(torch.complex128), bt.to(torch.complex128)
+    m, k = at.shape
+    n = bt.shape[1]
+    nmod = cfg.resolved_moduli
+    consts = device_constants(nmod)
+    prec = nat.SINGLE if cfg.precision == "single" else nat.DOUBLE
+    if at.dtype == torch.complex64:
+        prec |= 16  # CRTG_IN_C64
+    mode = nat.FAST if cfg.mode == "fast" else nat.ACCURATE
+    lib = nat.load()
+    need = lib.crtg_workspace_size(prec, mode, m, n, k, nmod, cfg.n_block)
+    if ws is None or ws.numel() < need:
+        ws = _workspace(need, dev)
+    odt = torch.complex64 if cfg.precision == "single" else torch.complex128
+    if out is None:
+        out = torch.empty((m, n), dtype=odt, device=dev)
+    diag = torch.zeros(nat.DIAG_LEN, dtype=torch.int64, device=dev)
+    mu = torch.empty(m, dtype=torch.int32, device=dev) if return_exponents else None
+    nu = torch.empty(n, dtype=torch.int32, device=dev) if return_exponents else None
+    nat.call("crtg_gemm_complex", prec, mode, m, n, k, at.data_ptr(), at.stride(0),
+             bt.data_ptr(), bt.stride(0), out.data_ptr(), out.stride(0),
+             ctypes.byref(consts), cfg.n_block, ws.data_ptr(), ws.numel(),
+             mu.data_ptr() if mu is not None else None,
+             nu.data_ptr() if nu is not None else None,
+             diag.data_ptr(), 1 if sync_check else 0, _stream_ptr(dev))
+    if diagnostics is not None:
+        d = diag.cpu().tolist()
+        for key, idx in (("clamped_mu", nat.DIAG_CLAMPED_MU), ("clamped_nu", nat.DIAG_CLAMPED_NU)):
+            if d[idx]:
+                diagnostics[key] = diagnostics.get(key, 0) + int(d[idx])
+    if return_exponents:
+        return out, mu, nu
+    return out
+
+
+def _colmajor_view(buf, ld, rows, cols, name):
+    """Column-major view with leading dimension (reference emulate.py:243-253)."""
+    if isinstance(buf, torch.Tensor):
+        if buf.dim() == 1:
+            if buf.numel() < ld * cols:
+                raise DimensionError(f"{name} buffer too small for ld={ld}")
+            return buf.as_strided((rows, cols), (1, ld))
+        if buf.dim() == 2:
+            if buf.shape[0] < rows or buf.shape[1] < cols:
+                raise DimensionError(f"{name} array smaller than {rows}x{cols}")
+            return buf[:rows, :cols]
+        raise DimensionError(f"{name} must be 1-D storage or a 2-D array")
+    arr = np.asarray(buf)
+    if arr.ndim == 1:
+        if arr.size < ld * cols:
+            raise DimensionError(f"{name} buffer too small for ld={ld}")
+        return arr[:ld * cols].reshape((ld, cols), order="F")[:rows, :]
+    if arr.ndim == 2:
+        if arr.shape[0] < rows or arr.shape[1] < cols:
+            raise DimensionError(f"{name} array smaller than {rows}x{cols}")
+        return arr[:rows, :cols]
+    raise DimensionError(f"{name} must be 1-D storage or a 2-D array")
+
+
+def gemm(domain: str, precision: str, m: int, n: int, k: int, a, lda: int, b, ldb: int,
+         c, ldc: int, cfg: EmuConfig | None = None):
+    """GEMM-style entry on column-major buffers with leading dimensions; writes
+    the product into ``c`` and returns it (reference emulate.py:256-278)."""
+    if cfg is None:
+        cfg = EmuConfig(precision=precision, domain=domain)
+    if cfg.precision != precision or cfg.domain != domain:
+        raise ConfigError("cfg disagrees with the requested domain/precision")
+    av = _colmajor_view(a, lda, m, k, "A")
+    bv = _colmajor_view(b, ldb, k, n, "B")
+    cv = _colmajor_view(c, ldc, m, n, "C")
+    if domain == "real":
+        raise ConfigError("real-domain emulation is outside this build's hot path "
+                          "(emulate_gemm_real); use domain='complex'")
+    result = emulate_gemm_complex(av, bv, cfg)
+    if isinstance(cv, torch.Tensor):
+        cv.copy_(torch.as_tensor(result).to(cv.device, cv.dtype))
+    else:
+        cv[...] = result
+    return c
+
+
+# ----------------------------------------------------------------------------
+# stage-level parity hooks
+# ----------------------------------------------------------------------------
+def _i8_device(x, name, dev):
+    if isinstance(x, torch.Tensor):
+        if x.dim() != 2:
+            raise DimensionError("operands must be 2-D")
+        if x.dtype != torch.int8:
+            raise DimensionError("operands must be int8")
+        return x.to(dev).contiguous(), True
+    arr = np.asarray(x)
+    if arr.ndim != 2:
+        raise DimensionError("operands must be 2-D")
+    if arr.dtype != np.int8:
+        raise DimensionError("operands must be int8")
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(dev), False
+
+
+def _gemm_i8_raw(at, bt, dev):
+    m, k = at.shape
+    n = bt.shape[1]
+    lib = nat.load()
+    ws = _workspace(lib.crtg_i8_workspace_size(m, n, k, 1), dev)
+    c = torch.empty((m, n), dtype=torch.int32, device=dev)
+    nat.call("crtg_gemm_i8_i32", m, n, k, at.data_ptr(), bt.data_ptr(), c.data_ptr(),
+             ws.data_ptr(), ws.numel(), _stream_ptr(dev))
+    return c
+
+
+def gemm_i8_i32(a, b):
+    """Exact int8 x int8 -> int32 product on tcgen05 (reference kernel.py:20-35)."""
+    dev = _device()
+    at, ta = _i8_device(a, "A", dev)
+    bt, tb = _i8_device(b, "B", dev)
+    if at.shape[1] != bt.shape[0]:
+        raise DimensionError(f"inner dimensions differ: {tuple(at.shape)} x {tuple(bt.shape)}")
+    k = at.shape[1]
+    if k > MAX_K_REAL:
+        raise DimensionError(f"inner dimension {k} exceeds {MAX_K_REAL}")
+    if k <= MAX_K_COMPLEX:
+        c = _gemm_i8_raw(at, bt, dev)
+    else:
+        # |partial| <= 2^30 per half; the reference raises beyond int32 (kernel.py:33-34)
+        h = MAX_K_COMPLEX
+        c64 = (_gemm_i8_raw(at[:, :h].contiguous(), bt[:h].contiguous(), dev).to(torch.int64)
+               + _gemm_i8_raw(at[:, h:].contiguous(), bt[h:].contiguous(), dev))
+        if c64.numel() and int(c64.abs().max()) > 2 ** 31 - 1:
+            raise ArithmeticError("dot product exceeds the 32-bit accumulator")
+        c = c64.to(torch.int32)
+    return c if (ta and tb) else c.cpu().numpy()
+
+
+def _residue_bounds(p):
+    lo = -(p // 2) if p % 2 == 0 else -((p - 1) // 2)
+    return lo, (p - 1) // 2
+
+
+def complex_gemm_mod(ar, ai, br, bi, p: int, strategy: str = "karatsuba",
+                     n_block: int = 8192):
+    """Modular complex product on residue operands (reference kernel.py:70-120).
+    All strategies are bitwise identical; the GPU runs the Karatsuba form."""
+    if strategy not in STRATEGIES:
+        raise DimensionError(f"unknown strategy {strategy!r}")
+    if n_block < 1:
+        raise DimensionError("n_block must be >= 1")
+    dev = _device()
+    ops = [_i8_device(np.asarray(x, dtype=np.int8) if not isinstance(x, torch.Tensor) else x,
+                      nm, dev) for x, nm in ((ar, "ar"), (ai, "ai"), (br, "br"), (bi, "bi"))]
+    (art, t0), (ait, _), (brt, _), (bit, _) = ops
+    if art.shape != ait.shape or brt.shape != bit.shape:
+        raise DimensionError("real/imaginary parts must share shapes")
+    if art.shape[1] != brt.shape[0]:
+        raise DimensionError(f"inner dimensions differ: {tuple(art.shape)} x {tuple(brt.shape)}")
+    m, k = art.shape
+    n = brt.shape[1]
+    if k > MAX_K_COMPLEX:
+        raise DimensionError(f"inner dimension {k} exceeds {MAX_K_COMPLEX} "
+                             "for complex modular products")
+    lo, hi = _residue_bounds(p)
+    for name, t in (("ar", art), ("ai", ait), ("br", brt), ("bi", bit)):
+        if t.numel() and (int(t.min()) < lo or int(t.max()) > hi):
+            raise DimensionError(f"{name} entries outside residue range of p={p}")
+    lib = nat.load()
+    ws = _workspace(lib.crtg_i8_workspace_size(m, n, k, 3), dev)
+    er = torch.empty((m, n), dtype=torch.int8, device=dev)
+    ei = torch.empty((m, n), dtype=torch.int8, device=dev)
+    nat.call("crtg_complex_gemm_mod", m, n, k, art.data_ptr(), ait.data_ptr(), brt.data_ptr(),
+             bit.data_ptr(), int(p), er.data_ptr(), ei.data_ptr(), ws.data_ptr(), ws.numel(),
+             _stream_ptr(dev))
+    if all(isinstance(x, torch.Tensor) for x in (ar, ai, br, bi)):
+        return er, ei
+    return er.cpu().numpy(), ei.cpu().numpy()
+
+
+def _scaling(a, b, ms: ModulusSet, mode: int, diagnostics):
+    dev = _device()
+    at, _ = _to_device_matrix(a, "A", dev)
+    bt, _ = _to_device_matrix(b, "B", dev)
+    if at.dtype != bt.dtype:
+        at, bt = at.to(torch.complex128), bt.to(torch.complex128)
+    if at.shape[1] != bt.shape[0]:
+        raise DimensionError("inner dimensions differ")
+    m, k = at.shape
+    n = bt.shape[1]
+    if mode == nat.ACCURATE and k > MAX_K_COMPLEX:
+        raise DimensionError(f"inner dimension {k} exceeds {MAX_K_COMPLEX} for the bound product")
+    consts = device_constants(len(ms))
+    prec = 16 if at.dtype == torch.complex64 else 0
+    lib = nat.load()
+    ws = _workspace(lib.crtg_workspace_size(prec, mode, m, n, k, len(ms), n), dev)
+    mu = torch.empty(m, dtype=torch.int32, device=dev)
+    nu = torch.empty(n, dtype=torch.int32, device=dev)
+    diag = torch.zeros(nat.DIAG_LEN, dtype=torch.int64, device=dev)
+    nat.call("crtg_scaling", prec, mode, m, n, k, at.data_ptr(), at.stride(0), bt.data_ptr(),
+             bt.stride(0), ctypes.byref(consts), ws.data_ptr(), ws.numel(), mu.data_ptr(),
+             nu.data_ptr(), diag.data_ptr(), _stream_ptr(dev))
+    d = diag.cpu().tolist()
+    if d[2] or d[3]:
+        raise DomainError("matrix entries must be finite")
+    if diagnostics is not None:
+        for key, idx in (("clamped_mu", 0), ("clamped_nu", 1)):
+            if d[idx]:
+                diagnostics[key] = diagnostics.get(key, 0) + int(d[idx])
+    return ScalingVectors(mu.cpu().numpy().astype(np.int64), nu.cpu().numpy().astype(np.int64))
+
+
+def fast_scaling(a, b, ms: ModulusSet, sc: ScalingConstants | None = None,
+                 diagnostics: dict | None = None) -> ScalingVectors:
+    """Cauchy-Schwarz exponents on the GPU (reference scaling.py:198-213).
+    Complex (or real, treated with a zero imaginary part) operands."""
+    return _scaling(a, b, ms, nat.FAST, diagnostics)
+
+
+def accurate_scaling(a, b, ms: ModulusSet, sc: ScalingConstants | None = None,
+                     diagnostics: dict | None = None) -> ScalingVectors:
+    """Bound-GEMM exponents on the GPU (reference scaling.py:229-274)."""
+    return _scaling(a, b, ms, nat.ACCURATE, diagnostics)
+
+
+def quantized_residues(mat, exps, ms: ModulusSet, axis: int = 0):
+    """trunc(mat * 2^exps) reduced to symmetric residues for every modulus:
+    int8 array (N, 3, rows, cols) with planes (re, im, sym(re+im)).  axis=0:
+    exps per row (left operand); axis=1: exps per column (right operand).
+    (reference quantize scaling.py:277-293 + residue_decompose crt.py:199-218 +
+    the Karatsuba sums kernel.py:101-103)."""
+    dev = _device()
+    xt, was_t = _to_device_matrix(mat, "matrix", dev)
+    exps_np = np.asarray(exps, dtype=np.int64)
+    if axis not in (0, 1):
+        raise ConfigError("axis must be 0 (rows) or 1 (columns)")
+    if exps_np.shape[0] != xt.shape[axis]:
+        raise DimensionError("exponent vector does not match matrix")
+    et = torch.from_numpy(np.clip(exps_np, -2 ** 31, 2 ** 31 - 1).astype(np.int32)).to(dev)
+    rows, kdim = (xt.shape[0], xt.shape[1]) if axis == 0 else (xt.shape[1], xt.shape[0])
+    consts = device_constants(len(ms))
+    nmod = len(ms)
+    r_pad = -(-rows // 256) * 256
+    k_pad = -(-kdim // 128) * 128
+    ws = _workspace(3 * nmod * r_pad * k_pad, dev)
+    out = torch.empty((nmod, 3, rows, kdim), dtype=torch.int8, device=dev)
+    diag = torch.zeros(nat.DIAG_LEN, dtype=torch.int64, device=dev)
+    prec = 16 if xt.dtype == torch.complex64 else 0
+    nat.call("crtg_residues", prec, axis, rows, kdim, xt.data_ptr(), xt.stride(0), et.data_ptr(),
+             ctypes.byref(consts), out.data_ptr(), ws.data_ptr(), ws.numel(), diag.data_ptr(),
+             _stream_ptr(dev))
+    d = diag.cpu().tolist()
+    if d[4] or d[5]:
+        raise DomainError("scaled magnitudes exceed the quantization budget")
+    if axis == 1:
+        out = out.transpose(2, 3)  # back to (k, n) orientation
+    return out if was_t else out.cpu().numpy()
+
+
+def crt_reconstruct(e_re, e_im, mu, nu, ms: ModulusSet, precision: str = "double"):
+    """CRT accumulate + reduce + inverse scaling of residue stacks (N, m, n)
+    (reference crt.py:221-258 + emulate.py:135-144, 234-240)."""
+    dev = _device()
+    ert = torch.as_tensor(np.asarray(e_re, np.int8) if not isinstance(e_re, torch.Tensor)
+                          else e_re).to(dev).contiguous()
+    eit = torch.as_tensor(np.asarray(e_im, np.int8) if not isinstance(e_im, torch.Tensor)
+                          else e_im).to(dev).contiguous()
+    nmod, m, n = ert.shape
+    if nmod != len(ms):
+        raise ConfigError("stack depth does not match modulus count")
+    mut = torch.as_tensor(np.asarray(mu, np.int64).astype(np.int32)).to(dev)
+    nut = torch.as_tensor(np.asarray(nu, np.int64).astype(np.int32)).to(dev)
+    odt = torch.complex64 if precision == "single" else torch.complex128
+    out = torch.empty((m, n), dtype=odt, device=dev)
+    nat.call("crtg_crt_reconstruct", nat.SINGLE if precision == "single" else nat.DOUBLE, m, n,
+             ert.data_ptr(), eit.data_ptr(), mut.data_ptr(), nut.data_ptr(),
+             ctypes.byref(device_constants(len(ms))), out.data_ptr(), out.stride(0),
+             _stream_ptr(dev))
+    return out.cpu().numpy()

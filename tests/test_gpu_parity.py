@@ -1,0 +1,298 @@
+"""GPU parity: every stage of the CUDA path against the reference's golden vectors
+and the CPU oracle (bit-exact; integer stages and final results alike).
+
+All tests here need a B200 and the built libcrtg.so (marker `gpu`)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from oracle import ozaki2 as orc
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def crt():
+    import paper_2512_08321_b200 as crt
+    from paper_2512_08321_b200 import _native
+    _native.load()
+    return crt
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _cases(golden):
+    return sorted({k.split("__")[0] for k in golden.files if k.endswith("__meta")})
+
+
+def _case_inputs(golden, tag):
+    g = lambda s: golden[f"{tag}__{s}"]  # noqa: E731
+    m, n, k, seed, N, dbl, fast = g("meta").tolist()
+    prec = "double" if dbl else "single"
+    mode = "fast" if fast else "accurate"
+    a = orc.gen_matrix(m, k, float(g("phi")), seed, prec)
+    b = orc.gen_matrix(k, n, float(g("phi")), seed + 1, prec)
+    return a, b, N, prec, mode, g
+
+
+# ---------------------------------------------------------------- K3: int8 GEMM
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (37, 29, 53), (128, 256, 128), (300, 500, 1000),
+                                   (129, 257, 4096), (64, 1000, 130)])
+def test_gemm_i8_i32_random(crt, m, n, k):
+    rng = np.random.default_rng(m * 7 + n * 11 + k)
+    a = rng.integers(-128, 128, (m, k), dtype=np.int8)
+    b = rng.integers(-128, 128, (k, n), dtype=np.int8)
+    c = crt.gemm_i8_i32(a, b)
+    assert c.dtype == np.int32
+    assert np.array_equal(c, orc.i8_product(a, b))
+
+
+def test_gemm_i8_i32_extremes(crt):
+    # all -128 with k = 4096 (reference tests/test_kernel.py:34-39)
+    a = np.full((130, 4096), -128, np.int8)
+    b = np.full((4096, 300), -128, np.int8)
+    c = crt.gemm_i8_i32(a, b)
+    assert np.all(c == 4096 * 16384)
+    # the k cap and the int32 accumulator bound
+    with pytest.raises(crt.DimensionError):
+        crt.gemm_i8_i32(np.zeros((1, 2 ** 17 + 1), np.int8), np.zeros((2 ** 17 + 1, 1), np.int8))
+
+
+def test_gemm_i8_i32_max_k(crt):
+    rng = np.random.default_rng(5)
+    a = rng.integers(-128, 128, (4, 2 ** 16), dtype=np.int8)
+    b = rng.integers(-128, 128, (2 ** 16, 256), dtype=np.int8)
+    assert np.array_equal(crt.gemm_i8_i32(a, b), orc.i8_product(a, b))
+
+
+# ------------------------------------------------------- K3: Karatsuba mod product
+@pytest.mark.parametrize("p", [256, 255, 251, 239, 199, 173])
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (40, 33, 70), (256, 512, 384), (131, 260, 1000)])
+def test_complex_gemm_mod(crt, p, m, n, k):
+    rng = np.random.default_rng(p + m + n + k)
+    lo, hi = (-(p // 2), p - 1 - p // 2) if p % 2 == 0 else (-((p - 1) // 2), (p - 1) // 2)
+    ar, ai = (rng.integers(lo, hi + 1, (m, k)).astype(np.int8) for _ in range(2))
+    br, bi = (rng.integers(lo, hi + 1, (k, n)).astype(np.int8) for _ in range(2))
+    er, ei = crt.complex_gemm_mod(ar, ai, br, bi, p)
+    xr, xi = orc.karatsuba_mod(ar, ai, br, bi, p)
+    assert np.array_equal(er, xr) and np.array_equal(ei, xi)
+
+
+def test_complex_gemm_mod_hand_case(crt):
+    # (1+2i)(3+4i) = -5+10i (reference tests/test_kernel.py:58-66)
+    er, ei = crt.complex_gemm_mod([[1]], [[2]], [[3]], [[4]], 251)
+    assert int(er[0, 0]) == -5 and int(ei[0, 0]) == 10
+
+
+def test_complex_gemm_mod_full_range_k_cap(crt):
+    # extreme residues at the complex k cap: int32 D-E would overflow without
+    # reducing D, E, F first (reference kernel.py:46-50)
+    k = 2 ** 16
+    ar = np.full((2, k), -128, np.int8)
+    ai = np.full((2, k), 127, np.int8)
+    br = np.full((k, 256), -128, np.int8)
+    bi = np.full((k, 256), -128, np.int8)
+    er, ei = crt.complex_gemm_mod(ar, ai, br, bi, 256)
+    xr, xi = orc.karatsuba_mod(ar, ai, br, bi, 256)
+    assert np.array_equal(er, xr) and np.array_equal(ei, xi)
+
+
+# ------------------------------------------------------------------ K1: scaling
+def test_scaling_vs_golden(crt, golden):
+    for tag in _cases(golden):
+        a, b, N, prec, mode, g = _case_inputs(golden, tag)
+        ms = crt.select_moduli(N)
+        fn = crt.fast_scaling if mode == "fast" else crt.accurate_scaling
+        diag = {}
+        sv = fn(a, b, ms, None, diag)
+        assert np.array_equal(sv.mu_exp, g("mu")), tag
+        assert np.array_equal(sv.nu_exp, g("nu")), tag
+        assert [diag.get("clamped_mu", 0), diag.get("clamped_nu", 0)] == g("diag").tolist()
+
+
+@pytest.mark.parametrize("k", [7, 127, 129, 1000, 4100, 70001])
+def test_fast_exponents_long_rows(crt, golden, k):
+    a = orc.gen_matrix(3, k, 4.0, 100 + k)
+    b = orc.gen_matrix(k, 2, 4.0, 200 + k)
+    sv = crt.fast_scaling(a, b, crt.select_moduli(14))
+    assert np.array_equal(sv.mu_exp, golden[f"pw_{k}__mu"])
+    assert np.array_equal(sv.nu_exp, golden[f"pw_{k}__nu"])
+
+
+def test_fast_exponents_random_rows(crt):
+    # pairwise order stress: wide dynamic range, odd lengths
+    for k in (9, 136, 250, 1023, 5000, 16384):
+        rng = np.random.default_rng(k)
+        a = (rng.standard_normal((33, k)) * np.exp(rng.standard_normal((33, k)) * 6)
+             + 1j * rng.standard_normal((33, k)) * np.exp(rng.standard_normal((33, k)) * 6))
+        b = (rng.standard_normal((k, 7)) * np.exp(rng.standard_normal((k, 7)) * 6)
+             + 1j * rng.standard_normal((k, 7)))
+        sv = crt.fast_scaling(a, b, crt.select_moduli(17))
+        mu, nu = orc.exponents(a, b, 17, "fast")
+        assert np.array_equal(sv.mu_exp, mu) and np.array_equal(sv.nu_exp, nu), k
+
+
+# ------------------------------------------------------------------ K2: residues
+def test_residues_vs_golden(crt, golden):
+    for tag in _cases(golden):
+        a, b, N, prec, mode, g = _case_inputs(golden, tag)
+        ms = crt.select_moduli(N)
+        ra = crt.quantized_residues(a, g("mu"), ms, axis=0)
+        rb = crt.quantized_residues(b, g("nu"), ms, axis=1)
+        assert np.array_equal(ra[:, 0], g("ar")) and np.array_equal(ra[:, 1], g("ai")), tag
+        assert np.array_equal(rb[:, 0], g("br")) and np.array_equal(rb[:, 1], g("bi")), tag
+        for idx, p in enumerate(ms.moduli):
+            assert np.array_equal(ra[idx, 2], orc.sym_residue_int(
+                g("ar")[idx].astype(np.int64) + g("ai")[idx], p)), tag
+
+
+def test_residues_wide_values(crt):
+    # |a'| up to 2^89 (N = 20 budgets reach 2^77; the reference allows < 2^90)
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal((40, 300)) + 1j * rng.standard_normal((40, 300)))
+    exps = rng.integers(0, 87, 40)
+    ms = crt.select_moduli(20)
+    got = crt.quantized_residues(x, exps, ms, axis=0)
+    ar = orc.truncate(np.ascontiguousarray(x.real), exps, 0)
+    ai = orc.truncate(np.ascontiguousarray(x.imag), exps, 0)
+    assert np.array_equal(got[:, 0], orc.residues(ar, orc.pick_moduli(20)))
+    assert np.array_equal(got[:, 1], orc.residues(ai, orc.pick_moduli(20)))
+
+
+def test_residues_overflow_is_domain_error(crt):
+    x = np.full((2, 3), 1.5 + 0j)
+    with pytest.raises(crt.DomainError):
+        crt.quantized_residues(x, np.array([90, 0]), crt.select_moduli(14), axis=0)
+
+
+# --------------------------------------------------------------------- K4: CRT
+def test_crt_vs_golden(crt, golden):
+    for tag in _cases(golden):
+        a, b, N, prec, mode, g = _case_inputs(golden, tag)
+        c = crt.crt_reconstruct(g("er"), g("ei"), g("mu"), g("nu"), crt.select_moduli(N), prec)
+        assert c.tobytes() == g("c").tobytes(), tag
+
+
+# ------------------------------------------------------------ end to end
+def test_emulate_small_golden(crt, golden):
+    for tag in _cases(golden):
+        a, b, N, prec, mode, g = _case_inputs(golden, tag)
+        cfg = crt.EmuConfig(precision=prec, domain="complex", mode=mode, num_moduli=N)
+        diag = {}
+        c = crt.emulate_gemm_complex(a, b, cfg, diag)
+        assert c.dtype == g("c").dtype, tag
+        assert c.tobytes() == g("c").tobytes(), tag
+        assert [diag.get("clamped_mu", 0), diag.get("clamped_nu", 0)] == g("diag").tolist()
+
+
+@pytest.mark.parametrize("tag", ["cfg1_z1024_fast14", "cfg1_z1024_accu14", "z512_fast20_phi4",
+                                 "z384_accu17_phi2", "c512_fast6_phi0", "c512_fast10_phi1",
+                                 "c512_accu8_phi1", "z_skinny_fast14", "z_ragged_fast13"])
+def test_emulate_hash_golden(crt, golden_hashes, tag):
+    h = golden_hashes[tag]
+    a = orc.gen_matrix(h["m"], h["k"], h["phi"], h["seed"], h["precision"])
+    b = orc.gen_matrix(h["k"], h["n"], h["phi"], h["seed"] + 1, h["precision"])
+    assert _sha(a) == h["a_sha"] and _sha(b) == h["b_sha"]
+    cfg = crt.EmuConfig(precision=h["precision"], domain="complex", mode=h["mode"],
+                        num_moduli=h["N"])
+    c = crt.emulate_gemm_complex(a, b, cfg)
+    assert _sha(c) == h["c_sha"], (c.reshape(-1)[:4], h["c_head"])
+
+
+def test_torch_inputs_and_n_block_invariance(crt):
+    a = orc.gen_matrix(300, 700, 1.0, 31)
+    b = orc.gen_matrix(700, 900, 1.0, 32)
+    ref = orc.emulate_complex(a, b, 14)
+    ta = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    tb = torch.from_numpy(np.ascontiguousarray(b)).cuda()
+    for nb in (1, 256, 300, 8192):
+        cfg = crt.EmuConfig(domain="complex", n_block=nb)
+        c = crt.emulate_gemm_complex(ta, tb, cfg)
+        assert isinstance(c, torch.Tensor) and c.is_cuda
+        assert c.cpu().numpy().tobytes() == ref.tobytes(), nb
+
+
+def test_conjugate_symmetry_and_integer_inputs(crt):
+    a = orc.gen_matrix(64, 96, 2.0, 40)
+    b = orc.gen_matrix(96, 80, 2.0, 41)
+    cfg = crt.EmuConfig(domain="complex")
+    c1 = crt.emulate_gemm_complex(a, b, cfg)
+    c2 = crt.emulate_gemm_complex(np.conj(a), np.conj(b), cfg)
+    assert np.array_equal(c1, np.conj(c2))
+    ai = np.round(a * 50)
+    bi = np.round(b * 50)
+    ci = crt.emulate_gemm_complex(ai, bi, cfg)
+    assert np.array_equal(ci, ai @ bi)
+
+
+def test_errors(crt):
+    cfg = crt.EmuConfig(domain="complex")
+    a = np.ones((4, 5), complex)
+    bad = a.copy()
+    bad[1, 2] = np.nan
+    with pytest.raises(crt.DomainError):
+        crt.emulate_gemm_complex(bad, np.ones((5, 3), complex), cfg)
+    with pytest.raises(crt.DomainError):
+        crt.emulate_gemm_complex(a, np.full((5, 3), np.inf + 0j), cfg)
+    with pytest.raises(crt.DimensionError):
+        crt.emulate_gemm_complex(a, np.ones((4, 3), complex), cfg)
+    with pytest.raises(crt.DimensionError):
+        crt.emulate_gemm_complex(np.ones((1, 2 ** 16 + 1)), np.ones((2 ** 16 + 1, 1)), cfg)
+    with pytest.raises(crt.ConfigError):
+        crt.emulate_gemm_complex(a, np.ones((5, 3)), crt.EmuConfig(domain="real"))
+
+
+def test_zero_rows_and_accurate_zero_b(crt):
+    a = orc.gen_matrix(20, 30, 1.0, 50)
+    b = orc.gen_matrix(30, 10, 1.0, 51)
+    a[3] = 0
+    b[:, 4] = 0
+    for mode in ("fast", "accurate"):
+        cfg = crt.EmuConfig(domain="complex", mode=mode)
+        c = crt.emulate_gemm_complex(a, b, cfg)
+        ref = orc.emulate_complex(a, b, None, mode)
+        assert c.tobytes() == ref.tobytes(), mode
+    # accurate mode with B == 0 and A != 0: mu = 1023 -> DomainError (reference behaviour)
+    with pytest.raises(crt.DomainError):
+        crt.emulate_gemm_complex(a, np.zeros((30, 10), complex),
+                                 crt.EmuConfig(domain="complex", mode="accurate"))
+
+
+def test_blas_gemm_colmajor(crt):
+    m, n, k = 7, 5, 9
+    rng = np.random.default_rng(8)
+    lda, ldb, ldc = 10, 12, 8
+    a = rng.standard_normal(lda * k) + 1j * rng.standard_normal(lda * k)
+    b = rng.standard_normal(ldb * n) + 1j * rng.standard_normal(ldb * n)
+    c = np.zeros(ldc * n, complex)
+    out = crt.gemm("complex", "double", m, n, k, a, lda, b, ldb, c, ldc)
+    av = a[:lda * k].reshape((lda, k), order="F")[:m]
+    bv = b[:ldb * n].reshape((ldb, n), order="F")[:k]
+    ref = orc.emulate_complex(av, bv, 14)
+    assert out is c
+    assert np.array_equal(c.reshape((ldc, n), order="F")[:m], ref)
+    assert np.all(c.reshape((ldc, n), order="F")[m:] == 0)
+
+
+# ------------------------------------------------------- full-size properties
+def test_subblock_parity_large(crt):
+    """Fast mode is row/column local: a block of the 4096^3 product equals the
+    emulation of the corresponding slabs, which the oracle can afford."""
+    m = n = k = 4096
+    a = orc.gen_matrix(m, k, 0.5, 60)
+    b = orc.gen_matrix(k, n, 0.5, 61)
+    cfg = crt.EmuConfig(domain="complex")
+    c = crt.emulate_gemm_complex(a, b, cfg)
+    rows = slice(1000, 1064)
+    cols = slice(3000, 3048)
+    ref = orc.emulate_complex(a[rows], b[:, cols], 14)
+    assert c[rows, cols].tobytes() == ref.tobytes()
+    # and the last ragged corner
+    ref2 = orc.emulate_complex(a[-5:], b[:, -7:], 14)
+    assert c[-5:, -7:].tobytes() == ref2.tobytes()
