@@ -129,9 +129,22 @@ DevConsts make_dev(const crtg_consts& K) {
   for (int l = 0; l < d.n; ++l) {
     const int p = K.moduli[l];
     d.mc[l] = make_mod(p);
+    const ModConst& mc = d.mc[l];
+    ResConst& rc = d.rc[l];
+    const uint32_t h = uint32_t(p / 2);
+    const uint32_t c53 = uint32_t((uint64_t(1) << 53) % uint64_t(p));
+    rc.c32 = mc.c32;
+    rc.c16 = mc.c16;
+    rc.h = h;
+    rc.k = uint32_t((h + uint32_t(p) - c53) % uint32_t(p));
+    rc.sum_k = uint32_t(p) - h;
+    rc.magic = mc.magic;
+    rc.shift = mc.is_pow2 ? -1 : mc.shift;  // -1 marks p = 256 (mask)
+    rc.p = p;
     uint32_t v = 1 % p;
     for (int s = 0; s < 40; ++s) {
       d.pow2mod[l][s] = uint16_t(v);
+      d.wide_k[l][s] = uint16_t((uint64_t(h) * ((uint32_t(p) + 1 - v) % uint32_t(p))) % uint32_t(p));
       v = (v * 2) % p;
     }
     d.coeff_hi[l] = K.coeff_hi[l];

@@ -49,10 +49,21 @@ struct ModConst {
   int32_t is_pow2;
 };
 
+// Residue-kernel constants.  With v = 2^53 + x (x = +-M, M < 2^53) split as
+// v = hi*2^32 + lo_h*2^16 + lo_l, u = hi*c32 + lo_h*c16 + lo_l + k is
+// congruent to x + h (h = floor(p/2)) and below 2^31, so one magic reduction gives
+// t = (x + h) mod p and the symmetric residue is t - h.
+struct ResConst {
+  uint32_t c32, c16, k, h, magic, sum_k;  // sum_k = p - h (re + im plane)
+  int32_t shift, p;
+};
+
 struct DevConsts {
   int32_t n;
   ModConst mc[CRTG_MAX_MODULI];
+  ResConst rc[CRTG_MAX_MODULI];
   uint16_t pow2mod[CRTG_MAX_MODULI][40];  // 2^s mod p, s < 40 (wide residues)
+  uint16_t wide_k[CRTG_MAX_MODULI][40];   // h * (1 - 2^s) mod p
   double coeff_hi[CRTG_MAX_MODULI];
   double coeff_lo[CRTG_MAX_MODULI];
   double p_hi, p_lo;

@@ -172,6 +172,163 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
   }
 }
 
+// ---------------------------------------------------------------------------
+// Residue kernel.  CTA tile = 16 operand rows x 128 K (one packed K block);
+// thread = 8 consecutive K of one row (16 real values).  Each value is
+// decomposed once into 3 registers (hi | s<<24, lo_h, lo_l of v = 2^53 +- M);
+// per modulus a value costs 6 integer ops.  Output goes through a 6 KiB smem
+// stage so every global store is a coalesced 16-byte write of a contiguous
+// 2 KiB run of the packed plane.
+// ---------------------------------------------------------------------------
+constexpr int kResRows = 16;
+
+struct Val3 {
+  uint32_t hi, lh, ll;
+};
+
+// x integer-valued, |x| < 2^90 -> v = 2^53 + sign*M (M < 2^53), shift s
+__device__ __forceinline__ Val3 split_value(double x) {
+  double a = fabs(x);
+  uint32_t s = 0;
+  if (a >= 9007199254740992.0) {
+    s = uint32_t(ilogb(a) - 52);
+    a = ldexp(a, -int(s));
+  }
+  const uint64_t M = uint64_t(a);
+  const uint64_t v = x < 0.0 ? (uint64_t(1) << 53) - M : (uint64_t(1) << 53) + M;
+  return {uint32_t(v >> 32) | (s << 24), uint32_t(v) >> 16, uint32_t(v) & 0xFFFFu};
+}
+
+template <bool WIDE>
+__device__ __forceinline__ uint32_t res_t(const Val3& v, const ResConst& c, int l,
+                                          const DevConsts& dc) {
+  // t = (x + h) mod p
+  const uint32_t hi = WIDE ? (v.hi & 0x00FFFFFFu) : v.hi;
+  const uint32_t u = hi * c.c32 + v.lh * c.c16 + v.ll + c.k;
+  uint32_t t;
+  if (c.shift < 0) {
+    t = u & 0xFFu;
+  } else {
+    t = u - uint32_t(c.p) * (__umulhi(u, c.magic) >> c.shift);
+  }
+  if (WIDE) {
+    const uint32_t s = v.hi >> 24;
+    if (s) {
+      const uint32_t w = t * dc.pow2mod[l][s] + dc.wide_k[l][s];
+      t = c.shift < 0 ? (w & 0xFFu) : w - uint32_t(c.p) * (__umulhi(w, c.magic) >> c.shift);
+    }
+  }
+  return t;
+}
+
+__device__ __forceinline__ uint32_t mod_small(uint32_t u, const ResConst& c) {
+  return c.shift < 0 ? (u & 0xFFu) : u - uint32_t(c.p) * (__umulhi(u, c.magic) >> c.shift);
+}
+
+// 4 values t_i in [0,p) -> packed int8 (t_i - h)
+__device__ __forceinline__ uint32_t pack_sym(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                             uint32_t h) {
+  const uint32_t lo = __byte_perm(a - h, b - h, 0x0040);
+  const uint32_t hi = __byte_perm(c - h, d - h, 0x0040);
+  return __byte_perm(lo, hi, 0x5410);
+}
+
+template <bool WIDE>
+__device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&im)[8],
+                                              const ResConst& c, int l, const DevConsts& dc,
+                                              uint32_t (&w)[3][2]) {
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint32_t tr[4], ti[4], ts[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      tr[j] = res_t<WIDE>(re[4 * half + j], c, l, dc);
+      ti[j] = res_t<WIDE>(im[4 * half + j], c, l, dc);
+      // (re + im) + h = (tr - h) + (ti - h) + h  (mod p)
+      ts[j] = mod_small(tr[j] + ti[j] + c.sum_k, c);
+    }
+    w[0][half] = pack_sym(tr[0], tr[1], tr[2], tr[3], c.h);
+    w[1][half] = pack_sym(ti[0], ti[1], ti[2], ti[3], c.h);
+    w[2][half] = pack_sym(ts[0], ts[1], ts[2], ts[3], c.h);
+  }
+}
+
+template <typename T, int OPERAND>
+__global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, int64_t ldx, int rows,
+                                                  int kdim, int64_t col0,
+                                                  const int32_t* __restrict__ exps,
+                                                  const __grid_constant__ DevConsts dc,
+                                                  int8_t* __restrict__ out, int64_t plane_bytes,
+                                                  int64_t rb_count,
+                                                  unsigned long long* __restrict__ overflow) {
+  __shared__ __align__(16) uint8_t stage[3][kResRows * 128];
+  const int kb = blockIdx.x;
+  const int r0 = blockIdx.y * kResRows;
+  int r, seg;  // row within the tile, 8-element K segment (0..15)
+  if (OPERAND == 0) {
+    r = threadIdx.x >> 4;
+    seg = threadIdx.x & 15;
+  } else {
+    r = threadIdx.x & 15;
+    seg = threadIdx.x >> 4;
+  }
+  const int row = r0 + r;
+  const int h0 = kb * 128 + seg * 8;
+  const bool row_ok = row < rows;
+  const int e = row_ok ? exps[row] : 0;
+
+  Val3 vr[8], vi[8];
+  int bad = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int h = h0 + t;
+    double re = 0.0, im = 0.0;
+    if (row_ok && h < kdim) {
+      const T* p = (OPERAND == 0) ? X + 2 * (int64_t(row) * ldx + h)
+                                  : X + 2 * (int64_t(h) * ldx + col0 + row);
+      load_c<T>(p, re, im);
+    }
+    double qr = trunc(ldexp_rn(re, e));
+    double qi = trunc(ldexp_rn(im, e));
+    if (!(fabs(qr) < 0x1p90)) { bad = 1; qr = 0.0; }
+    if (!(fabs(qi) < 0x1p90)) { bad = 1; qi = 0.0; }
+    vr[t] = split_value(qr);
+    vi[t] = split_value(qi);
+  }
+  uint32_t any_wide = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) any_wide |= (vr[t].hi | vi[t].hi) >> 24;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(overflow, 1ull);
+
+  // swizzled byte offset of this thread's 8 bytes inside the 2 KiB stage tile
+  const int chunk = seg >> 1;
+  const int soff = (r >> 3) * 1024 + (r & 7) * 128 + ((chunk ^ (r & 7)) << 4) + (seg & 1) * 8;
+  // the tile's 16 rows form one contiguous 2 KiB run of each packed plane
+  const int64_t goff = (int64_t(kb) * rb_count + (r0 >> 7)) * kBlockBytes + (r0 & 127) * 128;
+  const int q = threadIdx.x >> 7;        // copy-out: plane handled by this half
+  const int qi = threadIdx.x & 127;      // 16-byte slot within the 2 KiB run
+
+  for (int l = 0; l < dc.n; ++l) {
+    const ResConst c = dc.rc[l];
+    uint32_t w[3][2];
+    if (any_wide)
+      residue_words<true>(vr, vi, c, l, dc, w);
+    else
+      residue_words<false>(vr, vi, c, l, dc, w);
+#pragma unroll
+    for (int pl = 0; pl < 3; ++pl)
+      *reinterpret_cast<uint2*>(&stage[pl][soff]) = make_uint2(w[pl][0], w[pl][1]);
+    __syncthreads();
+    int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
+    reinterpret_cast<uint4*>(base + q * plane_bytes)[qi] =
+        reinterpret_cast<const uint4*>(stage[q])[qi];
+    if (q == 0)
+      reinterpret_cast<uint4*>(base + 2 * plane_bytes)[qi] =
+          reinterpret_cast<const uint4*>(stage[2])[qi];
+    __syncthreads();
+  }
+}
+
 // plain int8 -> packed plane (test hooks); one thread per 16-byte chunk
 __global__ void k_pack_i8(const int8_t* __restrict__ X, int trans, int64_t rows, int64_t kdim,
                           int64_t kpad, int8_t* __restrict__ out, int64_t rb_count,
@@ -203,11 +360,17 @@ template <typename T, int OP, int KIND>
 void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t col0,
                 const int32_t* exps, const DevConsts& dc, int8_t* out, int64_t plane_bytes,
                 int64_t rb_count, unsigned long long* overflow, cudaStream_t s) {
+  if constexpr (KIND == PACK_RESIDUE) {
+    dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kResRows));
+    k_residues<T, OP><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows), int(kdim),
+                                          col0, exps, dc, out, plane_bytes, rb_count, overflow);
+  } else {
   // cover every padded row of the plane so the GEMM reads zeros there
   dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kTileRows));
   k_pack<T, OP, KIND><<<grid, kThreads, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),
                                                 int(kdim), col0, exps, dc, out, plane_bytes,
                                                 rb_count, overflow);
+  }
 }
 
 }  // namespace
