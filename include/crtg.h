@@ -108,6 +108,35 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k,
                       void* ws, size_t ws_bytes, int32_t* mu_out, int32_t* nu_out,
                       uint64_t* diag, int sync_check, void* stream);
 
+/* ---- multi-GPU building blocks (output-tile sharding) ---- */
+
+/* The K2..K4 pipeline with caller-provided exponents (device int32 mu[m],
+ * nu[n]), e.g. accurate-mode exponents reduced across ranks. */
+int crtg_gemm_complex_exps(int precision, int64_t m, int64_t n, int64_t k,
+                           const void* A, int64_t lda, const void* B, int64_t ldb,
+                           void* C, int64_t ldc, const crtg_consts* K, int64_t n_block,
+                           const int32_t* mu, const int32_t* nu, void* ws, size_t ws_bytes,
+                           uint64_t* diag, int sync_check, void* stream);
+
+/* Accurate mode, local half (scaling.py:229-258): bound-product maxima of the
+ * local block (row_max int32[m], col_max int32[n]), normalisation exponents
+ * (bar_mu int32[m], bar_nu int32[n]) and absmax (row_abs double[m],
+ * col_abs double[n]).  Any output pointer may be NULL.  A rank holding
+ * A[I,:] and B[:,J] all-reduces row_max (MAX) over the ranks sharing I and
+ * col_max over the ranks sharing J, then calls crtg_accurate_exponents. */
+int crtg_accurate_partial(int precision, int64_t m, int64_t n, int64_t k,
+                          const void* A, int64_t lda, const void* B, int64_t ldb,
+                          const crtg_consts* K, void* ws, size_t ws_bytes,
+                          int32_t* row_max, int32_t* col_max, int32_t* bar_mu,
+                          int32_t* bar_nu, double* row_abs, double* col_abs,
+                          uint64_t* diag, void* stream);
+
+/* Accurate-mode exponents from (globally reduced) bound maxima
+ * (scaling.py:260-271); clamp events are added to *clamp_counter (device). */
+int crtg_accurate_exponents(int64_t count, const int32_t* maxb, const double* absval,
+                            const int32_t* bar, const crtg_consts* K, int32_t* out,
+                            uint64_t* clamp_counter, void* stream);
+
 /* ---- parity hooks: each reuses the production kernels of one stage ---- */
 
 /* Scaling vectors only (fast_scaling scaling.py:198-213 / accurate_scaling

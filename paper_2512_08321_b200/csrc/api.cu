@@ -152,6 +152,34 @@ DevConsts make_dev(const crtg_consts& K) {
   }
   d.p_hi = K.p_hi;
   d.p_lo = K.p_lo;
+  // S1 grid: every coeff_hi is a multiple of 2^g (crt.py:72-86); take the
+  // largest common power of two and split the integer quotients into limbs.
+  int g = 1100;
+  for (int l = 0; l < d.n; ++l) {
+    if (K.coeff_hi[l] == 0.0) continue;
+    int e;
+    const double fr = std::frexp(K.coeff_hi[l], &e);
+    // coeff_hi = fr * 2^e; lowest set bit of the 53-bit significand
+    const uint64_t mant = uint64_t(std::ldexp(fr, 53));
+    g = std::min(g, e - 53 + __builtin_ctzll(mant));
+  }
+  if (g == 1100) g = 0;
+  bool limbs_ok = true;
+  for (int l = 0; l < d.n; ++l) {
+    const double q = std::ldexp(K.coeff_hi[l], -g);
+    if (q >= 281474976710656.0) limbs_ok = false;  // 2^48
+    const uint64_t H = uint64_t(q);
+    d.hi_limb[l][0] = int32_t(H & 0xFFFF);
+    d.hi_limb[l][1] = int32_t((H >> 16) & 0xFFFF);
+    d.hi_limb[l][2] = int32_t(H >> 32);
+  }
+  d.hi_scale = limbs_ok ? std::ldexp(1.0, g) : 0.0;  // 0 -> kernel keeps the f64 S1 sum
+  {
+    const double c = 134217729.0 * d.p_hi;
+    d.p_split_hi = c - (c - d.p_hi);
+    d.p_split_lo = d.p_hi - d.p_split_hi;
+  }
+  d.inv_p = 1.0 / d.p_hi;
   d.p_fast = K.p_fast;
   d.p_accu = K.p_accu;
   d.delta = K.delta;
@@ -288,6 +316,59 @@ int check_dims(int64_t m, int64_t n, int64_t k, int64_t lda, int64_t ldb, int64_
   return CRTG_OK;
 }
 
+// accurate mode, the local part (scaling.py:229-258): absmax, bars, bound
+// operands and the tcgen05 bound GEMM -> row / column maxima in the plan
+int accurate_partial(const Plan& P, int precision, const void* A, int64_t lda, const void* B,
+                     int64_t ldb, const DevConsts& dc, void* ws, unsigned long long* diag,
+                     cudaStream_t s) {
+  const bool single = (precision & CRTG_IN_C64) != 0;
+  double* rowabs = at<double>(ws, P.rowabs);
+  double* colabs = at<double>(ws, P.colabs);
+  int32_t* bar_mu = at<int32_t>(ws, P.bar_mu);
+  int32_t* bar_nu = at<int32_t>(ws, P.bar_nu);
+  int32_t* rowmax = at<int32_t>(ws, P.rowmax);
+  int32_t* colmax = at<int32_t>(ws, P.colmax);
+  CRTG_TRY(cudaMemsetAsync(colabs, 0, P.colabs.bytes, s), "memset");
+  CRTG_TRY(cudaMemsetAsync(rowmax, 0, P.rowmax.bytes, s), "memset");
+  CRTG_TRY(cudaMemsetAsync(colmax, 0, P.colmax.bytes, s), "memset");
+  StageTimer timer(CRTG_STAGE_SCALING, s, 7);
+  PwTree tree{};
+  CRTG_TRY(launch_row_stats(single, false, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, nullptr,
+                            rowabs, diag, s),
+           "row absmax");
+  CRTG_TRY(launch_bar(rowabs, P.m, bar_mu, s), "bar");
+  CRTG_TRY(launch_col_absmax(single, B, ldb, P.k, P.n, colabs, diag, s), "col absmax");
+  CRTG_TRY(launch_bar(colabs, P.n, bar_nu, s), "bar");
+  const int64_t a_plane = P.m_pad * P.k_pad, b_plane = P.n_pad * P.k_pad;
+  int8_t* abars = at<int8_t>(ws, P.a_bars);
+  int8_t* bbars = at<int8_t>(ws, P.b_bars);
+  CRTG_TRY(launch_pack(single, 0, PACK_BARS, A, lda, P.m, P.k, 0, bar_mu, dc, abars, a_plane,
+                       P.m_pad / 128, diag + CRTG_DIAG_OVERFLOW_A, s),
+           "bars A");
+  CRTG_TRY(launch_pack(single, 1, PACK_BARS, B, ldb, P.n, P.k, 0, bar_nu, dc, bbars, b_plane,
+                       P.n_pad / 128, diag + CRTG_DIAG_OVERFLOW_B, s),
+           "bars B");
+  GemmArgs g{};
+  g.a = abars;
+  g.b = bbars;
+  g.a_plane = a_plane;
+  g.b_plane = b_plane;
+  g.a_rb = int(P.m_pad / 128);
+  g.b_rb = int(P.n_pad / 128);
+  g.mt = int(P.m_pad / 128);
+  g.nt = int(P.n_pad / 256);
+  g.kb = int(P.k_pad / 128);
+  g.nl = 1;
+  g.planes_per_l = 3;
+  g.nphase = 3;
+  g.m = int(P.m);
+  g.n = int(P.n);
+  g.row_max = rowmax;
+  g.col_max = colmax;
+  CRTG_TRY(launch_gemm(EPI_BOUND, g, sm_count(), s), "bound gemm");
+  return CRTG_OK;
+}
+
 // exponents (fast or accurate) into mu / nu of the plan
 int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t lda,
                 const void* B, int64_t ldb, const DevConsts& dc, void* ws,
@@ -326,52 +407,80 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
     return CRTG_OK;
   }
   // accurate mode (scaling.py:229-274)
-  int32_t* bar_mu = at<int32_t>(ws, P.bar_mu);
-  int32_t* bar_nu = at<int32_t>(ws, P.bar_nu);
-  int32_t* rowmax = at<int32_t>(ws, P.rowmax);
-  int32_t* colmax = at<int32_t>(ws, P.colmax);
-  CRTG_TRY(cudaMemsetAsync(rowmax, 0, P.rowmax.bytes, s), "memset");
-  CRTG_TRY(cudaMemsetAsync(colmax, 0, P.colmax.bytes, s), "memset");
-  StageTimer timer(CRTG_STAGE_SCALING, s, 9);
-  CRTG_TRY(launch_row_stats(single, false, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu, rowabs,
-                            diag, s),
-           "row absmax");
-  CRTG_TRY(launch_bar(rowabs, P.m, bar_mu, s), "bar");
-  CRTG_TRY(launch_col_absmax(single, B, ldb, P.k, P.n, colabs, diag, s), "col absmax");
-  CRTG_TRY(launch_bar(colabs, P.n, bar_nu, s), "bar");
-  const int64_t a_plane = P.m_pad * P.k_pad, b_plane = P.n_pad * P.k_pad;
-  int8_t* abars = at<int8_t>(ws, P.a_bars);
-  int8_t* bbars = at<int8_t>(ws, P.b_bars);
-  CRTG_TRY(launch_pack(single, 0, PACK_BARS, A, lda, P.m, P.k, 0, bar_mu, dc, abars, a_plane,
-                       P.m_pad / 128, diag + CRTG_DIAG_OVERFLOW_A, s),
-           "bars A");
-  CRTG_TRY(launch_pack(single, 1, PACK_BARS, B, ldb, P.n, P.k, 0, bar_nu, dc, bbars, b_plane,
-                       P.n_pad / 128, diag + CRTG_DIAG_OVERFLOW_B, s),
-           "bars B");
-  GemmArgs g{};
-  g.a = abars;
-  g.b = bbars;
-  g.a_plane = a_plane;
-  g.b_plane = b_plane;
-  g.a_rb = int(P.m_pad / 128);
-  g.b_rb = int(P.n_pad / 128);
-  g.mt = int(P.m_pad / 128);
-  g.nt = int(P.n_pad / 256);
-  g.kb = int(P.k_pad / 128);
-  g.nl = 1;
-  g.planes_per_l = 3;
-  g.nphase = 3;
-  g.m = int(P.m);
-  g.n = int(P.n);
-  g.row_max = rowmax;
-  g.col_max = colmax;
-  CRTG_TRY(launch_gemm(EPI_BOUND, g, sm_count(), s), "bound gemm");
-  CRTG_TRY(launch_accurate_exps(rowmax, rowabs, bar_mu, P.m, dc.p_accu, dc.delta, mu,
-                                diag + CRTG_DIAG_CLAMPED_MU, s),
+  if (int e = accurate_partial(P, precision, A, lda, B, ldb, dc, ws, diag, s)) return e;
+  StageTimer timer(CRTG_STAGE_SCALING, s, 2);
+  CRTG_TRY(launch_accurate_exps(at<int32_t>(ws, P.rowmax), rowabs, at<int32_t>(ws, P.bar_mu), P.m,
+                                dc.p_accu, dc.delta, mu, diag + CRTG_DIAG_CLAMPED_MU, s),
            "accurate mu");
-  CRTG_TRY(launch_accurate_exps(colmax, colabs, bar_nu, P.n, dc.p_accu, dc.delta, nu,
-                                diag + CRTG_DIAG_CLAMPED_NU, s),
+  CRTG_TRY(launch_accurate_exps(at<int32_t>(ws, P.colmax), colabs, at<int32_t>(ws, P.bar_nu), P.n,
+                                dc.p_accu, dc.delta, nu, diag + CRTG_DIAG_CLAMPED_NU, s),
            "accurate nu");
+  return CRTG_OK;
+}
+
+// K2..K4 with exponents already in device memory (mu: m, nu: n)
+int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const void* B,
+                 int64_t ldb, void* C, int64_t ldc, const DevConsts& dc, const int32_t* mu,
+                 const int32_t* nu, void* ws, unsigned long long* dg, cudaStream_t s) {
+  const int64_t m = P.m, n = P.n, k = P.k;
+  const int N = int(P.N);
+  const bool in32 = (precision & CRTG_IN_C64) != 0;
+  const bool single = (precision & CRTG_SINGLE) != 0;  // result type / CRT path
+  // K2: residues of A (once)
+  const int64_t a_plane = P.m_pad * P.k_pad;
+  int8_t* apack = at<int8_t>(ws, P.a_pack);
+  {
+    StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
+    CRTG_TRY(launch_pack(in32, 0, PACK_RESIDUE, A, lda, m, k, 0, mu, dc, apack, a_plane,
+                         P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s),
+             "residues A");
+  }
+
+  int8_t* bpack = at<int8_t>(ws, P.b_pack);
+  int8_t* ere = at<int8_t>(ws, P.e_re);
+  int8_t* eim = at<int8_t>(ws, P.e_im);
+  const size_t csz = single ? 8 : 16;
+  for (int64_t j0 = 0; j0 < n; j0 += P.nb) {
+    const int64_t w = std::min(P.nb, n - j0);
+    const int64_t w_pad = round_up(w, 256);
+    const int64_t b_plane = w_pad * P.k_pad;
+    {
+      StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
+      CRTG_TRY(launch_pack(in32, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack, b_plane,
+                           w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
+               "residues B");
+    }
+    GemmArgs g{};
+    g.a = apack;
+    g.b = bpack;
+    g.a_plane = a_plane;
+    g.b_plane = b_plane;
+    g.a_rb = int(P.m_pad / 128);
+    g.b_rb = int(w_pad / 128);
+    g.mt = int(P.m_pad / 128);
+    g.nt = int(w_pad / 256);
+    g.kb = int(P.k_pad / 128);
+    g.nl = N;
+    g.planes_per_l = 3;
+    g.nphase = 3;
+    g.m = int(m);
+    g.n = int(w);
+    g.e_re = ere;
+    g.e_im = eim;
+    g.e_ld = P.nb_pad;
+    g.e_plane = m * P.nb_pad;
+    for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
+    {
+      StageTimer timer(CRTG_STAGE_GEMM, s, 1);
+      CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
+    }
+    {
+      StageTimer timer(CRTG_STAGE_CRT, s, 1);
+      CRTG_TRY(launch_crt(single, m, w, ere, eim, g.e_plane, g.e_ld, mu, nu + j0, dc,
+                          static_cast<char*>(C) + j0 * csz, ldc, s),
+               "crt");
+    }
+  }
   return CRTG_OK;
 }
 
@@ -460,62 +569,7 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
   if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s)) return e;
   int32_t* mu = at<int32_t>(ws, P.mu);
   int32_t* nu = at<int32_t>(ws, P.nu);
-
-  // K2: residues of A (once)
-  const int64_t a_plane = P.m_pad * P.k_pad;
-  int8_t* apack = at<int8_t>(ws, P.a_pack);
-  {
-    StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
-    CRTG_TRY(launch_pack(in32, 0, PACK_RESIDUE, A, lda, m, k, 0, mu, dc, apack, a_plane,
-                         P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s),
-             "residues A");
-  }
-
-  int8_t* bpack = at<int8_t>(ws, P.b_pack);
-  int8_t* ere = at<int8_t>(ws, P.e_re);
-  int8_t* eim = at<int8_t>(ws, P.e_im);
-  const size_t csz = single ? 8 : 16;
-  for (int64_t j0 = 0; j0 < n; j0 += P.nb) {
-    const int64_t w = std::min(P.nb, n - j0);
-    const int64_t w_pad = round_up(w, 256);
-    const int64_t b_plane = w_pad * P.k_pad;
-    {
-      StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
-      CRTG_TRY(launch_pack(in32, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack, b_plane,
-                           w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
-               "residues B");
-    }
-    GemmArgs g{};
-    g.a = apack;
-    g.b = bpack;
-    g.a_plane = a_plane;
-    g.b_plane = b_plane;
-    g.a_rb = int(P.m_pad / 128);
-    g.b_rb = int(w_pad / 128);
-    g.mt = int(P.m_pad / 128);
-    g.nt = int(w_pad / 256);
-    g.kb = int(P.k_pad / 128);
-    g.nl = N;
-    g.planes_per_l = 3;
-    g.nphase = 3;
-    g.m = int(m);
-    g.n = int(w);
-    g.e_re = ere;
-    g.e_im = eim;
-    g.e_ld = P.nb_pad;
-    g.e_plane = m * P.nb_pad;
-    for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
-    {
-      StageTimer timer(CRTG_STAGE_GEMM, s, 1);
-      CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
-    }
-    {
-      StageTimer timer(CRTG_STAGE_CRT, s, 1);
-      CRTG_TRY(launch_crt(single, m, w, ere, eim, g.e_plane, g.e_ld, mu, nu + j0, dc,
-                          static_cast<char*>(C) + j0 * csz, ldc, s),
-               "crt");
-    }
-  }
+  if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s)) return e;
   if (mu_out) CRTG_TRY(cudaMemcpyAsync(mu_out, mu, 4 * m, cudaMemcpyDeviceToDevice, s), "copy");
   if (nu_out) CRTG_TRY(cudaMemcpyAsync(nu_out, nu, 4 * n, cudaMemcpyDeviceToDevice, s), "copy");
   if (sync_check) return check_diag(dg, s);
@@ -706,4 +760,73 @@ extern "C" int crtg_profile_read(double* ms, uint64_t* launches) {
     cudaEventDestroy(r.b);
   }
   return status;
+}
+
+extern "C" int crtg_gemm_complex_exps(int precision, int64_t m, int64_t n, int64_t k,
+                                      const void* A, int64_t lda, const void* B, int64_t ldb,
+                                      void* C, int64_t ldc, const crtg_consts* K, int64_t n_block,
+                                      const int32_t* mu, const int32_t* nu, void* ws,
+                                      size_t ws_bytes, uint64_t* diag, int sync_check,
+                                      void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if ((precision & ~(CRTG_SINGLE | CRTG_IN_C64)) != 0)
+    return fail(CRTG_ERR_CONFIG, "precision must be double or single");
+  if (!mu || !nu) return fail(CRTG_ERR_CONFIG, "exponent vectors are required");
+  if (int e = check_dims(m, n, k, lda, ldb, ldc)) return e;
+  const Plan P = make_plan(CRTG_FAST, m, n, k, N, n_block);
+  if (!ws || ws_bytes < P.total)
+    return fail(CRTG_ERR_WORKSPACE, "workspace too small: need " + std::to_string(P.total));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
+                                : at<unsigned long long>(ws, P.diag);
+  CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
+  const DevConsts dc = make_dev(*K);
+  if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s)) return e;
+  if (sync_check) return check_diag(dg, s);
+  return CRTG_OK;
+}
+
+extern "C" int crtg_accurate_partial(int precision, int64_t m, int64_t n, int64_t k,
+                                     const void* A, int64_t lda, const void* B, int64_t ldb,
+                                     const crtg_consts* K, void* ws, size_t ws_bytes,
+                                     int32_t* row_max, int32_t* col_max, int32_t* bar_mu,
+                                     int32_t* bar_nu, double* row_abs, double* col_abs,
+                                     uint64_t* diag, void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if (int e = check_dims(m, n, k, lda, ldb, n)) return e;
+  const Plan P = make_plan(CRTG_ACCURATE, m, n, k, N, n);
+  if (!ws || ws_bytes < P.total) return fail(CRTG_ERR_WORKSPACE, "workspace too small");
+  if (!diag) return fail(CRTG_ERR_CONFIG, "diag is required");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* dg = reinterpret_cast<unsigned long long*>(diag);
+  const DevConsts dc = make_dev(*K);
+  if (int e = accurate_partial(P, precision, A, lda, B, ldb, dc, ws, dg, s)) return e;
+  auto copy = [&](void* dst, const Region& r, size_t bytes) {
+    return dst ? int(cudaMemcpyAsync(dst, static_cast<char*>(ws) + r.off, bytes,
+                                     cudaMemcpyDeviceToDevice, s))
+               : 0;
+  };
+  CRTG_TRY(copy(row_max, P.rowmax, 4 * m), "copy");
+  CRTG_TRY(copy(col_max, P.colmax, 4 * n), "copy");
+  CRTG_TRY(copy(bar_mu, P.bar_mu, 4 * m), "copy");
+  CRTG_TRY(copy(bar_nu, P.bar_nu, 4 * n), "copy");
+  CRTG_TRY(copy(row_abs, P.rowabs, 8 * m), "copy");
+  CRTG_TRY(copy(col_abs, P.colabs, 8 * n), "copy");
+  return CRTG_OK;
+}
+
+extern "C" int crtg_accurate_exponents(int64_t count, const int32_t* maxb, const double* absval,
+                                       const int32_t* bar, const crtg_consts* K, int32_t* out,
+                                       uint64_t* clamp_counter, void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if (count < 1) return fail(CRTG_ERR_DIMENSION, "empty exponent vector");
+  g_launches += 1;
+  CRTG_TRY(launch_accurate_exps(maxb, absval, bar, count, K->p_accu, K->delta, out,
+                                reinterpret_cast<unsigned long long*>(clamp_counter),
+                                static_cast<cudaStream_t>(stream)),
+           "accurate exponents");
+  return CRTG_OK;
 }

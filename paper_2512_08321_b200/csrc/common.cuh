@@ -68,6 +68,12 @@ struct DevConsts {
   double coeff_lo[CRTG_MAX_MODULI];
   double p_hi, p_lo;
   float p_fast, p_accu, delta;
+  // CRT helpers: coeff_hi[l] = (H2*2^32 + H1*2^16 + H0) * 2^hi_shift with 16-bit
+  // limbs (integer-pipe accumulation of the exact S1 sum), Dekker split of p_hi
+  // and its reciprocal (division-free quotient with an exact fallback).
+  int32_t hi_limb[CRTG_MAX_MODULI][3];
+  double hi_scale;  // 2^hi_shift
+  double p_split_hi, p_split_lo, inv_p;
 };
 
 __device__ __forceinline__ uint32_t mod_u31(uint32_t u, const ModConst& c) {

@@ -37,13 +37,15 @@ __device__ __forceinline__ DD split(double a) {
   return {hi, __dsub_rn(a, hi)};
 }
 
-__device__ __forceinline__ DD two_prod(double a, double b) {
+// two_prod(p_hi, z) with the Dekker split of the constant p_hi precomputed on
+// the host (same values as split(p_hi) in ddarith.py:30-44)
+__device__ __forceinline__ DD two_prod_p(double a, double ah, double al, double b) {
   const double p = __dmul_rn(a, b);
-  const DD as = split(a), bs = split(b);
+  const DD bs = split(b);
   const double e = __dadd_rn(
-      __dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(as.hi, bs.hi), p), __dmul_rn(as.hi, bs.lo)),
-                __dmul_rn(as.lo, bs.hi)),
-      __dmul_rn(as.lo, bs.lo));
+      __dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(ah, bs.hi), p), __dmul_rn(ah, bs.lo)),
+                __dmul_rn(al, bs.hi)),
+      __dmul_rn(al, bs.lo));
   return {p, e};
 }
 
@@ -56,25 +58,41 @@ __device__ __forceinline__ DD dd_add(double ahi, double alo, double bhi, double 
   return quick_two_sum(s.hi, s2);
 }
 
-// symmetric_mod_wide (crt.py:154-184)
-__device__ __forceinline__ double reduce_double(double s1, double s2, double p_hi, double p_lo) {
-  const double q = __ddiv_rn(__dadd_rn(s1, s2), p_hi);
-  const double z = ceil(__dsub_rn(q, 0.5));
+// z = ceil(q - 0.5) with q = fl(s / p_hi) (crt.py:166-167).  The quotient is
+// formed with the reciprocal; whenever q - 0.5 lies within a few ulps of an
+// integer (where the two roundings could disagree) the exact division is used.
+__device__ __forceinline__ double quotient_z(double s, const DevConsts& dc) {
+  const double d = __dsub_rn(__dmul_rn(s, dc.inv_p), 0.5);
+  const double r = rint(d);
+  if (fabs(__dsub_rn(d, r)) > 0x1p-40 * (fabs(d) + 1.0)) return ceil(d);
+  return ceil(__dsub_rn(__ddiv_rn(s, dc.p_hi), 0.5));
+}
+
+// symmetric_mod_wide (crt.py:154-184), double-double path
+__device__ __forceinline__ double reduce_double(double s1, double s2, const DevConsts& dc) {
+  const double z = quotient_z(__dadd_rn(s1, s2), dc);
   const DD hl = two_sum(s1, s2);
-  DD pz = two_prod(p_hi, z);
-  pz.lo = __dadd_rn(pz.lo, __dmul_rn(p_lo, z));
+  DD pz = two_prod_p(dc.p_hi, dc.p_split_hi, dc.p_split_lo, z);
+  pz.lo = __dadd_rn(pz.lo, __dmul_rn(dc.p_lo, z));
   pz = quick_two_sum(pz.hi, pz.lo);
   const DD r = dd_add(hl.hi, hl.lo, -pz.hi, -pz.lo);
   return __dadd_rn(r.hi, r.lo);
 }
 
-__device__ __forceinline__ double reduce_single(double s, double p_hi, double p_lo) {
-  const double q = __ddiv_rn(__dadd_rn(s, 0.0), p_hi);
-  const double z = ceil(__dsub_rn(q, 0.5));
-  return __dsub_rn(__dsub_rn(s, __dmul_rn(z, p_hi)), __dmul_rn(z, p_lo));
+// plain float64 path (single precision results)
+__device__ __forceinline__ double reduce_single(double s, const DevConsts& dc) {
+  const double z = quotient_z(__dadd_rn(s, 0.0), dc);
+  return __dsub_rn(__dsub_rn(s, __dmul_rn(z, dc.p_hi)), __dmul_rn(z, dc.p_lo));
 }
 
-template <bool SINGLE>
+__device__ __forceinline__ uint32_t load_word(const int8_t* p, bool aligned, int64_t j0, int64_t n) {
+  if (aligned) return *reinterpret_cast<const uint32_t*>(p);
+  uint32_t w = 0;
+  for (int q = 0; q < 4 && j0 + q < n; ++q) w |= uint32_t(uint8_t(p[q])) << (8 * q);
+  return w;
+}
+
+template <bool SINGLE, bool LIMBS>
 __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t* __restrict__ e_re,
                                              const int8_t* __restrict__ e_im, int64_t e_plane,
                                              int64_t e_ld, const int32_t* __restrict__ mu,
@@ -86,33 +104,42 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
   if (t >= m * nq) return;
   const int64_t i = t / nq;
   const int64_t j0 = (t - i * nq) * 4;
-  double s1r[4] = {0, 0, 0, 0}, s2r[4] = {0, 0, 0, 0}, s1i[4] = {0, 0, 0, 0},
-         s2i[4] = {0, 0, 0, 0};
   const int8_t* pr = e_re + i * e_ld + j0;
   const int8_t* pi = e_im + i * e_ld + j0;
   const bool aligned = ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(pi) |
                          uintptr_t(e_plane)) & 3) == 0 && j0 + 4 <= n;
+  // S1 (exact, on a 2^g grid): integer limbs on the INT pipes; S2: the rounded
+  // f64 sequence of crt.py:239-240, l ascending, no FMA.
+  int32_t tr[3][4] = {}, ti[3][4] = {};
+  double s1r[4] = {0, 0, 0, 0}, s1i[4] = {0, 0, 0, 0};
+  double s2r[4] = {0, 0, 0, 0}, s2i[4] = {0, 0, 0, 0};
   for (int l = 0; l < dc.n; ++l) {
-    uint32_t wr, wi;
-    if (aligned) {
-      wr = *reinterpret_cast<const uint32_t*>(pr + l * e_plane);
-      wi = *reinterpret_cast<const uint32_t*>(pi + l * e_plane);
-    } else {
-      wr = wi = 0;
-      for (int q = 0; q < 4 && j0 + q < n; ++q) {
-        wr |= uint32_t(uint8_t(pr[l * e_plane + q])) << (8 * q);
-        wi |= uint32_t(uint8_t(pi[l * e_plane + q])) << (8 * q);
-      }
-    }
-    const double ch = dc.coeff_hi[l], cl = dc.coeff_lo[l];
+    const uint32_t wr = load_word(pr + l * e_plane, aligned, j0, n);
+    const uint32_t wi = load_word(pi + l * e_plane, aligned, j0, n);
+    const double cl = dc.coeff_lo[l];
+    const int32_t h0 = dc.hi_limb[l][0], h1 = dc.hi_limb[l][1], h2 = dc.hi_limb[l][2];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const double er = double(int8_t(wr >> (8 * q)));
-      const double ei = double(int8_t(wi >> (8 * q)));
-      s1r[q] = __dadd_rn(s1r[q], __dmul_rn(ch, er));
-      s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, er));
-      s1i[q] = __dadd_rn(s1i[q], __dmul_rn(ch, ei));
-      s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, ei));
+      const int32_t er = int32_t(int8_t(wr >> (8 * q)));
+      const int32_t ei = int32_t(int8_t(wi >> (8 * q)));
+      if constexpr (LIMBS) {
+        tr[0][q] += h0 * er; tr[1][q] += h1 * er; tr[2][q] += h2 * er;
+        ti[0][q] += h0 * ei; ti[1][q] += h1 * ei; ti[2][q] += h2 * ei;
+      } else {
+        s1r[q] = __dadd_rn(s1r[q], __dmul_rn(dc.coeff_hi[l], double(er)));
+        s1i[q] = __dadd_rn(s1i[q], __dmul_rn(dc.coeff_hi[l], double(ei)));
+      }
+      s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, double(er)));
+      s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, double(ei)));
+    }
+  }
+  if constexpr (LIMBS) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t ir = (int64_t(tr[2][q]) << 32) + (int64_t(tr[1][q]) << 16) + tr[0][q];
+      const int64_t ii = (int64_t(ti[2][q]) << 32) + (int64_t(ti[1][q]) << 16) + ti[0][q];
+      s1r[q] = __dmul_rn(double(ir), dc.hi_scale);  // exact
+      s1i[q] = __dmul_rn(double(ii), dc.hi_scale);
     }
   }
   const int32_t mi = mu[i];
@@ -122,8 +149,8 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
     if (j >= n) break;
     const int ex = -mi - nu[j];
     if (SINGLE) {
-      const double cr = reduce_single(__dadd_rn(s1r[q], s2r[q]), dc.p_hi, dc.p_lo);
-      const double ci = reduce_single(__dadd_rn(s1i[q], s2i[q]), dc.p_hi, dc.p_lo);
+      const double cr = reduce_single(__dadd_rn(s1r[q], s2r[q]), dc);
+      const double ci = reduce_single(__dadd_rn(s1i[q], s2i[q]), dc);
       const float re = __double2float_rn(ldexp_rn(cr, ex));
       const float im = __double2float_rn(ldexp_rn(ci, ex));
       const float xr = __fsub_rn(__fmul_rn(0.0f, im), 0.0f);
@@ -133,8 +160,8 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
       o.y = __fadd_rn(0.0f, xi);
       reinterpret_cast<float2*>(C)[i * ldc + j] = o;
     } else {
-      const double re = ldexp_rn(reduce_double(s1r[q], s2r[q], dc.p_hi, dc.p_lo), ex);
-      const double im = ldexp_rn(reduce_double(s1i[q], s2i[q], dc.p_hi, dc.p_lo), ex);
+      const double re = ldexp_rn(reduce_double(s1r[q], s2r[q], dc), ex);
+      const double im = ldexp_rn(reduce_double(s1i[q], s2i[q], dc), ex);
       const double xr = __dsub_rn(__dmul_rn(0.0, im), 0.0);
       const double xi = __dadd_rn(0.0, im);
       double2 o;
@@ -153,10 +180,14 @@ int launch_crt(bool single, int64_t m, int64_t n, const int8_t* e_re, const int8
   const int64_t total = m * ((n + 3) / 4);
   if (total <= 0) return 0;
   const unsigned grid = unsigned((total + 255) / 256);
-  if (single)
-    k_crt<true><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
-  else
-    k_crt<false><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
+  const bool limbs = dc.hi_scale != 0.0;
+  if (single) {
+    if (limbs) k_crt<true, true><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
+    else k_crt<true, false><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
+  } else {
+    if (limbs) k_crt<false, true><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
+    else k_crt<false, false><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
+  }
   return int(cudaGetLastError());
 }
 

@@ -186,16 +186,25 @@ struct Val3 {
   uint32_t hi, lh, ll;
 };
 
-// x integer-valued, |x| < 2^90 -> v = 2^53 + sign*M (M < 2^53), shift s
-__device__ __forceinline__ Val3 split_value(double x) {
-  double a = fabs(x);
+// q integer-valued, |q| < 2^90 -> v = 2^53 + sign*M (M < 2^53), shift s, read
+// straight from the IEEE bit pattern (no FP conversions):
+//   q = 1.f * 2^e2  ->  M = (2^52 | f) >> (52 - e2)  (e2 <= 52),  s = 0
+//                       M = (2^52 | f),  s = e2 - 52         (e2 >  52)
+__device__ __forceinline__ Val3 split_value(double q) {
+  const uint64_t bits = uint64_t(__double_as_longlong(q));
+  const int e2 = int((bits >> 52) & 0x7FF) - 1023;
+  const uint64_t sig = (bits & 0xFFFFFFFFFFFFFull) | (uint64_t(1) << 52);
+  uint64_t M;
   uint32_t s = 0;
-  if (a >= 9007199254740992.0) {
-    s = uint32_t(ilogb(a) - 52);
-    a = ldexp(a, -int(s));
+  if (e2 < 0) {
+    M = 0;
+  } else if (e2 <= 52) {
+    M = sig >> (52 - e2);
+  } else {
+    M = sig;
+    s = uint32_t(e2 - 52);
   }
-  const uint64_t M = uint64_t(a);
-  const uint64_t v = x < 0.0 ? (uint64_t(1) << 53) - M : (uint64_t(1) << 53) + M;
+  const uint64_t v = (bits >> 63) ? (uint64_t(1) << 53) - M : (uint64_t(1) << 53) + M;
   return {uint32_t(v >> 32) | (s << 24), uint32_t(v) >> 16, uint32_t(v) & 0xFFFFu};
 }
 
@@ -276,6 +285,10 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
   const int h0 = kb * 128 + seg * 8;
   const bool row_ok = row < rows;
   const int e = row_ok ? exps[row] : 0;
+  // 2^e for e in [-1023, 1023] is representable (2^-1023 subnormal): one
+  // correctly rounded multiply == np.ldexp
+  const double scale = __longlong_as_double(e >= -1022 ? int64_t(e + 1023) << 52
+                                                       : int64_t(1) << (e + 1074));
 
   Val3 vr[8], vi[8];
   int bad = 0;
@@ -288,8 +301,8 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
                                   : X + 2 * (int64_t(h) * ldx + col0 + row);
       load_c<T>(p, re, im);
     }
-    double qr = trunc(ldexp_rn(re, e));
-    double qi = trunc(ldexp_rn(im, e));
+    double qr = trunc(__dmul_rn(re, scale));
+    double qi = trunc(__dmul_rn(im, scale));
     if (!(fabs(qr) < 0x1p90)) { bad = 1; qr = 0.0; }
     if (!(fabs(qi) < 0x1p90)) { bad = 1; qi = 0.0; }
     vr[t] = split_value(qr);

@@ -355,7 +355,15 @@ def quantized_residues(mat, exps, ms: ModulusSet, axis: int = 0):
         raise ConfigError("axis must be 0 (rows) or 1 (columns)")
     if exps_np.shape[0] != xt.shape[axis]:
         raise DimensionError("exponent vector does not match matrix")
-    et = torch.from_numpy(np.clip(exps_np, -2 ** 31, 2 ** 31 - 1).astype(np.int32)).to(dev)
+    # np.ldexp semantics outside the kernel's exact-multiply range: 2^e with
+    # e > 1023 overflows any nonzero entry (DomainError in quantize), e < -1074
+    # flushes every entry to zero
+    big = exps_np > 1023
+    if big.any():
+        xs = xt.abs().amax(dim=1 if axis == 0 else 0).cpu().numpy()
+        if np.any(xs[big] != 0):
+            raise DomainError("scaled magnitudes exceed the quantization budget")
+    et = torch.from_numpy(np.clip(exps_np, -1074, 1023).astype(np.int32)).to(dev)
     rows, kdim = (xt.shape[0], xt.shape[1]) if axis == 0 else (xt.shape[1], xt.shape[0])
     consts = device_constants(len(ms))
     nmod = len(ms)
