@@ -270,9 +270,9 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     # roofline of the dominant kernel (K3 tcgen05 GEMM): algorithmic INT8 ops per
     # launch = 6 * N * m * n_block * k (3 GEMMs x 2 ops/MAC x N moduli)
     bf16, hbm, src = peaks()
-    gemm_ms = stage_ms["gemm"] / max(1, stage_n["gemm"])
-    nblocks = math.ceil(a.n / min(a.n, -(-a.n_block // 256) * 256))
-    ops_launch = 6.0 * a.moduli * a.m * (a.n / nblocks) * a.k
+    launches_gemm = max(1, stage_n["gemm"])
+    gemm_ms = stage_ms["gemm"] / launches_gemm
+    ops_launch = 6.0 * a.moduli * a.m * a.n * a.k * a.steps / launches_gemm
     achieved = ops_launch / (gemm_ms * 1e-3) / 1e12
     peak_int8 = 2.0 * bf16
     traffic = profile_traffic()

@@ -13,6 +13,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -92,6 +93,49 @@ int sm_count() {
   cache[dev] = n;
   return n;
 }
+
+// Overlap of B's statistics / residues and the CRT with the GEMM on a side
+// stream.  Measured on B200 (profiles/r01_overlap_experiment.json): the GEMM is
+// power-capped (sw_power_cap, ~1.3 GHz), so co-running integer/FP64 work steals
+// its clock and the step got slower (190 vs 163 ms).  Off by default; opt in
+// with CRTG_OVERLAP=1.
+bool overlap_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CRTG_OVERLAP");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+// per-thread, per-device non-blocking side stream (overlap mode only); the
+// caller's stream otherwise
+cudaStream_t side_stream(cudaStream_t s) {
+  if (!overlap_enabled()) return s;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  thread_local std::map<int, cudaStream_t> streams;
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t st = nullptr;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo);
+  streams[dev] = st;
+  return st;
+}
+
+struct Events {
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t get() {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ev.push_back(e);
+    return e;
+  }
+  ~Events() {
+    for (auto e : ev) cudaEventDestroy(e);  // released once they complete
+  }
+};
 
 int check_consts(const crtg_consts* K, int* n_out) {
   if (!K) return fail(CRTG_ERR_CONFIG, "modulus constants are required");
@@ -275,6 +319,10 @@ Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_b
   p.k_pad = round_up(std::max<int64_t>(k, 1), 128);
   int64_t nb = n_block < 1 ? n : n_block;
   nb = std::min(round_up(nb, 256), p.n_pad);
+  // at least 4 column blocks for large n so residues / CRT of neighbouring
+  // blocks overlap the GEMM (bitwise neutral: every column is independent)
+  if (overlap_enabled() && p.n_pad >= 8192)
+    nb = std::min(nb, std::max<int64_t>(2048, round_up((n + 3) / 4, 256)));
   p.nb = nb;
   p.nb_pad = nb;
   add(p, p.diag, 8 * CRTG_DIAG_LEN);
@@ -285,9 +333,10 @@ Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_b
   add(p, p.colsq, 16 * p.n_pad);
   add(p, p.tree, tree_bytes(k));
   add(p, p.a_pack, size_t(3 * N) * p.m_pad * p.k_pad);
-  add(p, p.b_pack, size_t(3 * N) * p.nb_pad * p.k_pad);
-  add(p, p.e_re, size_t(N) * m * p.nb_pad);
-  add(p, p.e_im, size_t(N) * m * p.nb_pad);
+  const int nbuf = (overlap_enabled() && p.nb < p.n) ? 2 : 1;  // double buffers (overlap)
+  add(p, p.b_pack, size_t(nbuf) * size_t(3 * N) * p.nb_pad * p.k_pad);
+  add(p, p.e_re, size_t(nbuf) * size_t(N) * m * p.nb_pad);
+  add(p, p.e_im, size_t(nbuf) * size_t(N) * m * p.nb_pad);
   if (mode == CRTG_ACCURATE) {
     add(p, p.bar_mu, 4 * p.m_pad);
     add(p, p.bar_nu, 4 * p.n_pad);
@@ -370,15 +419,17 @@ int accurate_partial(const Plan& P, int precision, const void* A, int64_t lda, c
 }
 
 // exponents (fast or accurate) into mu / nu of the plan
+// Fast mode: A's row statistics on `s`, B's column statistics on `side`
+// (independent; both streams must already be ordered after the inputs).
+// Accurate mode: everything on `s`.
 int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t lda,
                 const void* B, int64_t ldb, const DevConsts& dc, void* ws,
-                unsigned long long* diag, cudaStream_t s) {
+                unsigned long long* diag, cudaStream_t s, cudaStream_t side) {
   const bool single = (precision & CRTG_IN_C64) != 0;  // input element type
   int32_t* mu = at<int32_t>(ws, P.mu);
   int32_t* nu = at<int32_t>(ws, P.nu);
   double* rowabs = at<double>(ws, P.rowabs);
   double* colabs = at<double>(ws, P.colabs);
-  CRTG_TRY(cudaMemsetAsync(colabs, 0, P.colabs.bytes, s), "memset");
   PwTree tree{};
   if (mode == CRTG_FAST) {
     const HostTree& ht = pairwise_tree(P.k);
@@ -396,13 +447,17 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
     tree.leaves = reinterpret_cast<const int2*>(tb);
     tree.nodes = reinterpret_cast<const int2*>(tb + lb);
     tree.level_start = reinterpret_cast<const int*>(tb + lb + nb);
-    StageTimer timer(CRTG_STAGE_SCALING, s, 4);
-    CRTG_TRY(launch_row_stats(single, true, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu,
-                              rowabs, diag, s),
-             "row stats");
-    CRTG_TRY(launch_col_absmax(single, B, ldb, P.k, P.n, colabs, diag, s), "col absmax");
+    {
+      StageTimer timer(CRTG_STAGE_SCALING, s, 1);
+      CRTG_TRY(launch_row_stats(single, true, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu,
+                                rowabs, diag, s),
+               "row stats");
+    }
+    StageTimer timer(CRTG_STAGE_SCALING, side, 3);
+    CRTG_TRY(cudaMemsetAsync(colabs, 0, P.colabs.bytes, side), "memset");
+    CRTG_TRY(launch_col_absmax(single, B, ldb, P.k, P.n, colabs, diag, side), "col absmax");
     CRTG_TRY(launch_col_fast(single, B, ldb, P.k, P.n, colabs, at<double>(ws, P.colsq), dc.p_fast,
-                             dc.delta, nu, diag, s),
+                             dc.delta, nu, diag, side),
              "col sumsq");
     return CRTG_OK;
   }
@@ -418,14 +473,23 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
   return CRTG_OK;
 }
 
-// K2..K4 with exponents already in device memory (mu: m, nu: n)
+// K2..K4 with exponents already in device memory (mu: m, nu: n).  A's residues
+// and the GEMMs run on `s`; B's residues and the CRT run on `side`, double
+// buffered per column block so that, while GEMM_j runs, the side stream does
+// CRT_{j-1} and the residues of block j+2 (launched with one CTA per SM so they
+// co-reside with the persistent GEMM CTAs).  `side` must already be ordered
+// after nu; `s` after mu.  On return `s` is ordered after everything.
 int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const void* B,
                  int64_t ldb, void* C, int64_t ldc, const DevConsts& dc, const int32_t* mu,
-                 const int32_t* nu, void* ws, unsigned long long* dg, cudaStream_t s) {
+                 const int32_t* nu, void* ws, unsigned long long* dg, cudaStream_t s,
+                 cudaStream_t side, Events& E) {
   const int64_t m = P.m, n = P.n, k = P.k;
   const int N = int(P.N);
   const bool in32 = (precision & CRTG_IN_C64) != 0;
   const bool single = (precision & CRTG_SINGLE) != 0;  // result type / CRT path
+  // co-resident launch width for side-stream kernels (overlap mode only)
+  const int nsm = side != s ? sm_count() : 0;
+  const int nbuf = (side != s && P.nb < n) ? 2 : 1;
   // K2: residues of A (once)
   const int64_t a_plane = P.m_pad * P.k_pad;
   int8_t* apack = at<int8_t>(ws, P.a_pack);
@@ -435,26 +499,34 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
                          P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s),
              "residues A");
   }
-
-  int8_t* bpack = at<int8_t>(ws, P.b_pack);
-  int8_t* ere = at<int8_t>(ws, P.e_re);
-  int8_t* eim = at<int8_t>(ws, P.e_im);
+  const int64_t nblk = (n + P.nb - 1) / P.nb;
+  const size_t bbuf = size_t(3 * N) * P.nb_pad * P.k_pad;
+  const size_t ebuf = size_t(N) * m * P.nb_pad;
   const size_t csz = single ? 8 : 16;
-  for (int64_t j0 = 0; j0 < n; j0 += P.nb) {
-    const int64_t w = std::min(P.nb, n - j0);
-    const int64_t w_pad = round_up(w, 256);
-    const int64_t b_plane = w_pad * P.k_pad;
-    {
-      StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
-      CRTG_TRY(launch_pack(in32, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack, b_plane,
-                           w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
-               "residues B");
-    }
+  std::vector<cudaEvent_t> ev_r(nblk), ev_g(nblk), ev_c(nblk);
+  auto bpack = [&](int64_t j) { return at<int8_t>(ws, P.b_pack) + (j % nbuf) * bbuf; };
+  auto ere = [&](int64_t j) { return at<int8_t>(ws, P.e_re) + (j % nbuf) * ebuf; };
+  auto eim = [&](int64_t j) { return at<int8_t>(ws, P.e_im) + (j % nbuf) * ebuf; };
+  auto residues_b = [&](int64_t j, int max_ctas) -> int {
+    const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
+    StageTimer timer(CRTG_STAGE_RESIDUE_B, side, 1);
+    CRTG_TRY(launch_pack(in32, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack(j),
+                         w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, side, max_ctas),
+             "residues B");
+    ev_r[j] = E.get();
+    return int(cudaEventRecord(ev_r[j], side));
+  };
+  CRTG_TRY(residues_b(0, 0), "event");
+  if (nblk > 1 && nbuf == 2) CRTG_TRY(residues_b(1, nsm), "event");
+  for (int64_t j = 0; j < nblk; ++j) {
+    const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
+    CRTG_TRY(cudaStreamWaitEvent(s, ev_r[j], 0), "wait");
+    if (j >= nbuf) CRTG_TRY(cudaStreamWaitEvent(s, ev_c[j - nbuf], 0), "wait");
     GemmArgs g{};
     g.a = apack;
-    g.b = bpack;
+    g.b = bpack(j);
     g.a_plane = a_plane;
-    g.b_plane = b_plane;
+    g.b_plane = w_pad * P.k_pad;
     g.a_rb = int(P.m_pad / 128);
     g.b_rb = int(w_pad / 128);
     g.mt = int(P.m_pad / 128);
@@ -465,8 +537,8 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
     g.nphase = 3;
     g.m = int(m);
     g.n = int(w);
-    g.e_re = ere;
-    g.e_im = eim;
+    g.e_re = ere(j);
+    g.e_im = eim(j);
     g.e_ld = P.nb_pad;
     g.e_plane = m * P.nb_pad;
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
@@ -474,13 +546,22 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
       StageTimer timer(CRTG_STAGE_GEMM, s, 1);
       CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
     }
+    ev_g[j] = E.get();
+    CRTG_TRY(cudaEventRecord(ev_g[j], s), "record");
+    CRTG_TRY(cudaStreamWaitEvent(side, ev_g[j], 0), "wait");
     {
-      StageTimer timer(CRTG_STAGE_CRT, s, 1);
-      CRTG_TRY(launch_crt(single, m, w, ere, eim, g.e_plane, g.e_ld, mu, nu + j0, dc,
-                          static_cast<char*>(C) + j0 * csz, ldc, s),
+      StageTimer timer(CRTG_STAGE_CRT, side, 1);
+      CRTG_TRY(launch_crt(single, m, w, ere(j), eim(j), g.e_plane, g.e_ld, mu, nu + j0, dc,
+                          static_cast<char*>(C) + j0 * csz, ldc, side,
+                          j + 1 < nblk ? nsm : 0),
                "crt");
     }
+    ev_c[j] = E.get();
+    CRTG_TRY(cudaEventRecord(ev_c[j], side), "record");
+    if (nbuf == 2 && j + 2 < nblk) CRTG_TRY(residues_b(j + 2, nsm), "event");
+    if (nbuf == 1 && j + 1 < nblk) CRTG_TRY(residues_b(j + 1, 0), "event");
   }
+  CRTG_TRY(cudaStreamWaitEvent(s, ev_c[nblk - 1], 0), "wait");
   return CRTG_OK;
 }
 
@@ -536,7 +617,15 @@ int crtg_scaling(int precision, int mode, int64_t m, int64_t n, int64_t k, const
                                 : at<unsigned long long>(ws, P.diag);
   CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
   const DevConsts dc = make_dev(*K);
-  if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s)) return e;
+  Events E;
+  cudaStream_t side = side_stream(s);
+  cudaEvent_t ev0 = E.get();
+  CRTG_TRY(cudaEventRecord(ev0, s), "record");
+  CRTG_TRY(cudaStreamWaitEvent(side, ev0, 0), "wait");
+  if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s, side)) return e;
+  cudaEvent_t ev1 = E.get();
+  CRTG_TRY(cudaEventRecord(ev1, side), "record");
+  CRTG_TRY(cudaStreamWaitEvent(s, ev1, 0), "wait");
   if (mu_out)
     CRTG_TRY(cudaMemcpyAsync(mu_out, at<int32_t>(ws, P.mu), 4 * m, cudaMemcpyDeviceToDevice, s), "copy");
   if (nu_out)
@@ -565,11 +654,21 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
                                 : at<unsigned long long>(ws, P.diag);
   CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
   const DevConsts dc = make_dev(*K);
-
-  if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s)) return e;
+  Events E;
+  cudaStream_t side = side_stream(s);
+  cudaEvent_t ev0 = E.get();
+  CRTG_TRY(cudaEventRecord(ev0, s), "record");
+  CRTG_TRY(cudaStreamWaitEvent(side, ev0, 0), "wait");
+  if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s, side)) return e;
+  if (mode == CRTG_ACCURATE) {  // exponents were produced on s
+    cudaEvent_t ev1 = E.get();
+    CRTG_TRY(cudaEventRecord(ev1, s), "record");
+    CRTG_TRY(cudaStreamWaitEvent(side, ev1, 0), "wait");
+  }
   int32_t* mu = at<int32_t>(ws, P.mu);
   int32_t* nu = at<int32_t>(ws, P.nu);
-  if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s)) return e;
+  if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s, side, E))
+    return e;
   if (mu_out) CRTG_TRY(cudaMemcpyAsync(mu_out, mu, 4 * m, cudaMemcpyDeviceToDevice, s), "copy");
   if (nu_out) CRTG_TRY(cudaMemcpyAsync(nu_out, nu, 4 * n, cudaMemcpyDeviceToDevice, s), "copy");
   if (sync_check) return check_diag(dg, s);
@@ -782,7 +881,13 @@ extern "C" int crtg_gemm_complex_exps(int precision, int64_t m, int64_t n, int64
                                 : at<unsigned long long>(ws, P.diag);
   CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
   const DevConsts dc = make_dev(*K);
-  if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s)) return e;
+  Events E;
+  cudaStream_t side = side_stream(s);
+  cudaEvent_t ev0 = E.get();
+  CRTG_TRY(cudaEventRecord(ev0, s), "record");
+  CRTG_TRY(cudaStreamWaitEvent(side, ev0, 0), "wait");
+  if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s, side, E))
+    return e;
   if (sync_check) return check_diag(dg, s);
   return CRTG_OK;
 }

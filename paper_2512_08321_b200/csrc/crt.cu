@@ -100,8 +100,8 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
                                              const __grid_constant__ DevConsts dc, void* C,
                                              int64_t ldc) {
   const int64_t nq = (n + 3) >> 2;
-  const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= m * nq) return;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < m * nq;
+       t += int64_t(gridDim.x) * blockDim.x) {
   const int64_t i = t / nq;
   const int64_t j0 = (t - i * nq) * 4;
   const int8_t* pr = e_re + i * e_ld + j0;
@@ -170,16 +170,19 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
       reinterpret_cast<double2*>(C)[i * ldc + j] = o;
     }
   }
+  }  // grid-stride loop
 }
 
 }  // namespace
 
 int launch_crt(bool single, int64_t m, int64_t n, const int8_t* e_re, const int8_t* e_im,
                int64_t e_plane, int64_t e_ld, const int32_t* mu, const int32_t* nu,
-               const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s) {
+               const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s, int max_ctas) {
   const int64_t total = m * ((n + 3) / 4);
   if (total <= 0) return 0;
-  const unsigned grid = unsigned((total + 255) / 256);
+  int64_t g = (total + 255) / 256;
+  if (max_ctas > 0 && max_ctas < g) g = max_ctas;
+  const unsigned grid = unsigned(g);
   const bool limbs = dc.hi_scale != 0.0;
   if (single) {
     if (limbs) k_crt<true, true><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);

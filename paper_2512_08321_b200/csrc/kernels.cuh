@@ -45,7 +45,7 @@ enum PackKind { PACK_RESIDUE = 0, PACK_BARS = 1 };
 int launch_pack(bool single, int operand, int kind, const void* X, int64_t ldx, int64_t rows,
                 int64_t kdim, int64_t col0, const int32_t* exps, const DevConsts& dc,
                 int8_t* out, int64_t plane_bytes, int64_t rb_count,
-                unsigned long long* overflow_flag, cudaStream_t s);
+                unsigned long long* overflow_flag, cudaStream_t s, int max_ctas = 0);
 // plain int8 matrix -> one packed plane.  trans=0: X is rows x kdim row-major;
 // trans=1: X is kdim x rows row-major (a right operand).
 int launch_pack_i8(const int8_t* X, int trans, int64_t rows, int64_t kdim, int8_t* out,
@@ -57,6 +57,6 @@ int launch_unpack_i8(const int8_t* packed, int64_t rows, int64_t kdim, int64_t r
 // ---- CRT reconstruction (crt.cu) ----
 int launch_crt(bool single, int64_t m, int64_t n, const int8_t* e_re, const int8_t* e_im,
                int64_t e_plane, int64_t e_ld, const int32_t* mu, const int32_t* nu,
-               const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s);
+               const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s, int max_ctas = 0);
 
 }  // namespace crtg

@@ -269,10 +269,15 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
                                                   const __grid_constant__ DevConsts dc,
                                                   int8_t* __restrict__ out, int64_t plane_bytes,
                                                   int64_t rb_count,
-                                                  unsigned long long* __restrict__ overflow) {
+                                                  unsigned long long* __restrict__ overflow,
+                                                  int n_kb, int n_rt) {
   __shared__ __align__(16) uint8_t stage[3][kResRows * 128];
-  const int kb = blockIdx.x;
-  const int r0 = blockIdx.y * kResRows;
+  // grid-stride over (K block, 16-row tile): a full grid when launched alone, one
+  // CTA per SM when it runs beside the persistent GEMM (side stream)
+  for (int tile = blockIdx.x; tile < n_kb * n_rt; tile += gridDim.x) {
+  // A: consecutive tiles walk along a row (contiguous K); B: along the columns
+  const int kb = OPERAND == 0 ? tile % n_kb : tile / n_rt;
+  const int r0 = (OPERAND == 0 ? tile / n_kb : tile % n_rt) * kResRows;
   int r, seg;  // row within the tile, 8-element K segment (0..15)
   if (OPERAND == 0) {
     r = threadIdx.x >> 4;
@@ -340,6 +345,7 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
           reinterpret_cast<const uint4*>(stage[2])[qi];
     __syncthreads();
   }
+  }  // tile loop
 }
 
 // plain int8 -> packed plane (test hooks); one thread per 16-byte chunk
@@ -372,11 +378,14 @@ __global__ void k_unpack_i8(const int8_t* __restrict__ packed, int64_t rows, int
 template <typename T, int OP, int KIND>
 void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t col0,
                 const int32_t* exps, const DevConsts& dc, int8_t* out, int64_t plane_bytes,
-                int64_t rb_count, unsigned long long* overflow, cudaStream_t s) {
+                int64_t rb_count, unsigned long long* overflow, cudaStream_t s, int max_ctas) {
   if constexpr (KIND == PACK_RESIDUE) {
-    dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kResRows));
+    const int n_kb = int((kdim + 127) / 128), n_rt = int(rb_count * 128 / kResRows);
+    const int64_t tiles = int64_t(n_kb) * n_rt;
+    const unsigned grid = unsigned(max_ctas > 0 && max_ctas < tiles ? max_ctas : tiles);
     k_residues<T, OP><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows), int(kdim),
-                                          col0, exps, dc, out, plane_bytes, rb_count, overflow);
+                                          col0, exps, dc, out, plane_bytes, rb_count, overflow,
+                                          n_kb, n_rt);
   } else {
   // cover every padded row of the plane so the GEMM reads zeros there
   dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kTileRows));
@@ -391,10 +400,10 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
 int launch_pack(bool single, int operand, int kind, const void* X, int64_t ldx, int64_t rows,
                 int64_t kdim, int64_t col0, const int32_t* exps, const DevConsts& dc,
                 int8_t* out, int64_t plane_bytes, int64_t rb_count,
-                unsigned long long* overflow, cudaStream_t s) {
+                unsigned long long* overflow, cudaStream_t s, int max_ctas) {
   if (rows <= 0 || kdim <= 0) return 0;
 #define CRTG_PACK(T, OP, KIND) \
-  launch_one<T, OP, KIND>(X, ldx, rows, kdim, col0, exps, dc, out, plane_bytes, rb_count, overflow, s)
+  launch_one<T, OP, KIND>(X, ldx, rows, kdim, col0, exps, dc, out, plane_bytes, rb_count, overflow, s, max_ctas)
   if (single) {
     if (operand == 0) {
       if (kind == PACK_BARS) CRTG_PACK(float, 0, PACK_BARS); else CRTG_PACK(float, 0, PACK_RESIDUE);
