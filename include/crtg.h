@@ -108,6 +108,22 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k,
                       void* ws, size_t ws_bytes, int32_t* mu_out, int32_t* nu_out,
                       uint64_t* diag, int sync_check, void* stream);
 
+/*
+ * The same product on HOST buffers (pinned for full overlap): A, B, C are host
+ * pointers; B's column blocks are copied in (copy engine) while the GPU works on
+ * the blocks already resident and finished C blocks are copied back while the
+ * next block computes.  `ws` is a DEVICE workspace of
+ * crtg_host_workspace_size(...) bytes.  On return (stream-ordered) C is complete
+ * once `stream` is synchronized.
+ */
+size_t crtg_host_workspace_size(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                                int num_moduli, int64_t n_block);
+int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                           const void* A, int64_t lda, const void* B, int64_t ldb,
+                           void* C, int64_t ldc, const crtg_consts* K, int64_t n_block,
+                           void* ws, size_t ws_bytes, uint64_t* diag, int sync_check,
+                           void* stream);
+
 /* ---- multi-GPU building blocks (output-tile sharding) ---- */
 
 /* The K2..K4 pipeline with caller-provided exponents (device int32 mu[m],

@@ -43,6 +43,10 @@ SIGNATURES = {
                                        _vp, _vp, _sz, _vp]),
     "crtg_crt_reconstruct": (_c_int, [_c_int, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp,
                                       _c_i64, _vp]),
+    "crtg_host_workspace_size": (_sz, [_c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_i64]),
+    "crtg_gemm_complex_host": (_c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp,
+                                        _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _sz, _vp, _c_int,
+                                        _vp]),
     "crtg_gemm_complex_exps": (_c_int, [_c_int, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp,
                                         _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _vp, _vp, _sz,
                                         _vp, _c_int, _vp]),

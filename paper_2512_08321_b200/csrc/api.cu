@@ -935,3 +935,227 @@ extern "C" int crtg_accurate_exponents(int64_t count, const int32_t* maxb, const
            "accurate exponents");
   return CRTG_OK;
 }
+
+namespace {
+// per-thread, per-device copy-engine streams for the host-buffer entry
+cudaStream_t copy_stream(int which) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  thread_local std::map<int, cudaStream_t> streams[2];
+  auto it = streams[which].find(dev);
+  if (it != streams[which].end()) return it->second;
+  cudaStream_t st = nullptr;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  streams[which][dev] = st;
+  return st;
+}
+}  // namespace
+
+// host-entry chunking: A in row chunks (multiples of 128 rows), B in column
+// blocks, so the first GEMM starts once one chunk of each has arrived
+struct HostChunks {
+  int64_t rows;  // rows per A chunk
+  int64_t cols;  // columns per B block (= plan nb)
+};
+
+HostChunks host_chunks(const Plan& P) {
+  HostChunks h;
+  h.rows = P.m >= 2048 ? round_up((P.m + 3) / 4, 128) : P.m;
+  h.cols = P.nb;
+  return h;
+}
+
+Plan host_plan(int mode, int64_t m, int64_t n, int64_t k, int N, int64_t n_block) {
+  // column blocks of at most n/4 (>= 1024) so transfers and compute interleave
+  int64_t nb = n_block < 1 ? n : n_block;
+  if (n >= 4096) nb = std::min(nb, std::max<int64_t>(1024, round_up((n + 3) / 4, 256)));
+  return make_plan(mode, m, n, k, N, nb);
+}
+
+extern "C" size_t crtg_host_workspace_size(int precision, int mode, int64_t m, int64_t n,
+                                           int64_t k, int num_moduli, int64_t n_block) {
+  const Plan P = host_plan(mode, m, n, k, num_moduli, n_block);
+  const HostChunks hc = host_chunks(P);
+  const size_t esz = (precision & CRTG_IN_C64) ? 8 : 16;
+  const size_t csz = (precision & CRTG_SINGLE) ? 8 : 16;
+  auto r = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return P.total + r(size_t(m) * k * esz) + r(size_t(k) * n * esz) +
+         2 * r(size_t(hc.rows) * P.nb * csz);
+}
+
+// End-to-end entry on HOST buffers (pinned for full overlap).  Transfers are
+// ordered A_0, B_0, A_1 .. A_last, B_1 .. B_last on a copy-engine stream; the
+// GEMM of tile (A chunk i, B block j) starts as soon as both are resident and
+// each finished C tile goes back on a second copy stream while the next tile
+// computes.  Fast mode computes the statistics per chunk/block (they are row /
+// column local); accurate mode needs every bound maximum first and so waits for
+// all inputs before its exponents.
+extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                                      const void* A, int64_t lda, const void* B, int64_t ldb,
+                                      void* C, int64_t ldc, const crtg_consts* K, int64_t n_block,
+                                      void* ws, size_t ws_bytes, uint64_t* diag, int sync_check,
+                                      void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if ((precision & ~(CRTG_SINGLE | CRTG_IN_C64)) != 0)
+    return fail(CRTG_ERR_CONFIG, "precision must be double or single");
+  if (mode != CRTG_FAST && mode != CRTG_ACCURATE) return fail(CRTG_ERR_CONFIG, "bad mode");
+  if (int e = check_dims(m, n, k, lda, ldb, ldc)) return e;
+  const Plan P = host_plan(mode, m, n, k, N, n_block);
+  const HostChunks hc = host_chunks(P);
+  if (!ws || ws_bytes < crtg_host_workspace_size(precision, mode, m, n, k, N, n_block))
+    return fail(CRTG_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t h2d = copy_stream(0), d2h = copy_stream(1);
+  const bool in32 = (precision & CRTG_IN_C64) != 0;
+  const bool single = (precision & CRTG_SINGLE) != 0;
+  const size_t esz = in32 ? 8 : 16, csz = single ? 8 : 16;
+  auto r = [](size_t x) { return (x + 255) & ~size_t(255); };
+  char* dA = static_cast<char*>(ws) + P.total;
+  char* dB = dA + r(size_t(m) * k * esz);
+  char* dC = dB + r(size_t(k) * n * esz);
+  const size_t cbuf = r(size_t(hc.rows) * P.nb * csz);
+  unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
+                                : at<unsigned long long>(ws, P.diag);
+  const DevConsts dc = make_dev(*K);
+  Events E;
+  cudaEvent_t ev0 = E.get();
+  CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
+  CRTG_TRY(cudaMemsetAsync(at<double>(ws, P.colabs), 0, P.colabs.bytes, s), "memset");
+  CRTG_TRY(cudaEventRecord(ev0, s), "record");
+  CRTG_TRY(cudaStreamWaitEvent(h2d, ev0, 0), "wait");
+  CRTG_TRY(cudaStreamWaitEvent(d2h, ev0, 0), "wait");
+
+  const int64_t nrc = (m + hc.rows - 1) / hc.rows;
+  const int64_t nblk = (n + P.nb - 1) / P.nb;
+  std::vector<cudaEvent_t> evA(nrc), evB(nblk);
+  auto copy_a = [&](int64_t i) -> int {
+    const int64_t i0 = i * hc.rows, h = std::min(hc.rows, m - i0);
+    CRTG_TRY(cudaMemcpy2DAsync(dA + size_t(i0) * k * esz, k * esz,
+                               static_cast<const char*>(A) + size_t(i0) * lda * esz, lda * esz,
+                               k * esz, h, cudaMemcpyHostToDevice, h2d),
+             "H2D A");
+    evA[i] = E.get();
+    return int(cudaEventRecord(evA[i], h2d));
+  };
+  auto copy_b = [&](int64_t j) -> int {
+    const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0);
+    CRTG_TRY(cudaMemcpy2DAsync(dB + j0 * esz, n * esz, static_cast<const char*>(B) + j0 * esz,
+                               ldb * esz, w * esz, k, cudaMemcpyHostToDevice, h2d),
+             "H2D B");
+    evB[j] = E.get();
+    return int(cudaEventRecord(evB[j], h2d));
+  };
+  CRTG_TRY(copy_a(0), "record");
+  CRTG_TRY(copy_b(0), "record");
+  for (int64_t i = 1; i < nrc; ++i) CRTG_TRY(copy_a(i), "record");
+  for (int64_t j = 1; j < nblk; ++j) CRTG_TRY(copy_b(j), "record");
+
+  int32_t* mu = at<int32_t>(ws, P.mu);
+  int32_t* nu = at<int32_t>(ws, P.nu);
+  PwTree tree{};
+  if (mode == CRTG_ACCURATE) {
+    CRTG_TRY(cudaStreamWaitEvent(s, evA[nrc - 1], 0), "wait");
+    CRTG_TRY(cudaStreamWaitEvent(s, evB[nblk - 1], 0), "wait");
+    if (int e = run_scaling(P, precision, mode, dA, k, dB, n, dc, ws, dg, s, s)) return e;
+  } else {
+    const HostTree& ht = pairwise_tree(P.k);
+    char* tb = at<char>(ws, P.tree);
+    const size_t lb = ht.leaves.size() * sizeof(int2), nbt = ht.nodes.size() * sizeof(int2),
+                 sb = ht.level_start.size() * sizeof(int);
+    CRTG_TRY(cudaMemcpyAsync(tb, ht.leaves.data(), lb, cudaMemcpyHostToDevice, s), "tree copy");
+    if (nbt) CRTG_TRY(cudaMemcpyAsync(tb + lb, ht.nodes.data(), nbt, cudaMemcpyHostToDevice, s), "tree copy");
+    CRTG_TRY(cudaMemcpyAsync(tb + lb + nbt, ht.level_start.data(), sb, cudaMemcpyHostToDevice, s),
+             "tree copy");
+    tree = PwTree{int(ht.leaves.size()), int(ht.nodes.size()), int(ht.level_start.size()) - 1,
+                  reinterpret_cast<const int2*>(tb), reinterpret_cast<const int2*>(tb + lb),
+                  reinterpret_cast<const int*>(tb + lb + nbt)};
+  }
+  const int64_t a_plane = P.m_pad * P.k_pad;
+  int8_t* apack = at<int8_t>(ws, P.a_pack);
+  int8_t* bpack = at<int8_t>(ws, P.b_pack);
+  std::vector<cudaEvent_t> evD;
+  int64_t tile = 0;
+  for (int64_t j = 0; j < nblk; ++j) {
+    const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
+    for (int64_t i = 0; i < nrc; ++i, ++tile) {
+      const int64_t i0 = i * hc.rows, h = std::min(hc.rows, m - i0);
+      const bool last_rows = i == nrc - 1;
+      if (j == 0) {  // A chunk i: statistics (fast) and residues, once
+        CRTG_TRY(cudaStreamWaitEvent(s, evA[i], 0), "wait");
+        const char* Ai = dA + size_t(i0) * k * esz;
+        if (mode == CRTG_FAST) {
+          StageTimer timer(CRTG_STAGE_SCALING, s, 1);
+          CRTG_TRY(launch_row_stats(in32, true, Ai, k, h, k, tree, dc.p_fast, dc.delta, mu + i0,
+                                    at<double>(ws, P.rowabs) + i0, dg, s),
+                   "row stats");
+        }
+        StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
+        CRTG_TRY(launch_pack(in32, 0, PACK_RESIDUE, Ai, k, h, k, 0, mu + i0, dc, apack, a_plane,
+                             P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s, 0, i0,
+                             last_rows ? P.m_pad - i0 : h),
+                 "residues A");
+      }
+      if (i == 0) {  // B block j: statistics (fast) and residues, once
+        CRTG_TRY(cudaStreamWaitEvent(s, evB[j], 0), "wait");
+        if (mode == CRTG_FAST) {
+          StageTimer timer(CRTG_STAGE_SCALING, s, 3);
+          const char* Bj = dB + j0 * esz;
+          double* cabs = at<double>(ws, P.colabs) + j0;
+          CRTG_TRY(launch_col_absmax(in32, Bj, n, k, w, cabs, dg, s), "col absmax");
+          CRTG_TRY(launch_col_fast(in32, Bj, n, k, w, cabs, at<double>(ws, P.colsq) + 2 * j0,
+                                   dc.p_fast, dc.delta, nu + j0, dg, s),
+                   "col sumsq");
+        }
+        StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
+        CRTG_TRY(launch_pack(in32, 1, PACK_RESIDUE, dB, n, w, k, j0, nu + j0, dc, bpack,
+                             w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
+                 "residues B");
+      }
+      GemmArgs g{};
+      g.a = apack;
+      g.b = bpack;
+      g.a_plane = a_plane;
+      g.b_plane = w_pad * P.k_pad;
+      g.a_rb = int(P.m_pad / 128);
+      g.b_rb = int(w_pad / 128);
+      g.mt0 = int(i0 / 128);
+      g.mt = int((last_rows ? P.m_pad - i0 : h) / 128);
+      g.nt = int(w_pad / 256);
+      g.kb = int(P.k_pad / 128);
+      g.nl = N;
+      g.planes_per_l = 3;
+      g.nphase = 3;
+      g.m = int(i0 + h);
+      g.n = int(w);
+      g.e_re = at<int8_t>(ws, P.e_re);
+      g.e_im = at<int8_t>(ws, P.e_im);
+      g.e_ld = P.nb_pad;
+      g.e_plane = m * P.nb_pad;
+      for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
+      {
+        StageTimer timer(CRTG_STAGE_GEMM, s, 1);
+        CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
+      }
+      if (tile >= 2) CRTG_TRY(cudaStreamWaitEvent(s, evD[tile - 2], 0), "wait");
+      char* cblk = dC + (tile & 1) * cbuf;
+      {
+        StageTimer timer(CRTG_STAGE_CRT, s, 1);
+        CRTG_TRY(launch_crt(single, h, w, g.e_re + i0 * g.e_ld, g.e_im + i0 * g.e_ld, g.e_plane,
+                            g.e_ld, mu + i0, nu + j0, dc, cblk, w, s),
+                 "crt");
+      }
+      cudaEvent_t evC = E.get();
+      CRTG_TRY(cudaEventRecord(evC, s), "record");
+      CRTG_TRY(cudaStreamWaitEvent(d2h, evC, 0), "wait");
+      CRTG_TRY(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(i0) * ldc + j0) * csz, ldc * csz,
+                                 cblk, w * csz, w * csz, h, cudaMemcpyDeviceToHost, d2h),
+               "D2H C");
+      evD.push_back(E.get());
+      CRTG_TRY(cudaEventRecord(evD.back(), d2h), "record");
+    }
+  }
+  CRTG_TRY(cudaStreamWaitEvent(s, evD.back(), 0), "wait");
+  if (sync_check) return check_diag(dg, s);
+  return CRTG_OK;
+}

@@ -64,7 +64,7 @@ __device__ __forceinline__ void decode_tile(int t, const GemmArgs& g, int& l, in
   const int first = grp * kGroupM;
   const int gm = min(kGroupM, g.mt - first);
   const int in = r - grp * kGroupM * g.nt;
-  tm = first + in % gm;
+  tm = first + in % gm + g.mt0;
   tn = in / gm;
 }
 

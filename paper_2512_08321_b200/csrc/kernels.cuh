@@ -45,7 +45,8 @@ enum PackKind { PACK_RESIDUE = 0, PACK_BARS = 1 };
 int launch_pack(bool single, int operand, int kind, const void* X, int64_t ldx, int64_t rows,
                 int64_t kdim, int64_t col0, const int32_t* exps, const DevConsts& dc,
                 int8_t* out, int64_t plane_bytes, int64_t rb_count,
-                unsigned long long* overflow_flag, cudaStream_t s, int max_ctas = 0);
+                unsigned long long* overflow_flag, cudaStream_t s, int max_ctas = 0,
+                int64_t row_base = 0, int64_t fill_rows = 0);
 // plain int8 matrix -> one packed plane.  trans=0: X is rows x kdim row-major;
 // trans=1: X is kdim x rows row-major (a right operand).
 int launch_pack_i8(const int8_t* X, int trans, int64_t rows, int64_t kdim, int8_t* out,

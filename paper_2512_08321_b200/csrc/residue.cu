@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
                                                   int8_t* __restrict__ out, int64_t plane_bytes,
                                                   int64_t rb_count,
                                                   unsigned long long* __restrict__ overflow,
-                                                  int n_kb, int n_rt) {
+                                                  int n_kb, int n_rt, int row_base) {
   __shared__ __align__(16) uint8_t stage[3][kResRows * 128];
   // grid-stride over (K block, 16-row tile): a full grid when launched alone, one
   // CTA per SM when it runs beside the persistent GEMM (side stream)
@@ -322,7 +322,8 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
   const int chunk = seg >> 1;
   const int soff = (r >> 3) * 1024 + (r & 7) * 128 + ((chunk ^ (r & 7)) << 4) + (seg & 1) * 8;
   // the tile's 16 rows form one contiguous 2 KiB run of each packed plane
-  const int64_t goff = (int64_t(kb) * rb_count + (r0 >> 7)) * kBlockBytes + (r0 & 127) * 128;
+  const int gr0 = r0 + row_base;  // row of this tile inside the packed plane
+  const int64_t goff = (int64_t(kb) * rb_count + (gr0 >> 7)) * kBlockBytes + (gr0 & 127) * 128;
   const int q = threadIdx.x >> 7;        // copy-out: plane handled by this half
   const int qi = threadIdx.x & 127;      // 16-byte slot within the 2 KiB run
 
@@ -378,14 +379,18 @@ __global__ void k_unpack_i8(const int8_t* __restrict__ packed, int64_t rows, int
 template <typename T, int OP, int KIND>
 void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t col0,
                 const int32_t* exps, const DevConsts& dc, int8_t* out, int64_t plane_bytes,
-                int64_t rb_count, unsigned long long* overflow, cudaStream_t s, int max_ctas) {
+                int64_t rb_count, unsigned long long* overflow, cudaStream_t s, int max_ctas,
+                int64_t row_base, int64_t fill_rows) {
   if constexpr (KIND == PACK_RESIDUE) {
-    const int n_kb = int((kdim + 127) / 128), n_rt = int(rb_count * 128 / kResRows);
+    // tiles cover the plane from row_base up to fill_rows (the zero padding of
+    // the last chunk included)
+    const int64_t extent = fill_rows > 0 ? fill_rows : rb_count * 128 - row_base;
+    const int n_kb = int((kdim + 127) / 128), n_rt = int((extent + kResRows - 1) / kResRows);
     const int64_t tiles = int64_t(n_kb) * n_rt;
     const unsigned grid = unsigned(max_ctas > 0 && max_ctas < tiles ? max_ctas : tiles);
     k_residues<T, OP><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows), int(kdim),
                                           col0, exps, dc, out, plane_bytes, rb_count, overflow,
-                                          n_kb, n_rt);
+                                          n_kb, n_rt, int(row_base));
   } else {
   // cover every padded row of the plane so the GEMM reads zeros there
   dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kTileRows));
@@ -400,10 +405,11 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
 int launch_pack(bool single, int operand, int kind, const void* X, int64_t ldx, int64_t rows,
                 int64_t kdim, int64_t col0, const int32_t* exps, const DevConsts& dc,
                 int8_t* out, int64_t plane_bytes, int64_t rb_count,
-                unsigned long long* overflow, cudaStream_t s, int max_ctas) {
+                unsigned long long* overflow, cudaStream_t s, int max_ctas, int64_t row_base,
+                int64_t fill_rows) {
   if (rows <= 0 || kdim <= 0) return 0;
 #define CRTG_PACK(T, OP, KIND) \
-  launch_one<T, OP, KIND>(X, ldx, rows, kdim, col0, exps, dc, out, plane_bytes, rb_count, overflow, s, max_ctas)
+  launch_one<T, OP, KIND>(X, ldx, rows, kdim, col0, exps, dc, out, plane_bytes, rb_count, overflow, s, max_ctas, row_base, fill_rows)
   if (single) {
     if (operand == 0) {
       if (kind == PACK_BARS) CRTG_PACK(float, 0, PACK_BARS); else CRTG_PACK(float, 0, PACK_RESIDUE);

@@ -100,18 +100,77 @@ def emulate_gemm_complex(a, b, cfg: EmuConfig | None = None,
     if cfg.domain != "complex":
         raise ConfigError("config domain must be 'complex'")
     dev = _device()
+    on_dev = [isinstance(x, torch.Tensor) and x.is_cuda for x in (a, b)]
+    if not any(on_dev):
+        # host operands: stream them through the copy engines (crtg_gemm_complex_host)
+        ha, a_torch = _host_matrix(a, "A")
+        hb, b_torch = _host_matrix(b, "B")
+        _check_shapes(ha, hb)
+        out = run_complex_host(ha, hb, cfg, diagnostics, dev)
+        return out if (a_torch and b_torch) else out.numpy()
     at, a_torch = _to_device_matrix(a, "A", dev)
     bt, b_torch = _to_device_matrix(b, "B", dev)
-    if at.shape[1] != bt.shape[0]:
-        raise DimensionError(f"inner dimensions differ: {tuple(at.shape)} x {tuple(bt.shape)}")
-    m, k = at.shape
-    n = bt.shape[1]
-    if k > MAX_K_COMPLEX:
-        raise DimensionError(f"inner dimension {k} exceeds {MAX_K_COMPLEX}")
+    _check_shapes(at, bt)
     out = run_complex(at, bt, cfg, diagnostics, dev)
     if a_torch and b_torch:
         return out
     return out.cpu().numpy()
+
+
+def _check_shapes(at, bt):
+    if at.shape[1] != bt.shape[0]:
+        raise DimensionError(f"inner dimensions differ: {tuple(at.shape)} x {tuple(bt.shape)}")
+    if at.shape[1] > MAX_K_COMPLEX:
+        raise DimensionError(f"inner dimension {at.shape[1]} exceeds {MAX_K_COMPLEX}")
+
+
+def _host_matrix(x, name: str):
+    """-> (contiguous pinned CPU complex tensor, was_torch)."""
+    if isinstance(x, torch.Tensor):
+        t = x
+        if t.dim() != 2:
+            raise DimensionError(f"{name} must be 2-D")
+        if t.dtype not in (torch.complex64, torch.complex128):
+            t = t.to(torch.complex128)
+        t = t.contiguous()
+        return (t if t.is_pinned() else t.pin_memory()), True
+    arr = np.asarray(x)
+    if arr.ndim != 2:
+        raise DimensionError(f"{name} must be 2-D")
+    if arr.dtype not in (np.complex64, np.complex128):
+        arr = arr.astype(np.complex128)
+    return torch.from_numpy(np.ascontiguousarray(arr)).pin_memory(), False
+
+
+def run_complex_host(ha: torch.Tensor, hb: torch.Tensor, cfg: EmuConfig,
+                     diagnostics: dict | None = None, dev=None):
+    """Host (pinned) operands in, pinned host result out; H2D of B's column blocks
+    and D2H of C's blocks overlap the GPU work (crtg_gemm_complex_host)."""
+    dev = dev or _device()
+    if ha.dtype != hb.dtype:
+        ha, hb = ha.to(torch.complex128).pin_memory(), hb.to(torch.complex128).pin_memory()
+    m, k = ha.shape
+    n = hb.shape[1]
+    nmod = cfg.resolved_moduli
+    prec = nat.SINGLE if cfg.precision == "single" else nat.DOUBLE
+    if ha.dtype == torch.complex64:
+        prec |= 16
+    mode = nat.FAST if cfg.mode == "fast" else nat.ACCURATE
+    lib = nat.load()
+    ws = _workspace(lib.crtg_host_workspace_size(prec, mode, m, n, k, nmod, cfg.n_block), dev)
+    odt = torch.complex64 if cfg.precision == "single" else torch.complex128
+    out = torch.empty((m, n), dtype=odt, pin_memory=True)
+    diag = torch.zeros(nat.DIAG_LEN, dtype=torch.int64, device=dev)
+    nat.call("crtg_gemm_complex_host", prec, mode, m, n, k, ha.data_ptr(), ha.stride(0),
+             hb.data_ptr(), hb.stride(0), out.data_ptr(), out.stride(0),
+             ctypes.byref(device_constants(nmod)), cfg.n_block, ws.data_ptr(), ws.numel(),
+             diag.data_ptr(), 1, _stream_ptr(dev))
+    if diagnostics is not None:
+        d = diag.cpu().tolist()
+        for key, idx in (("clamped_mu", nat.DIAG_CLAMPED_MU), ("clamped_nu", nat.DIAG_CLAMPED_NU)):
+            if d[idx]:
+                diagnostics[key] = diagnostics.get(key, 0) + int(d[idx])
+    return out
 
 
 def run_complex(at: torch.Tensor, bt: torch.Tensor, cfg: EmuConfig,
