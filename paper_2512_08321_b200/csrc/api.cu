@@ -107,6 +107,26 @@ bool overlap_enabled() {
   return on;
 }
 
+// K3 kernel choice.  Default: the 1-CTA 128x256 kernel (gemm_tc.cu).  The
+// CTA-pair kernel (cta_group::2, 256x256, gemm_pair.cu; CRTG_GEMM=pair) is
+// bit-identical and moves a third less L2->SMEM data, but measured no faster
+// on B200 (148 vs 152 ms/GEMM-step, both at the sw_power_cap clock): the
+// kernel is bound by MAC energy under the 1 kW cap
+// (profiles/r01_gemm_pair_experiment.json).
+bool pair_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CRTG_GEMM");
+    return v && std::string(v) == "pair";
+  }();
+  return on;
+}
+
+int run_gemm(int mode, const GemmArgs& g, cudaStream_t s) {
+  if (pair_enabled() && mode != EPI_BOUND && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
+    return launch_gemm_pair(mode, g, sm_count(), s);
+  return launch_gemm(mode, g, sm_count(), s);
+}
+
 // per-thread, per-device non-blocking side stream (overlap mode only); the
 // caller's stream otherwise
 cudaStream_t side_stream(cudaStream_t s) {
@@ -314,7 +334,7 @@ Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_b
   p.n = n;
   p.k = k;
   p.N = N;
-  p.m_pad = round_up(std::max<int64_t>(m, 1), 128);
+  p.m_pad = round_up(std::max<int64_t>(m, 1), 256);  // even 128-row tiles (CTA pairs)
   p.n_pad = round_up(std::max<int64_t>(n, 1), 256);
   p.k_pad = round_up(std::max<int64_t>(k, 1), 128);
   int64_t nb = n_block < 1 ? n : n_block;
@@ -544,7 +564,7 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
     {
       StageTimer timer(CRTG_STAGE_GEMM, s, 1);
-      CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
+      CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
     }
     ev_g[j] = E.get();
     CRTG_TRY(cudaEventRecord(ev_g[j], s), "record");
@@ -700,7 +720,7 @@ int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim, const 
 }
 
 size_t crtg_i8_workspace_size(int64_t m, int64_t n, int64_t k, int nplanes) {
-  const int64_t m_pad = round_up(m, 128), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
+  const int64_t m_pad = round_up(m, 256), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
   size_t t = 0;
   t += round_up(size_t(nplanes) * m_pad * k_pad, 256);
   t += round_up(size_t(nplanes) * n_pad * k_pad, 256);
@@ -717,7 +737,7 @@ int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A, const int
   if (ws_bytes < crtg_i8_workspace_size(m, n, k, 1))
     return fail(CRTG_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t m_pad = round_up(m, 128), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
+  const int64_t m_pad = round_up(m, 256), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
   int8_t* ap = static_cast<int8_t*>(ws);
   int8_t* bp = ap + round_up(m_pad * k_pad, 256);
   int32_t* raw = reinterpret_cast<int32_t*>(bp + round_up(n_pad * k_pad, 256));
@@ -742,7 +762,7 @@ int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A, const int
   g.raw = raw;
   g.raw_ld = n_pad;
   g.raw_plane = m * n_pad;
-  CRTG_TRY(launch_gemm(EPI_RAW, g, sm_count(), s), "i8 gemm");
+  CRTG_TRY(run_gemm(EPI_RAW, g, s), "i8 gemm");
   CRTG_TRY(cudaMemcpy2DAsync(C, n * 4, raw, n_pad * 4, n * 4, m, cudaMemcpyDeviceToDevice, s),
            "copy out");
   return CRTG_OK;
@@ -770,7 +790,7 @@ extern "C" int crtg_complex_gemm_mod(int64_t m, int64_t n, int64_t k, const int8
   if (ws_bytes < crtg_i8_workspace_size(m, n, k, 3))
     return fail(CRTG_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t m_pad = round_up(m, 128), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
+  const int64_t m_pad = round_up(m, 256), n_pad = round_up(n, 256), k_pad = round_up(k, 128);
   const int64_t a_plane = m_pad * k_pad, b_plane = n_pad * k_pad;
   int8_t* ap = static_cast<int8_t*>(ws);
   int8_t* bp = ap + round_up(3 * a_plane, 256);
@@ -808,7 +828,7 @@ extern "C" int crtg_complex_gemm_mod(int64_t m, int64_t n, int64_t k, const int8
   g.e_ld = n_pad;
   g.e_plane = 0;
   g.mc[0] = mc;
-  CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
+  CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
   CRTG_TRY(cudaMemcpy2DAsync(e_re, n, g.e_re, n_pad, n, m, cudaMemcpyDeviceToDevice, s), "copy");
   CRTG_TRY(cudaMemcpy2DAsync(e_im, n, g.e_im, n_pad, n, m, cudaMemcpyDeviceToDevice, s), "copy");
   return CRTG_OK;
@@ -960,7 +980,7 @@ struct HostChunks {
 
 HostChunks host_chunks(const Plan& P) {
   HostChunks h;
-  h.rows = P.m >= 2048 ? round_up((P.m + 3) / 4, 128) : P.m;
+  h.rows = P.m >= 2048 ? round_up((P.m + 3) / 4, 256) : P.m;
   h.cols = P.nb;
   return h;
 }
@@ -1135,7 +1155,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
       for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
       {
         StageTimer timer(CRTG_STAGE_GEMM, s, 1);
-        CRTG_TRY(launch_gemm(EPI_KARATSUBA, g, sm_count(), s), "karatsuba gemm");
+        CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
       }
       if (tile >= 2) CRTG_TRY(cudaStreamWaitEvent(s, evD[tile - 2], 0), "wait");
       char* cblk = dC + (tile & 1) * cbuf;

@@ -1,0 +1,92 @@
+// gemm_epilogue.cuh — TMEM -> register epilogues shared by the 1-CTA and the
+// CTA-pair tcgen05 GEMMs (gemm_tc.cu, gemm_pair.cu).
+//
+// One thread owns one TMEM lane = one output row of the tile and 256 columns,
+// read in 8 chunks of 32 (tcgen05.ld.32x32b.x32).
+//   KARATSUBA phase 0 (D = Ar*Br): keep D mod p in st[] (packed bytes);
+//   phase 1 (E = Ai*Bi): write e_R = sym(D - E), keep (D + E) mod p;
+//   phase 2 (F = As*Bs): write e_I = sym(F - (D + E))     (kernel.py:45-51).
+//   Reducing D, E, F mod p before combining keeps every value in int32 (the
+//   reference widens to int64, kernel.py:46-50) and gives the same residue.
+//   RAW: store the int32 accumulator (gemm_i8_i32 parity hook).
+#pragma once
+#include "common.cuh"
+#include "gemm_tc.cuh"
+
+namespace crtg {
+
+__device__ __forceinline__ uint32_t ep_pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return (a & 0xFF) | ((b & 0xFF) << 8) | ((c & 0xFF) << 16) | (d << 24);
+}
+
+__device__ __forceinline__ uint32_t ep_byte(uint32_t w, int i) { return (w >> (8 * i)) & 0xFF; }
+
+template <int MODE>
+__device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr, int s, int l,
+                                               int row, bool row_ok, int col_base,
+                                               const ModConst& mc, uint32_t (&st)[64]) {
+  if (MODE == EPI_RAW) {
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      uint32_t v[32];
+      tmem_ld32(taddr + c * 32, v);
+      tmem_wait_ld();
+      if (row_ok) {
+        int32_t* dst = g.raw + (int64_t)s * g.raw_plane + (int64_t)row * g.raw_ld + col_base + c * 32;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+          reinterpret_cast<uint4*>(dst)[w] = make_uint4(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]);
+      }
+    }
+    return;
+  }
+  int8_t* dst_base = nullptr;
+  if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint32_t v[32];
+    tmem_ld32(taddr + c * 32, v);
+    tmem_wait_ld();
+    uint32_t out[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint32_t r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = mod_i32(int32_t(v[4 * w + j]), mc);
+      if (s == 0) {
+        st[c * 8 + w] = ep_pack4(r[0], r[1], r[2], r[3]);
+      } else if (s == 1) {
+        uint32_t o[4], keep[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int32_t dm = int32_t(ep_byte(st[c * 8 + w], j));
+          int32_t x = dm - int32_t(r[j]);
+          x += (x < 0) ? mc.p : 0;
+          o[j] = uint32_t(to_sym(uint32_t(x), mc));
+          int32_t y = dm + int32_t(r[j]);
+          y -= (y >= mc.p) ? mc.p : 0;
+          keep[j] = uint32_t(y);
+        }
+        out[w] = ep_pack4(o[0], o[1], o[2], o[3] & 0xFF);
+        st[c * 8 + w] = ep_pack4(keep[0], keep[1], keep[2], keep[3]);
+      } else {
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          int32_t x = int32_t(r[j]) - int32_t(ep_byte(st[c * 8 + w], j));
+          x += (x < 0) ? mc.p : 0;
+          o[j] = uint32_t(to_sym(uint32_t(x), mc));
+        }
+        out[w] = ep_pack4(o[0], o[1], o[2], o[3] & 0xFF);
+      }
+    }
+    if (s != 0 && row_ok) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst_base + c * 32);
+      d4[0] = make_uint4(out[0], out[1], out[2], out[3]);
+      d4[1] = make_uint4(out[4], out[5], out[6], out[7]);
+    }
+  }
+}
+
+}  // namespace crtg

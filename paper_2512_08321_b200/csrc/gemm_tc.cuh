@@ -34,5 +34,8 @@ struct GemmArgs {
 size_t gemm_smem_bytes();
 // returns a cudaError_t value (0 = success)
 int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream);
+// CTA-pair variant (cta_group::2, 256x256 tiles; KARATSUBA and RAW); g.mt and
+// g.mt0 must be even (rows padded to 256)
+int launch_gemm_pair(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream);
 
 }  // namespace crtg
