@@ -205,11 +205,16 @@ DevConsts make_dev(const crtg_consts& K) {
     rc.magic = mc.magic;
     rc.shift = mc.is_pow2 ? -1 : mc.shift;  // -1 marks p = 256 (mask)
     rc.p = p;
-    uint32_t v = 1 % p;
-    for (int s = 0; s < 40; ++s) {
-      d.pow2mod[l][s] = uint16_t(v);
-      d.wide_k[l][s] = uint16_t((uint64_t(h) * ((uint32_t(p) + 1 - v) % uint32_t(p))) % uint32_t(p));
-      v = (v * 2) % p;
+    {
+      uint64_t c = 1 % uint64_t(p);
+      for (int i = 0; i < 6; ++i) {
+        rc.cw[i] = uint32_t(c);
+        c = (c << 16) % uint64_t(p);
+      }
+      // 2^90 mod p
+      uint64_t t = 1 % uint64_t(p);
+      for (int i = 0; i < 90; ++i) t = (t * 2) % uint64_t(p);
+      rc.kw = uint32_t((h + uint32_t(p) - uint32_t(t)) % uint32_t(p));
     }
     d.coeff_hi[l] = K.coeff_hi[l];
     d.coeff_lo[l] = K.coeff_lo[l];

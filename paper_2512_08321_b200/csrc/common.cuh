@@ -56,14 +56,15 @@ struct ModConst {
 struct ResConst {
   uint32_t c32, c16, k, h, magic, sum_k;  // sum_k = p - h (re + im plane)
   int32_t shift, p;
+  // wide values (|a'| >= 2^53): v = 2^90 + a' in six 16-bit limbs,
+  // u = sum_i limb_i * (2^(16 i) mod p) + kw  ==  a' + h  (mod p)
+  uint32_t cw[6], kw;
 };
 
 struct DevConsts {
   int32_t n;
   ModConst mc[CRTG_MAX_MODULI];
   ResConst rc[CRTG_MAX_MODULI];
-  uint16_t pow2mod[CRTG_MAX_MODULI][40];  // 2^s mod p, s < 40 (wide residues)
-  uint16_t wide_k[CRTG_MAX_MODULI][40];   // h * (1 - 2^s) mod p
   double coeff_hi[CRTG_MAX_MODULI];
   double coeff_lo[CRTG_MAX_MODULI];
   double p_hi, p_lo;

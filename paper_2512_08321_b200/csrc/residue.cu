@@ -35,36 +35,6 @@ __device__ __forceinline__ void load_c<float>(const float* p, double& re, double
   im = double(v.y);
 }
 
-// integer-valued a' -> (sign, 53-bit significand split, power-of-two shift),
-// packed in two registers: hi = M>>32 (21 bits) | s << 24 | neg << 31, lo = M.
-struct Dec {
-  uint32_t hi;
-  uint32_t lo;
-};
-
-__device__ __forceinline__ Dec decompose(double v) {
-  uint32_t tag = v < 0.0 ? 0x80000000u : 0u;
-  double a = fabs(v);
-  if (a >= 9007199254740992.0) {  // 2^53: a' = M * 2^s
-    const int s = ilogb(a) - 52;
-    a = ldexp(a, -s);  // exact
-    tag |= uint32_t(s) << 24;
-  }
-  const uint64_t M = uint64_t(a);
-  return {uint32_t(M >> 32) | tag, uint32_t(M)};
-}
-
-__device__ __forceinline__ uint32_t residue_u(const Dec& d, const ModConst& c,
-                                              const uint16_t* pow2mod) {
-  // hi*2^32 + lo_h*2^16 + lo_l  ==  hi*c32 + lo_h*c16 + lo_l   (mod p), < 2^30
-  const uint32_t u = (d.hi & 0x1FFFFFu) * c.c32 + (d.lo >> 16) * c.c16 + (d.lo & 0xFFFFu);
-  uint32_t r = mod_u31(u, c);
-  const uint32_t s = (d.hi >> 24) & 0x3Fu;
-  if (s) r = mod_u31(r * uint32_t(pow2mod[s]), c);
-  if ((d.hi >> 31) && r) r = uint32_t(c.p) - r;
-  return r;
-}
-
 template <typename T, int OPERAND, int KIND>
 __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int64_t ldx, int rows,
                                                   int kdim, int64_t col0,
@@ -108,7 +78,7 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
   // the CTA's 32 rows are one contiguous 4 KiB run of the packed plane
   const int64_t goff = (int64_t(kb) * rb_count + (r0 >> 7)) * kBlockBytes + (r0 & 127) * 128;
 
-  if (KIND == PACK_BARS) {
+  {
     // bound operands: ceil(|x| 2^bar) in [0, 64] and their difference
     uint32_t w[3][4] = {};
 #pragma unroll
@@ -127,111 +97,76 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
     for (int q = 0; q < 3; ++q)
       reinterpret_cast<uint4*>(out + q * plane_bytes + goff)[threadIdx.x] =
           reinterpret_cast<const uint4*>(stage[q])[threadIdx.x];
-    return;
-  }
-
-  // quantize: a' = trunc(x 2^e), |a'| < 2^90 (else DomainError, flagged)
-  Dec dr[16], di[16];
-  int bad = 0;
-#pragma unroll
-  for (int t = 0; t < 16; ++t) {
-    double qr = trunc(ldexp_rn(re[t], e));
-    double qi = trunc(ldexp_rn(im[t], e));
-    if (!(fabs(qr) < 0x1p90)) { bad = 1; qr = 0.0; }
-    if (!(fabs(qi) < 0x1p90)) { bad = 1; qi = 0.0; }
-    dr[t] = decompose(qr);
-    di[t] = decompose(qi);
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(overflow, 1ull);
-
-  for (int l = 0; l < dc.n; ++l) {
-    const ModConst mc = dc.mc[l];
-    const uint16_t* p2 = dc.pow2mod[l];
-    uint32_t w[3][4] = {};
-#pragma unroll
-    for (int t = 0; t < 16; ++t) {
-      const uint32_t ur = residue_u(dr[t], mc, p2);
-      const uint32_t ui = residue_u(di[t], mc, p2);
-      uint32_t us = ur + ui;
-      us -= (us >= uint32_t(mc.p)) ? uint32_t(mc.p) : 0u;
-      const int sh = 8 * (t & 3);
-      w[0][t >> 2] |= (uint32_t(to_sym(ur, mc)) & 0xFF) << sh;
-      w[1][t >> 2] |= (uint32_t(to_sym(ui, mc)) & 0xFF) << sh;
-      w[2][t >> 2] |= (uint32_t(to_sym(us, mc)) & 0xFF) << sh;
-    }
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-      *reinterpret_cast<uint4*>(&stage[q][soff]) = make_uint4(w[q][0], w[q][1], w[q][2], w[q][3]);
-    __syncthreads();
-    int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-      reinterpret_cast<uint4*>(base + q * plane_bytes)[threadIdx.x] =
-          reinterpret_cast<const uint4*>(stage[q])[threadIdx.x];
-    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
 // Residue kernel.  CTA tile = 16 operand rows x 128 K (one packed K block);
 // thread = 8 consecutive K of one row (16 real values).  Each value is
-// decomposed once into 3 registers (hi | s<<24, lo_h, lo_l of v = 2^53 +- M);
-// per modulus a value costs 6 integer ops.  Output goes through a 6 KiB smem
-// stage so every global store is a coalesced 16-byte write of a contiguous
-// 2 KiB run of the packed plane.
+// decomposed once into 3 registers; per modulus a value then costs 6 (narrow)
+// or ~15 (wide) integer ops.  Output goes through a 6 KiB smem stage so every
+// global store is a coalesced 16-byte write of a contiguous 2 KiB run of the
+// packed plane.
 // ---------------------------------------------------------------------------
 constexpr int kResRows = 16;
 
+// Value representations (3 registers each), read straight from the IEEE bits:
+//  narrow (|a'| < 2^53): v = 2^53 + a' as (v >> 32, (v >> 16) & 0xffff, v & 0xffff)
+//      u = hi*(2^32 mod p) + lh*(2^16 mod p) + ll + k           (< 2^31)
+//  wide (some |a'| >= 2^53 in the thread): v = 2^90 + a' (< 2^91) as six 16-bit
+//      limbs packed two per register, u = sum limb_i*(2^(16i) mod p) + kw (< 2^27)
+// Both give u == a' + floor(p/2) (mod p); one magic reduction -> t in [0,p).
 struct Val3 {
-  uint32_t hi, lh, ll;
+  uint32_t w0, w1, w2;
 };
 
-// q integer-valued, |q| < 2^90 -> v = 2^53 + sign*M (M < 2^53), shift s, read
-// straight from the IEEE bit pattern (no FP conversions):
-//   q = 1.f * 2^e2  ->  M = (2^52 | f) >> (52 - e2)  (e2 <= 52),  s = 0
-//                       M = (2^52 | f),  s = e2 - 52         (e2 >  52)
-__device__ __forceinline__ Val3 split_value(double q) {
+__device__ __forceinline__ void int_parts(double q, uint64_t& M, int& s) {
   const uint64_t bits = uint64_t(__double_as_longlong(q));
   const int e2 = int((bits >> 52) & 0x7FF) - 1023;
   const uint64_t sig = (bits & 0xFFFFFFFFFFFFFull) | (uint64_t(1) << 52);
-  uint64_t M;
-  uint32_t s = 0;
+  s = 0;
   if (e2 < 0) {
     M = 0;
   } else if (e2 <= 52) {
     M = sig >> (52 - e2);
   } else {
     M = sig;
-    s = uint32_t(e2 - 52);
+    s = e2 - 52;
   }
-  const uint64_t v = (bits >> 63) ? (uint64_t(1) << 53) - M : (uint64_t(1) << 53) + M;
-  return {uint32_t(v >> 32) | (s << 24), uint32_t(v) >> 16, uint32_t(v) & 0xFFFFu};
 }
 
-template <bool WIDE>
-__device__ __forceinline__ uint32_t res_t(const Val3& v, const ResConst& c, int l,
-                                          const DevConsts& dc) {
-  // t = (x + h) mod p
-  const uint32_t hi = WIDE ? (v.hi & 0x00FFFFFFu) : v.hi;
-  const uint32_t u = hi * c.c32 + v.lh * c.c16 + v.ll + c.k;
-  uint32_t t;
-  if (c.shift < 0) {
-    t = u & 0xFFu;
-  } else {
-    t = u - uint32_t(c.p) * (__umulhi(u, c.magic) >> c.shift);
-  }
-  if (WIDE) {
-    const uint32_t s = v.hi >> 24;
-    if (s) {
-      const uint32_t w = t * dc.pow2mod[l][s] + dc.wide_k[l][s];
-      t = c.shift < 0 ? (w & 0xFFu) : w - uint32_t(c.p) * (__umulhi(w, c.magic) >> c.shift);
-    }
-  }
-  return t;
+__device__ __forceinline__ Val3 split_narrow(double q) {
+  uint64_t M;
+  int s;
+  int_parts(q, M, s);
+  const uint64_t v = (q < 0.0) ? (uint64_t(1) << 53) - M : (uint64_t(1) << 53) + M;
+  return {uint32_t(v >> 32), uint32_t(v) >> 16, uint32_t(v) & 0xFFFFu};
+}
+
+__device__ __forceinline__ Val3 split_wide(double q) {
+  uint64_t M;
+  int s;
+  int_parts(q, M, s);
+  const unsigned __int128 mag = (unsigned __int128)M << s;
+  const unsigned __int128 base = (unsigned __int128)1 << 90;
+  const unsigned __int128 v = (q < 0.0) ? base - mag : base + mag;
+  return {uint32_t(v), uint32_t(v >> 32), uint32_t(v >> 64)};
 }
 
 __device__ __forceinline__ uint32_t mod_small(uint32_t u, const ResConst& c) {
   return c.shift < 0 ? (u & 0xFFu) : u - uint32_t(c.p) * (__umulhi(u, c.magic) >> c.shift);
+}
+
+template <bool WIDE>
+__device__ __forceinline__ uint32_t res_t(const Val3& v, const ResConst& c) {
+  uint32_t u;
+  if (WIDE) {
+    u = (v.w0 & 0xFFFFu) + (v.w0 >> 16) * c.cw[1] + (v.w1 & 0xFFFFu) * c.cw[2] +
+        (v.w1 >> 16) * c.cw[3] + (v.w2 & 0xFFFFu) * c.cw[4] + (v.w2 >> 16) * c.cw[5] + c.kw;
+  } else {
+    u = v.w0 * c.c32 + v.w1 * c.c16 + v.w2 + c.k;
+  }
+  return mod_small(u, c);  // t = (a' + h) mod p
 }
 
 // 4 values t_i in [0,p) -> packed int8 (t_i - h)
@@ -244,15 +179,14 @@ __device__ __forceinline__ uint32_t pack_sym(uint32_t a, uint32_t b, uint32_t c,
 
 template <bool WIDE>
 __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&im)[8],
-                                              const ResConst& c, int l, const DevConsts& dc,
-                                              uint32_t (&w)[3][2]) {
+                                              const ResConst& c, uint32_t (&w)[3][2]) {
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
     uint32_t tr[4], ti[4], ts[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      tr[j] = res_t<WIDE>(re[4 * half + j], c, l, dc);
-      ti[j] = res_t<WIDE>(im[4 * half + j], c, l, dc);
+      tr[j] = res_t<WIDE>(re[4 * half + j], c);
+      ti[j] = res_t<WIDE>(im[4 * half + j], c);
       // (re + im) + h = (tr - h) + (ti - h) + h  (mod p)
       ts[j] = mod_small(tr[j] + ti[j] + c.sum_k, c);
     }
@@ -295,8 +229,9 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
   const double scale = __longlong_as_double(e >= -1022 ? int64_t(e + 1023) << 52
                                                        : int64_t(1) << (e + 1074));
 
-  Val3 vr[8], vi[8];
+  double qr[8], qi[8];
   int bad = 0;
+  bool wide = false;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int h = h0 + t;
@@ -306,16 +241,18 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
                                   : X + 2 * (int64_t(h) * ldx + col0 + row);
       load_c<T>(p, re, im);
     }
-    double qr = trunc(__dmul_rn(re, scale));
-    double qi = trunc(__dmul_rn(im, scale));
-    if (!(fabs(qr) < 0x1p90)) { bad = 1; qr = 0.0; }
-    if (!(fabs(qi) < 0x1p90)) { bad = 1; qi = 0.0; }
-    vr[t] = split_value(qr);
-    vi[t] = split_value(qi);
+    qr[t] = trunc(__dmul_rn(re, scale));
+    qi[t] = trunc(__dmul_rn(im, scale));
+    if (!(fabs(qr[t]) < 0x1p90)) { bad = 1; qr[t] = 0.0; }
+    if (!(fabs(qi[t]) < 0x1p90)) { bad = 1; qi[t] = 0.0; }
+    wide |= fabs(qr[t]) >= 0x1p53 || fabs(qi[t]) >= 0x1p53;
   }
-  uint32_t any_wide = 0;
+  Val3 vr[8], vi[8];
 #pragma unroll
-  for (int t = 0; t < 8; ++t) any_wide |= (vr[t].hi | vi[t].hi) >> 24;
+  for (int t = 0; t < 8; ++t) {
+    vr[t] = wide ? split_wide(qr[t]) : split_narrow(qr[t]);
+    vi[t] = wide ? split_wide(qi[t]) : split_narrow(qi[t]);
+  }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(overflow, 1ull);
 
   // swizzled byte offset of this thread's 8 bytes inside the 2 KiB stage tile
@@ -324,26 +261,26 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
   // the tile's 16 rows form one contiguous 2 KiB run of each packed plane
   const int gr0 = r0 + row_base;  // row of this tile inside the packed plane
   const int64_t goff = (int64_t(kb) * rb_count + (gr0 >> 7)) * kBlockBytes + (gr0 & 127) * 128;
-  const int q = threadIdx.x >> 7;        // copy-out: plane handled by this half
-  const int qi = threadIdx.x & 127;      // 16-byte slot within the 2 KiB run
+  const int cq = threadIdx.x >> 7;       // copy-out: plane handled by this half
+  const int cs = threadIdx.x & 127;      // 16-byte slot within the 2 KiB run
 
   for (int l = 0; l < dc.n; ++l) {
     const ResConst c = dc.rc[l];
     uint32_t w[3][2];
-    if (any_wide)
-      residue_words<true>(vr, vi, c, l, dc, w);
+    if (wide)
+      residue_words<true>(vr, vi, c, w);
     else
-      residue_words<false>(vr, vi, c, l, dc, w);
+      residue_words<false>(vr, vi, c, w);
 #pragma unroll
     for (int pl = 0; pl < 3; ++pl)
       *reinterpret_cast<uint2*>(&stage[pl][soff]) = make_uint2(w[pl][0], w[pl][1]);
     __syncthreads();
     int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
-    reinterpret_cast<uint4*>(base + q * plane_bytes)[qi] =
-        reinterpret_cast<const uint4*>(stage[q])[qi];
-    if (q == 0)
-      reinterpret_cast<uint4*>(base + 2 * plane_bytes)[qi] =
-          reinterpret_cast<const uint4*>(stage[2])[qi];
+    reinterpret_cast<uint4*>(base + cq * plane_bytes)[cs] =
+        reinterpret_cast<const uint4*>(stage[cq])[cs];
+    if (cq == 0)
+      reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
+          reinterpret_cast<const uint4*>(stage[2])[cs];
     __syncthreads();
   }
   }  // tile loop
