@@ -110,24 +110,39 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
   int32_t tr[3][4] = {}, ti[3][4] = {};
   double s1r[4] = {0, 0, 0, 0}, s1i[4] = {0, 0, 0, 0};
   double s2r[4] = {0, 0, 0, 0}, s2i[4] = {0, 0, 0, 0};
-  for (int l = 0; l < dc.n; ++l) {
-    const uint32_t wr = load_word(pr + l * e_plane, aligned, j0, n);
-    const uint32_t wi = load_word(pi + l * e_plane, aligned, j0, n);
-    const double cl = dc.coeff_lo[l];
-    const int32_t h0 = dc.hi_limb[l][0], h1 = dc.hi_limb[l][1], h2 = dc.hi_limb[l][2];
+  // residue words are loaded in batches of kB moduli ahead of the arithmetic
+  // (latency-bound otherwise); terms are still added in ascending l
+  constexpr int kB = 5;
+  for (int l0 = 0; l0 < dc.n; l0 += kB) {
+    uint32_t wr[kB], wi[kB];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int32_t er = int32_t(int8_t(wr >> (8 * q)));
-      const int32_t ei = int32_t(int8_t(wi >> (8 * q)));
-      if constexpr (LIMBS) {
-        tr[0][q] += h0 * er; tr[1][q] += h1 * er; tr[2][q] += h2 * er;
-        ti[0][q] += h0 * ei; ti[1][q] += h1 * ei; ti[2][q] += h2 * ei;
-      } else {
-        s1r[q] = __dadd_rn(s1r[q], __dmul_rn(dc.coeff_hi[l], double(er)));
-        s1i[q] = __dadd_rn(s1i[q], __dmul_rn(dc.coeff_hi[l], double(ei)));
+    for (int b = 0; b < kB; ++b) {
+      wr[b] = wi[b] = 0;
+      if (l0 + b < dc.n) {
+        wr[b] = load_word(pr + (l0 + b) * e_plane, aligned, j0, n);
+        wi[b] = load_word(pi + (l0 + b) * e_plane, aligned, j0, n);
       }
-      s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, double(er)));
-      s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, double(ei)));
+    }
+#pragma unroll
+    for (int b = 0; b < kB; ++b) {
+      const int l = l0 + b;
+      if (l >= dc.n) break;
+      const double cl = dc.coeff_lo[l];
+      const int32_t h0 = dc.hi_limb[l][0], h1 = dc.hi_limb[l][1], h2 = dc.hi_limb[l][2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int32_t er = int32_t(int8_t(wr[b] >> (8 * q)));
+        const int32_t ei = int32_t(int8_t(wi[b] >> (8 * q)));
+        if constexpr (LIMBS) {
+          tr[0][q] += h0 * er; tr[1][q] += h1 * er; tr[2][q] += h2 * er;
+          ti[0][q] += h0 * ei; ti[1][q] += h1 * ei; ti[2][q] += h2 * ei;
+        } else {
+          s1r[q] = __dadd_rn(s1r[q], __dmul_rn(dc.coeff_hi[l], double(er)));
+          s1i[q] = __dadd_rn(s1i[q], __dmul_rn(dc.coeff_hi[l], double(ei)));
+        }
+        s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, double(er)));
+        s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, double(ei)));
+      }
     }
   }
   if constexpr (LIMBS) {
