@@ -51,7 +51,12 @@ enum crtg_status {
  * and the double-double CRT path; single -> complex64 result and the plain-f64
  * CRT path, crt.py:246-258).  OR in CRTG_IN_C64 when the inputs are complex64
  * (read and upcast exactly on the device); otherwise inputs are complex128. */
-enum crtg_precision { CRTG_DOUBLE = 0, CRTG_SINGLE = 1, CRTG_IN_C64 = 16 };
+enum crtg_precision {
+  CRTG_DOUBLE = 0,
+  CRTG_SINGLE = 1,
+  CRTG_IN_C64 = 16, /* complex entry points: inputs are complex64 */
+  CRTG_IN_F32 = 16  /* real entry point: inputs are float32 */
+};
 enum crtg_mode { CRTG_FAST = 0, CRTG_ACCURATE = 1 };
 
 /* diag[] slots (device uint64) */
@@ -62,6 +67,7 @@ enum crtg_diag {
   CRTG_DIAG_NONFINITE_B = 3,
   CRTG_DIAG_OVERFLOW_A = 4,  /* scaling.py:290-292, crt.py:209-210 */
   CRTG_DIAG_OVERFLOW_B = 5,
+  CRTG_DIAG_INT32_OVERFLOW = 6, /* kernel.py:33-34 (real path, k > 2^16 only) */
   CRTG_DIAG_LEN = 8
 };
 
@@ -123,6 +129,25 @@ int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_t n, int64_
                            void* C, int64_t ldc, const crtg_consts* K, int64_t n_block,
                            void* ws, size_t ws_bytes, uint64_t* diag, int sync_check,
                            void* stream);
+
+/*
+ * Real domain, C = A @ B with real float64 / float32 inputs (replaces
+ * emulate_gemm_real, emulate.py:169-190): one INT8 product
+ * per modulus.  a_colmajor / b_colmajor give each operand's storage order
+ * (lda / ldb are then the column strides): the reference keeps the caller's
+ * layout for real operands, and numpy's summation order for the fast-mode
+ * exponents follows it (pairwise along the contiguous axis, sequential along the
+ * strided one) — the library reproduces both.  C is row-major (ldc).  Result
+ * float64 (CRTG_DOUBLE) or float32 (CRTG_SINGLE); OR CRTG_IN_F32 for float32
+ * inputs.  k <= 2^17 (fast) / 2^16 (accurate).
+ */
+size_t crtg_real_workspace_size(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                                int num_moduli, int64_t n_block);
+int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                   const void* A, int64_t lda, int a_colmajor, const void* B, int64_t ldb,
+                   int b_colmajor, void* C, int64_t ldc, const crtg_consts* K, int64_t n_block,
+                   void* ws, size_t ws_bytes, int32_t* mu_out, int32_t* nu_out,
+                   uint64_t* diag, int sync_check, void* stream);
 
 /* ---- multi-GPU building blocks (output-tile sharding) ---- */
 

@@ -8,7 +8,7 @@ hand-written tcgen05 / TMA kernels in `libcrtg.so` (include/crtg.h).
 
 from .config import DEFAULT_N_BLOCK, MAX_K_COMPLEX, MAX_K_REAL, STRATEGIES, EmuConfig
 from .emulate import (ScalingVectors, accurate_scaling, complex_gemm_mod, crt_reconstruct,
-                      emulate_gemm_complex, fast_scaling, gemm, gemm_i8_i32,
+                      emulate_gemm_complex, emulate_gemm_real, fast_scaling, gemm, gemm_i8_i32,
                       quantized_residues, run_complex)
 from .errors import ConfigError, DimensionError, DomainError
 from .moduli import ModulusSet, ScalingConstants, select_moduli
@@ -19,6 +19,6 @@ __all__ = [
     "ConfigError", "DEFAULT_N_BLOCK", "DimensionError", "DomainError", "EmuConfig",
     "MAX_K_COMPLEX", "MAX_K_REAL", "ModulusSet", "STRATEGIES", "ScalingConstants",
     "ScalingVectors", "accurate_scaling", "complex_gemm_mod", "crt_reconstruct",
-    "emulate_gemm_complex", "fast_scaling", "gemm", "gemm_i8_i32", "quantized_residues",
+    "emulate_gemm_complex", "emulate_gemm_real", "fast_scaling", "gemm", "gemm_i8_i32", "quantized_residues",
     "run_complex", "select_moduli",
 ]

@@ -47,6 +47,10 @@ SIGNATURES = {
     "crtg_gemm_complex_host": (_c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp,
                                         _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _sz, _vp, _c_int,
                                         _vp]),
+    "crtg_real_workspace_size": (_sz, [_c_int, _c_int, _c_i64, _c_i64, _c_i64, _c_int, _c_i64]),
+    "crtg_gemm_real": (_c_int, [_c_int, _c_int, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _c_int, _vp,
+                                _c_i64, _c_int, _vp, _c_i64, _vp, _c_i64, _vp, _sz, _vp, _vp,
+                                _vp, _c_int, _vp]),
     "crtg_gemm_complex_exps": (_c_int, [_c_int, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp,
                                         _c_i64, _vp, _c_i64, _vp, _c_i64, _vp, _vp, _vp, _sz,
                                         _vp, _c_int, _vp]),

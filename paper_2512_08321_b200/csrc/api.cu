@@ -323,7 +323,7 @@ struct Region {
 struct Plan {
   int64_t m, n, k, N, nb, m_pad, n_pad, nb_pad, k_pad;
   Region diag, mu, nu, rowabs, colabs, colsq, tree, bar_mu, bar_nu, rowmax, colmax, a_pack,
-      b_pack, e_re, e_im, a_bars, b_bars;
+      b_pack, e_re, e_im, a_bars, b_bars, rowsq;
   size_t total = 0;
 };
 
@@ -333,7 +333,8 @@ void add(Plan& p, Region& r, size_t bytes) {
   p.total += (bytes + 255) & ~size_t(255);
 }
 
-Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_block) {
+Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_block,
+               bool real = false) {
   Plan p{};
   p.m = m;
   p.n = n;
@@ -357,11 +358,13 @@ Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_b
   add(p, p.colabs, 8 * p.n_pad);
   add(p, p.colsq, 16 * p.n_pad);
   add(p, p.tree, tree_bytes(k));
-  add(p, p.a_pack, size_t(3 * N) * p.m_pad * p.k_pad);
+  add(p, p.a_pack, size_t(real ? N : 3 * N) * p.m_pad * p.k_pad);
   const int nbuf = (overlap_enabled() && p.nb < p.n) ? 2 : 1;  // double buffers (overlap)
-  add(p, p.b_pack, size_t(nbuf) * size_t(3 * N) * p.nb_pad * p.k_pad);
+  const int ppm = real ? 1 : 3;  // planes per modulus
+  add(p, p.b_pack, size_t(nbuf) * size_t(ppm * N) * p.nb_pad * p.k_pad);
   add(p, p.e_re, size_t(nbuf) * size_t(N) * m * p.nb_pad);
-  add(p, p.e_im, size_t(nbuf) * size_t(N) * m * p.nb_pad);
+  add(p, p.e_im, real ? 0 : size_t(nbuf) * size_t(N) * m * p.nb_pad);
+  add(p, p.rowsq, real ? 16 * p.m_pad : 0);
   if (mode == CRTG_ACCURATE) {
     add(p, p.bar_mu, 4 * p.m_pad);
     add(p, p.bar_nu, 4 * p.n_pad);
@@ -407,19 +410,19 @@ int accurate_partial(const Plan& P, int precision, const void* A, int64_t lda, c
   CRTG_TRY(cudaMemsetAsync(colmax, 0, P.colmax.bytes, s), "memset");
   StageTimer timer(CRTG_STAGE_SCALING, s, 7);
   PwTree tree{};
-  CRTG_TRY(launch_row_stats(single, false, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, nullptr,
+  CRTG_TRY(launch_row_stats(single ? E_C64 : E_C128, false, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, nullptr,
                             rowabs, diag, s),
            "row absmax");
   CRTG_TRY(launch_bar(rowabs, P.m, bar_mu, s), "bar");
-  CRTG_TRY(launch_col_absmax(single, B, ldb, P.k, P.n, colabs, diag, s), "col absmax");
+  CRTG_TRY(launch_col_absmax(single ? E_C64 : E_C128, B, ldb, P.k, P.n, colabs, diag, s), "col absmax");
   CRTG_TRY(launch_bar(colabs, P.n, bar_nu, s), "bar");
   const int64_t a_plane = P.m_pad * P.k_pad, b_plane = P.n_pad * P.k_pad;
   int8_t* abars = at<int8_t>(ws, P.a_bars);
   int8_t* bbars = at<int8_t>(ws, P.b_bars);
-  CRTG_TRY(launch_pack(single, 0, PACK_BARS, A, lda, P.m, P.k, 0, bar_mu, dc, abars, a_plane,
+  CRTG_TRY(launch_pack(single ? E_C64 : E_C128, 0, PACK_BARS, A, lda, P.m, P.k, 0, bar_mu, dc, abars, a_plane,
                        P.m_pad / 128, diag + CRTG_DIAG_OVERFLOW_A, s),
            "bars A");
-  CRTG_TRY(launch_pack(single, 1, PACK_BARS, B, ldb, P.n, P.k, 0, bar_nu, dc, bbars, b_plane,
+  CRTG_TRY(launch_pack(single ? E_C64 : E_C128, 1, PACK_BARS, B, ldb, P.n, P.k, 0, bar_nu, dc, bbars, b_plane,
                        P.n_pad / 128, diag + CRTG_DIAG_OVERFLOW_B, s),
            "bars B");
   GemmArgs g{};
@@ -474,14 +477,14 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
     tree.level_start = reinterpret_cast<const int*>(tb + lb + nb);
     {
       StageTimer timer(CRTG_STAGE_SCALING, s, 1);
-      CRTG_TRY(launch_row_stats(single, true, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu,
+      CRTG_TRY(launch_row_stats(single ? E_C64 : E_C128, true, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu,
                                 rowabs, diag, s),
                "row stats");
     }
     StageTimer timer(CRTG_STAGE_SCALING, side, 3);
     CRTG_TRY(cudaMemsetAsync(colabs, 0, P.colabs.bytes, side), "memset");
-    CRTG_TRY(launch_col_absmax(single, B, ldb, P.k, P.n, colabs, diag, side), "col absmax");
-    CRTG_TRY(launch_col_fast(single, B, ldb, P.k, P.n, colabs, at<double>(ws, P.colsq), dc.p_fast,
+    CRTG_TRY(launch_col_absmax(single ? E_C64 : E_C128, B, ldb, P.k, P.n, colabs, diag, side), "col absmax");
+    CRTG_TRY(launch_col_fast(single ? E_C64 : E_C128, B, ldb, P.k, P.n, colabs, at<double>(ws, P.colsq), dc.p_fast,
                              dc.delta, nu, diag, side),
              "col sumsq");
     return CRTG_OK;
@@ -520,7 +523,7 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
   int8_t* apack = at<int8_t>(ws, P.a_pack);
   {
     StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
-    CRTG_TRY(launch_pack(in32, 0, PACK_RESIDUE, A, lda, m, k, 0, mu, dc, apack, a_plane,
+    CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 0, PACK_RESIDUE, A, lda, m, k, 0, mu, dc, apack, a_plane,
                          P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s),
              "residues A");
   }
@@ -535,7 +538,7 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
   auto residues_b = [&](int64_t j, int max_ctas) -> int {
     const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
     StageTimer timer(CRTG_STAGE_RESIDUE_B, side, 1);
-    CRTG_TRY(launch_pack(in32, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack(j),
+    CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack(j),
                          w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, side, max_ctas),
              "residues B");
     ev_r[j] = E.get();
@@ -576,7 +579,7 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
     CRTG_TRY(cudaStreamWaitEvent(side, ev_g[j], 0), "wait");
     {
       StageTimer timer(CRTG_STAGE_CRT, side, 1);
-      CRTG_TRY(launch_crt(single, m, w, ere(j), eim(j), g.e_plane, g.e_ld, mu, nu + j0, dc,
+      CRTG_TRY(launch_crt(single, false, m, w, ere(j), eim(j), g.e_plane, g.e_ld, mu, nu + j0, dc,
                           static_cast<char*>(C) + j0 * csz, ldc, side,
                           j + 1 < nblk ? nsm : 0),
                "crt");
@@ -598,6 +601,8 @@ int check_diag(const unsigned long long* diag_dev, cudaStream_t s) {
   if (h[CRTG_DIAG_NONFINITE_B]) return fail(CRTG_ERR_DOMAIN, "B contains non-finite entries");
   if (h[CRTG_DIAG_OVERFLOW_A] || h[CRTG_DIAG_OVERFLOW_B])
     return fail(CRTG_ERR_DOMAIN, "scaled magnitudes exceed the quantization budget");
+  if (h[CRTG_DIAG_INT32_OVERFLOW])
+    return fail(CRTG_ERR_ARITH, "dot product exceeds the 32-bit accumulator");
   return CRTG_OK;
 }
 
@@ -714,7 +719,7 @@ int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim, const 
   int8_t* packed = static_cast<int8_t*>(ws);
   unsigned long long* ovf = reinterpret_cast<unsigned long long*>(diag) +
                             (operand == 0 ? CRTG_DIAG_OVERFLOW_A : CRTG_DIAG_OVERFLOW_B);
-  CRTG_TRY(launch_pack((precision & CRTG_IN_C64) != 0, operand, PACK_RESIDUE, X, ldx, rows, kdim, 0,
+  CRTG_TRY(launch_pack((precision & CRTG_IN_C64) ? E_C64 : E_C128, operand, PACK_RESIDUE, X, ldx, rows, kdim, 0,
                        exps, dc, packed, plane, r_pad / 128, ovf, s),
            "residues");
   g_launches += uint64_t(1 + 3 * N);
@@ -847,7 +852,7 @@ extern "C" int crtg_crt_reconstruct(int precision, int64_t m, int64_t n, const i
   if (m < 1 || n < 1 || ldc < n) return fail(CRTG_ERR_DIMENSION, "bad shape");
   const DevConsts dc = make_dev(*K);
   g_launches += 1;
-  CRTG_TRY(launch_crt((precision & CRTG_SINGLE) != 0, m, n, e_re, e_im, m * n, n, mu, nu, dc, C, ldc,
+  CRTG_TRY(launch_crt((precision & CRTG_SINGLE) != 0, false, m, n, e_re, e_im, m * n, n, mu, nu, dc, C, ldc,
                       static_cast<cudaStream_t>(stream)),
            "crt");
   return CRTG_OK;
@@ -1111,12 +1116,12 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
         const char* Ai = dA + size_t(i0) * k * esz;
         if (mode == CRTG_FAST) {
           StageTimer timer(CRTG_STAGE_SCALING, s, 1);
-          CRTG_TRY(launch_row_stats(in32, true, Ai, k, h, k, tree, dc.p_fast, dc.delta, mu + i0,
+          CRTG_TRY(launch_row_stats(in32 ? E_C64 : E_C128, true, Ai, k, h, k, tree, dc.p_fast, dc.delta, mu + i0,
                                     at<double>(ws, P.rowabs) + i0, dg, s),
                    "row stats");
         }
         StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
-        CRTG_TRY(launch_pack(in32, 0, PACK_RESIDUE, Ai, k, h, k, 0, mu + i0, dc, apack, a_plane,
+        CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 0, PACK_RESIDUE, Ai, k, h, k, 0, mu + i0, dc, apack, a_plane,
                              P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s, 0, i0,
                              last_rows ? P.m_pad - i0 : h),
                  "residues A");
@@ -1127,13 +1132,13 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
           StageTimer timer(CRTG_STAGE_SCALING, s, 3);
           const char* Bj = dB + j0 * esz;
           double* cabs = at<double>(ws, P.colabs) + j0;
-          CRTG_TRY(launch_col_absmax(in32, Bj, n, k, w, cabs, dg, s), "col absmax");
-          CRTG_TRY(launch_col_fast(in32, Bj, n, k, w, cabs, at<double>(ws, P.colsq) + 2 * j0,
+          CRTG_TRY(launch_col_absmax(in32 ? E_C64 : E_C128, Bj, n, k, w, cabs, dg, s), "col absmax");
+          CRTG_TRY(launch_col_fast(in32 ? E_C64 : E_C128, Bj, n, k, w, cabs, at<double>(ws, P.colsq) + 2 * j0,
                                    dc.p_fast, dc.delta, nu + j0, dg, s),
                    "col sumsq");
         }
         StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
-        CRTG_TRY(launch_pack(in32, 1, PACK_RESIDUE, dB, n, w, k, j0, nu + j0, dc, bpack,
+        CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 1, PACK_RESIDUE, dB, n, w, k, j0, nu + j0, dc, bpack,
                              w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
                  "residues B");
       }
@@ -1166,7 +1171,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
       char* cblk = dC + (tile & 1) * cbuf;
       {
         StageTimer timer(CRTG_STAGE_CRT, s, 1);
-        CRTG_TRY(launch_crt(single, h, w, g.e_re + i0 * g.e_ld, g.e_im + i0 * g.e_ld, g.e_plane,
+        CRTG_TRY(launch_crt(single, false, h, w, g.e_re + i0 * g.e_ld, g.e_im + i0 * g.e_ld, g.e_plane,
                             g.e_ld, mu + i0, nu + j0, dc, cblk, w, s),
                  "crt");
       }
@@ -1181,6 +1186,214 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     }
   }
   CRTG_TRY(cudaStreamWaitEvent(s, evD.back(), 0), "wait");
+  if (sync_check) return check_diag(dg, s);
+  return CRTG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Real domain (emulate_gemm_real, emulate.py:169-190).
+// The reference keeps the caller's memory layout for real operands, so numpy
+// sums the squares pairwise along the contiguous axis and sequentially along the
+// strided one; an operand stored column-major is therefore processed as the
+// transpose of a row-major matrix by the "other" kernel family, which yields
+// exactly that order.
+// ---------------------------------------------------------------------------
+namespace {
+int load_tree(const Plan& P, void* ws, cudaStream_t s, PwTree& tree) {
+  const HostTree& ht = pairwise_tree(P.k);
+  char* tb = at<char>(ws, P.tree);
+  const size_t lb = ht.leaves.size() * sizeof(int2), nbt = ht.nodes.size() * sizeof(int2),
+               sb = ht.level_start.size() * sizeof(int);
+  if (lb + nbt + sb + 64 > P.tree.bytes) return fail(CRTG_ERR_WORKSPACE, "tree region too small");
+  CRTG_TRY(cudaMemcpyAsync(tb, ht.leaves.data(), lb, cudaMemcpyHostToDevice, s), "tree copy");
+  if (nbt) CRTG_TRY(cudaMemcpyAsync(tb + lb, ht.nodes.data(), nbt, cudaMemcpyHostToDevice, s), "tree copy");
+  CRTG_TRY(cudaMemcpyAsync(tb + lb + nbt, ht.level_start.data(), sb, cudaMemcpyHostToDevice, s),
+           "tree copy");
+  tree = PwTree{int(ht.leaves.size()), int(ht.nodes.size()), int(ht.level_start.size()) - 1,
+                reinterpret_cast<const int2*>(tb), reinterpret_cast<const int2*>(tb + lb),
+                reinterpret_cast<const int*>(tb + lb + nbt)};
+  return CRTG_OK;
+}
+}  // namespace
+
+extern "C" size_t crtg_real_workspace_size(int precision, int mode, int64_t m, int64_t n,
+                                           int64_t k, int num_moduli, int64_t n_block) {
+  (void)precision;
+  return make_plan(mode, m, n, k, num_moduli, n_block, true).total;
+}
+
+extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int64_t k,
+                              const void* A, int64_t lda, int a_colmajor, const void* B,
+                              int64_t ldb, int b_colmajor, void* C, int64_t ldc,
+                              const crtg_consts* K, int64_t n_block, void* ws, size_t ws_bytes,
+                              int32_t* mu_out, int32_t* nu_out, uint64_t* diag, int sync_check,
+                              void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if ((precision & ~(CRTG_SINGLE | CRTG_IN_F32)) != 0)
+    return fail(CRTG_ERR_CONFIG, "precision must be double or single");
+  if (mode != CRTG_FAST && mode != CRTG_ACCURATE) return fail(CRTG_ERR_CONFIG, "bad mode");
+  // k cap: 2^17 in fast mode, 2^16 in accurate mode (emulate.py:179-182)
+  const int64_t kcap = mode == CRTG_FAST ? (int64_t(1) << 17) : (int64_t(1) << 16);
+  if (m < 1 || n < 1 || k < 1) return fail(CRTG_ERR_DIMENSION, "m, n, k must be positive");
+  if (k > kcap)
+    return fail(CRTG_ERR_DIMENSION,
+                "inner dimension " + std::to_string(k) + " exceeds " + std::to_string(kcap));
+  if ((a_colmajor ? lda < m : lda < k) || (b_colmajor ? ldb < k : ldb < n) || ldc < n)
+    return fail(CRTG_ERR_DIMENSION, "leading dimension too small");
+  const Plan P = make_plan(mode, m, n, k, N, n_block, true);
+  if (!ws || ws_bytes < P.total)
+    return fail(CRTG_ERR_WORKSPACE, "workspace too small: need " + std::to_string(P.total));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int elem = (precision & CRTG_IN_F32) ? E_F32 : E_F64;
+  const size_t esz = (precision & CRTG_IN_F32) ? 4 : 8;
+  const bool single = (precision & CRTG_SINGLE) != 0;
+  unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
+                                : at<unsigned long long>(ws, P.diag);
+  const DevConsts dc = make_dev(*K);
+  int32_t* mu = at<int32_t>(ws, P.mu);
+  int32_t* nu = at<int32_t>(ws, P.nu);
+  double* rowabs = at<double>(ws, P.rowabs);
+  double* colabs = at<double>(ws, P.colabs);
+  CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
+  CRTG_TRY(cudaMemsetAsync(rowabs, 0, P.rowabs.bytes, s), "memset");
+  CRTG_TRY(cudaMemsetAsync(colabs, 0, P.colabs.bytes, s), "memset");
+  // operand A rows: row-major -> row kernels; column-major -> column kernels on A^T.
+  // operand B columns: row-major -> column kernels; column-major -> row kernels on B^T.
+  // diag offsets: the row kernels report into (NONFINITE_A, CLAMPED_MU), the column
+  // kernels into (NONFINITE_B, CLAMPED_NU); +-1 re-targets them to the other operand.
+  {
+    StageTimer timer(CRTG_STAGE_SCALING, s, mode == CRTG_FAST ? 6 : 11);
+    PwTree tree{};
+    if (mode == CRTG_FAST) {
+      if (int e = load_tree(P, ws, s, tree)) return e;
+      if (!a_colmajor) {
+        CRTG_TRY(launch_row_stats(elem, true, A, lda, m, k, tree, dc.p_fast, dc.delta, mu, rowabs,
+                                  dg, s), "row stats");
+      } else {
+        CRTG_TRY(launch_col_absmax(elem, A, lda, k, m, rowabs, dg - 1, s), "col absmax");
+        CRTG_TRY(launch_col_fast(elem, A, lda, k, m, rowabs, at<double>(ws, P.rowsq), dc.p_fast,
+                                 dc.delta, mu, dg - 1, s), "col sumsq");
+      }
+      if (!b_colmajor) {
+        CRTG_TRY(launch_col_absmax(elem, B, ldb, k, n, colabs, dg, s), "col absmax");
+        CRTG_TRY(launch_col_fast(elem, B, ldb, k, n, colabs, at<double>(ws, P.colsq), dc.p_fast,
+                                 dc.delta, nu, dg, s), "col sumsq");
+      } else {
+        CRTG_TRY(launch_row_stats(elem, true, B, ldb, n, k, tree, dc.p_fast, dc.delta, nu, colabs,
+                                  dg + 1, s), "row stats");
+      }
+    } else {
+      // accurate: absmax -> bars -> bound operands -> tcgen05 bound GEMM -> exponents
+      if (!a_colmajor)
+        CRTG_TRY(launch_row_stats(elem, false, A, lda, m, k, tree, dc.p_fast, dc.delta, nullptr,
+                                  rowabs, dg, s), "row absmax");
+      else
+        CRTG_TRY(launch_col_absmax(elem, A, lda, k, m, rowabs, dg - 1, s), "col absmax");
+      if (!b_colmajor)
+        CRTG_TRY(launch_col_absmax(elem, B, ldb, k, n, colabs, dg, s), "col absmax");
+      else
+        CRTG_TRY(launch_row_stats(elem, false, B, ldb, n, k, tree, dc.p_fast, dc.delta, nullptr,
+                                  colabs, dg + 1, s), "row absmax");
+      int32_t* bar_mu = at<int32_t>(ws, P.bar_mu);
+      int32_t* bar_nu = at<int32_t>(ws, P.bar_nu);
+      int32_t* rowmax = at<int32_t>(ws, P.rowmax);
+      int32_t* colmax = at<int32_t>(ws, P.colmax);
+      CRTG_TRY(cudaMemsetAsync(rowmax, 0, P.rowmax.bytes, s), "memset");
+      CRTG_TRY(cudaMemsetAsync(colmax, 0, P.colmax.bytes, s), "memset");
+      CRTG_TRY(launch_bar(rowabs, m, bar_mu, s), "bar");
+      CRTG_TRY(launch_bar(colabs, n, bar_nu, s), "bar");
+      const int64_t a_plane = P.m_pad * P.k_pad, b_plane = P.n_pad * P.k_pad;
+      int8_t* abars = at<int8_t>(ws, P.a_bars);
+      int8_t* bbars = at<int8_t>(ws, P.b_bars);
+      // bars of a real operand: planes (A, 0, A) so the complex bound product
+      // max(cross + diff, cross) reduces to the real bound A*B (scaling.py:257-258)
+      CRTG_TRY(launch_pack(elem, a_colmajor ? 1 : 0, PACK_BARS, A, lda, m, k, 0, bar_mu, dc, abars,
+                           a_plane, P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s), "bars A");
+      CRTG_TRY(launch_pack(elem, b_colmajor ? 0 : 1, PACK_BARS, B, ldb, n, k, 0, bar_nu, dc, bbars,
+                           b_plane, P.n_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s), "bars B");
+      GemmArgs g{};
+      g.a = abars;
+      g.b = bbars;
+      g.a_plane = a_plane;
+      g.b_plane = b_plane;
+      g.a_rb = int(P.m_pad / 128);
+      g.b_rb = int(P.n_pad / 128);
+      g.mt = int(P.m_pad / 128);
+      g.nt = int(P.n_pad / 256);
+      g.kb = int(P.k_pad / 128);
+      g.nl = 1;
+      g.planes_per_l = 3;
+      g.nphase = 3;
+      g.m = int(m);
+      g.n = int(n);
+      g.row_max = rowmax;
+      g.col_max = colmax;
+      CRTG_TRY(launch_gemm(EPI_BOUND, g, sm_count(), s), "bound gemm");
+      CRTG_TRY(launch_accurate_exps(rowmax, rowabs, bar_mu, m, dc.p_accu, dc.delta, mu,
+                                    dg + CRTG_DIAG_CLAMPED_MU, s), "accurate mu");
+      CRTG_TRY(launch_accurate_exps(colmax, colabs, bar_nu, n, dc.p_accu, dc.delta, nu,
+                                    dg + CRTG_DIAG_CLAMPED_NU, s), "accurate nu");
+    }
+  }
+  // residues of A: one plane per modulus
+  const int64_t a_plane = P.m_pad * P.k_pad;
+  int8_t* apack = at<int8_t>(ws, P.a_pack);
+  {
+    StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
+    CRTG_TRY(launch_pack(elem, a_colmajor ? 1 : 0, PACK_RESIDUE, A, lda, m, k, 0, mu, dc, apack,
+                         a_plane, P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s), "residues A");
+  }
+  int8_t* bpack = at<int8_t>(ws, P.b_pack);
+  int8_t* ere = at<int8_t>(ws, P.e_re);
+  const size_t csz = single ? 4 : 8;
+  for (int64_t j0 = 0; j0 < n; j0 += P.nb) {
+    const int64_t w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
+    {
+      StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
+      if (!b_colmajor)
+        CRTG_TRY(launch_pack(elem, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack,
+                             w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
+                 "residues B");
+      else
+        CRTG_TRY(launch_pack(elem, 0, PACK_RESIDUE, static_cast<const char*>(B) + j0 * ldb * esz,
+                             ldb, w, k, 0, nu + j0, dc, bpack, w_pad * P.k_pad, w_pad / 128,
+                             dg + CRTG_DIAG_OVERFLOW_B, s),
+                 "residues B");
+    }
+    GemmArgs g{};
+    g.a = apack;
+    g.b = bpack;
+    g.a_plane = a_plane;
+    g.b_plane = w_pad * P.k_pad;
+    g.a_rb = int(P.m_pad / 128);
+    g.b_rb = int(w_pad / 128);
+    g.mt = int(P.m_pad / 128);
+    g.nt = int(w_pad / 256);
+    g.kb = int(P.k_pad / 128);
+    g.nl = N;
+    g.planes_per_l = 1;
+    g.nphase = 1;
+    g.m = int(m);
+    g.n = int(w);
+    g.e_re = ere;
+    g.e_ld = P.nb_pad;
+    g.e_plane = m * P.nb_pad;
+    g.overflow = dg + CRTG_DIAG_INT32_OVERFLOW;
+    for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
+    {
+      StageTimer timer(CRTG_STAGE_GEMM, s, 1);
+      CRTG_TRY(launch_gemm(EPI_REAL, g, sm_count(), s), "real gemm");
+    }
+    {
+      StageTimer timer(CRTG_STAGE_CRT, s, 1);
+      CRTG_TRY(launch_crt(single, true, m, w, ere, nullptr, g.e_plane, g.e_ld, mu, nu + j0, dc,
+                          static_cast<char*>(C) + j0 * csz, ldc, s),
+               "crt");
+    }
+  }
+  if (mu_out) CRTG_TRY(cudaMemcpyAsync(mu_out, mu, 4 * m, cudaMemcpyDeviceToDevice, s), "copy");
+  if (nu_out) CRTG_TRY(cudaMemcpyAsync(nu_out, nu, 4 * n, cudaMemcpyDeviceToDevice, s), "copy");
   if (sync_check) return check_diag(dg, s);
   return CRTG_OK;
 }

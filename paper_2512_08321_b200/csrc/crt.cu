@@ -89,7 +89,7 @@ __device__ __forceinline__ uint32_t load_word(const int8_t* p, bool aligned, int
   return w;
 }
 
-template <bool SINGLE, bool LIMBS>
+template <bool SINGLE, bool LIMBS, bool REAL>
 __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t* __restrict__ e_re,
                                              const int8_t* __restrict__ e_im, int64_t e_plane,
                                              int64_t e_ld, const int32_t* __restrict__ mu,
@@ -103,8 +103,10 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
   const int64_t j0 = (t - i * nq) * 4;
   const int8_t* pr = e_re + i * e_ld + j0;
   const int8_t* pi = e_im + i * e_ld + j0;
-  const bool aligned = ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(pi) |
-                         uintptr_t(e_plane)) & 3) == 0 && j0 + 4 <= n;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(pr) |
+                         (REAL ? 0 : reinterpret_cast<uintptr_t>(pi)) | uintptr_t(e_plane)) & 3) ==
+                            0 &&
+                        j0 + 4 <= n;
   // S1 (exact, on a 2^g grid): integer limbs on the INT pipes; S2: the rounded
   // f64 sequence of crt.py:239-240, l ascending, no FMA.
   int32_t tr[3][4] = {}, ti[3][4] = {};
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
       wr[b] = wi[b] = 0;
       if (l0 + b < dc.n) {
         wr[b] = load_word(pr + (l0 + b) * e_plane, aligned, j0, n);
-        wi[b] = load_word(pi + (l0 + b) * e_plane, aligned, j0, n);
+        if (!REAL) wi[b] = load_word(pi + (l0 + b) * e_plane, aligned, j0, n);
       }
     }
 #pragma unroll
@@ -160,7 +162,16 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
     const int64_t j = j0 + q;
     if (j >= n) break;
     const int ex = -mi - nu[j];
-    if (SINGLE) {
+    if (REAL) {
+      // emulate_gemm_real: inverse_scale of the reduced real value, one cast
+      if (SINGLE) {
+        const double cr = reduce_single(__dadd_rn(s1r[q], s2r[q]), dc);
+        reinterpret_cast<float*>(C)[i * ldc + j] = __double2float_rn(ldexp_rn(cr, ex));
+      } else {
+        reinterpret_cast<double*>(C)[i * ldc + j] =
+            ldexp_rn(reduce_double(s1r[q], s2r[q], dc), ex);
+      }
+    } else if (SINGLE) {
       const double cr = reduce_single(__dadd_rn(s1r[q], s2r[q]), dc);
       const double ci = reduce_single(__dadd_rn(s1i[q], s2i[q]), dc);
       const float re = __double2float_rn(ldexp_rn(cr, ex));
@@ -187,22 +198,26 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
 
 }  // namespace
 
-int launch_crt(bool single, int64_t m, int64_t n, const int8_t* e_re, const int8_t* e_im,
-               int64_t e_plane, int64_t e_ld, const int32_t* mu, const int32_t* nu,
-               const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s, int max_ctas) {
+int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
+               const int8_t* e_im, int64_t e_plane, int64_t e_ld, const int32_t* mu,
+               const int32_t* nu, const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s,
+               int max_ctas) {
   const int64_t total = m * ((n + 3) / 4);
   if (total <= 0) return 0;
   int64_t g = (total + 255) / 256;
   if (max_ctas > 0 && max_ctas < g) g = max_ctas;
   const unsigned grid = unsigned(g);
   const bool limbs = dc.hi_scale != 0.0;
-  if (single) {
-    if (limbs) k_crt<true, true><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
-    else k_crt<true, false><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
+#define CRTG_CRT(S, L, R) \
+  k_crt<S, L, R><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
+  if (real) {
+    if (single) { if (limbs) CRTG_CRT(true, true, true); else CRTG_CRT(true, false, true); }
+    else { if (limbs) CRTG_CRT(false, true, true); else CRTG_CRT(false, false, true); }
   } else {
-    if (limbs) k_crt<false, true><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
-    else k_crt<false, false><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc);
+    if (single) { if (limbs) CRTG_CRT(true, true, false); else CRTG_CRT(true, false, false); }
+    else { if (limbs) CRTG_CRT(false, true, false); else CRTG_CRT(false, false, false); }
   }
+#undef CRTG_CRT
   return int(cudaGetLastError());
 }
 

@@ -40,6 +40,38 @@ __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr
     }
     return;
   }
+  if (MODE == EPI_REAL) {
+    // one product per modulus (emulate_gemm_real -> crt_integer_gemm, emulate.py:103-132):
+    // e = sym(D mod p).  |D| <= k*128^2 with k <= 2^17 can reach 2^31 only for p = 256
+    // with every product (-128)^2; the int32 accumulator then wraps to INT32_MIN,
+    // which is exactly the reference's ArithmeticError case (kernel.py:33-34).
+    int8_t* dst = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+    bool wrapped = false;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      uint32_t v[32];
+      tmem_ld32(taddr + c * 32, v);
+      tmem_wait_ld();
+      uint32_t out[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        uint32_t o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          wrapped |= v[4 * w + j] == 0x80000000u;
+          o[j] = uint32_t(to_sym(mod_i32(int32_t(v[4 * w + j]), mc), mc));
+        }
+        out[w] = ep_pack4(o[0], o[1], o[2], o[3] & 0xFF);
+      }
+      if (row_ok) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+        d4[0] = make_uint4(out[0], out[1], out[2], out[3]);
+        d4[1] = make_uint4(out[4], out[5], out[6], out[7]);
+      }
+    }
+    if (wrapped && row_ok && g.overflow) atomicAdd(g.overflow, 1ull);
+    return;
+  }
   int8_t* dst_base = nullptr;
   if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
   if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;

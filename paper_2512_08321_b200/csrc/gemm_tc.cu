@@ -258,6 +258,12 @@ int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {
       if (err != cudaSuccess) return int(err);
       k_gemm_i8<EPI_RAW><<<grid, 256, smem, stream>>>(g);
       break;
+    case EPI_REAL:
+      err = cudaFuncSetAttribute(k_gemm_i8<EPI_REAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(smem));
+      if (err != cudaSuccess) return int(err);
+      k_gemm_i8<EPI_REAL><<<grid, 256, smem, stream>>>(g);
+      break;
     default:
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_BOUND>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

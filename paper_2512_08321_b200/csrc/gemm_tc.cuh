@@ -7,7 +7,7 @@
 
 namespace crtg {
 
-enum EpiMode { EPI_KARATSUBA = 0, EPI_RAW = 1, EPI_BOUND = 2 };
+enum EpiMode { EPI_KARATSUBA = 0, EPI_RAW = 1, EPI_BOUND = 2, EPI_REAL = 3 };
 
 struct GemmArgs {
   const int8_t* a;   // packed A planes: [nl][planes_per_l] x (k_pad x 128*a_rb)
@@ -28,6 +28,7 @@ struct GemmArgs {
   int64_t raw_plane, raw_ld;
   int32_t* row_max;  // BOUND: [mt*128]
   int32_t* col_max;  // BOUND: [nt*256]
+  unsigned long long* overflow;  // REAL: int32 accumulator overflow (kernel.py:33-34)
   ModConst mc[CRTG_MAX_MODULI];
 };
 

@@ -7,6 +7,9 @@
 
 namespace crtg {
 
+// element type of an input matrix
+enum Elem { E_C128 = 0, E_C64 = 1, E_F64 = 2, E_F32 = 3 };
+
 // numpy pairwise-sum recursion of one row, flattened: leaves (start, len) in
 // order, internal nodes (left slot, right slot) sorted by height; value slot s
 // < nleaves is a leaf, else internal node s - nleaves.
@@ -20,14 +23,14 @@ struct PwTree {
 // ---- scaling (scaling.cu) ----
 // A rows: absmax (+ non-finite flag) and, in fast mode, the pairwise sum of
 // squares and the exponent.  Writes mu[i] (fast) or rowabs[i] (always).
-int launch_row_stats(bool single, bool fast, const void* A, int64_t lda, int64_t m, int64_t k,
+int launch_row_stats(int elem, bool fast, const void* A, int64_t lda, int64_t m, int64_t k,
                      const PwTree& tree, float p_fast, float delta, int32_t* mu, double* rowabs,
                      unsigned long long* diag, cudaStream_t s);
 // B columns: absmax per column (atomic max on the bit pattern) + non-finite flag.
-int launch_col_absmax(bool single, const void* B, int64_t ldb, int64_t k, int64_t n,
+int launch_col_absmax(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
                       double* colabs, unsigned long long* diag, cudaStream_t s);
 // B columns: sequential sums of squares (numpy axis-0 order) and the exponent.
-int launch_col_fast(bool single, const void* B, int64_t ldb, int64_t k, int64_t n,
+int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
                     const double* colabs, double* colsq, float p_fast, float delta, int32_t* nu,
                     unsigned long long* diag, cudaStream_t s);
 // accurate mode: bar = 5 - floor_log2(absmax) (0 for zero rows/cols)
@@ -41,8 +44,9 @@ int launch_accurate_exps(const int32_t* maxb, const double* absval, const int32_
 enum PackKind { PACK_RESIDUE = 0, PACK_BARS = 1 };
 // operand 0: rows of A (m x k row-major complex), exps per row;
 // operand 1: columns [col0, col0+rows) of B (k x n row-major complex), exps per column.
-// Writes planes [nplanes_mod][3] of k_pad x rb_count*128 packed bytes.
-int launch_pack(bool single, int operand, int kind, const void* X, int64_t ldx, int64_t rows,
+// Writes planes [N][3] (complex: re, im, re+im) or [N][1] (real) of
+// k_pad x rb_count*128 packed bytes.
+int launch_pack(int elem, int operand, int kind, const void* X, int64_t ldx, int64_t rows,
                 int64_t kdim, int64_t col0, const int32_t* exps, const DevConsts& dc,
                 int8_t* out, int64_t plane_bytes, int64_t rb_count,
                 unsigned long long* overflow_flag, cudaStream_t s, int max_ctas = 0,
@@ -56,7 +60,8 @@ int launch_unpack_i8(const int8_t* packed, int64_t rows, int64_t kdim, int64_t r
                      int8_t* out, cudaStream_t s);
 
 // ---- CRT reconstruction (crt.cu) ----
-int launch_crt(bool single, int64_t m, int64_t n, const int8_t* e_re, const int8_t* e_im,
+// real = true: e_im unused, C is a real f64 / f32 matrix
+int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re, const int8_t* e_im,
                int64_t e_plane, int64_t e_ld, const int32_t* mu, const int32_t* nu,
                const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s, int max_ctas = 0);
 

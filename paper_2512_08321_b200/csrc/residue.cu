@@ -20,22 +20,24 @@ namespace {
 constexpr int kTileRows = 32;  // operand rows per CTA
 constexpr int kThreads = 256;  // 32 rows x 8 sixteen-byte K chunks
 
-template <typename T>
-__device__ __forceinline__ void load_c(const T* p, double& re, double& im);
-template <>
-__device__ __forceinline__ void load_c<double>(const double* p, double& re, double& im) {
-  const double2 v = *reinterpret_cast<const double2*>(p);
-  re = v.x;
-  im = v.y;
-}
-template <>
-__device__ __forceinline__ void load_c<float>(const float* p, double& re, double& im) {
-  const float2 v = *reinterpret_cast<const float2*>(p);
-  re = double(v.x);
-  im = double(v.y);
+// element (row, h) of an operand: complex interleaved or real (im = 0)
+template <typename T, bool REAL>
+__device__ __forceinline__ void load_c(const T* p, double& re, double& im) {
+  if constexpr (REAL) {
+    re = double(*p);
+    im = 0.0;
+  } else if constexpr (sizeof(T) == 8) {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    re = v.x;
+    im = v.y;
+  } else {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    re = double(v.x);
+    im = double(v.y);
+  }
 }
 
-template <typename T, int OPERAND, int KIND>
+template <typename T, int OPERAND, int KIND, bool REAL>
 __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int64_t ldx, int rows,
                                                   int kdim, int64_t col0,
                                                   const int32_t* __restrict__ exps,
@@ -67,9 +69,9 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
     re[t] = 0.0;
     im[t] = 0.0;
     if (row_ok && h < kdim) {
-      const T* p = (OPERAND == 0) ? X + 2 * (int64_t(row) * ldx + h)
-                                  : X + 2 * (int64_t(h) * ldx + col0 + row);
-      load_c<T>(p, re[t], im[t]);
+      const T* p = (OPERAND == 0) ? X + (REAL ? 1 : 2) * (int64_t(row) * ldx + h)
+                                  : X + (REAL ? 1 : 2) * (int64_t(h) * ldx + col0 + row);
+      load_c<T, REAL>(p, re[t], im[t]);
     }
   }
 
@@ -196,7 +198,7 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
   }
 }
 
-template <typename T, int OPERAND>
+template <typename T, int OPERAND, bool REAL>
 __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, int64_t ldx, int rows,
                                                   int kdim, int64_t col0,
                                                   const int32_t* __restrict__ exps,
@@ -237,9 +239,9 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
     const int h = h0 + t;
     double re = 0.0, im = 0.0;
     if (row_ok && h < kdim) {
-      const T* p = (OPERAND == 0) ? X + 2 * (int64_t(row) * ldx + h)
-                                  : X + 2 * (int64_t(h) * ldx + col0 + row);
-      load_c<T>(p, re, im);
+      const T* p = (OPERAND == 0) ? X + (REAL ? 1 : 2) * (int64_t(row) * ldx + h)
+                                  : X + (REAL ? 1 : 2) * (int64_t(h) * ldx + col0 + row);
+      load_c<T, REAL>(p, re, im);
     }
     qr[t] = trunc(__dmul_rn(re, scale));
     qi[t] = trunc(__dmul_rn(im, scale));
@@ -266,22 +268,44 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
 
   for (int l = 0; l < dc.n; ++l) {
     const ResConst c = dc.rc[l];
-    uint32_t w[3][2];
-    if (wide)
-      residue_words<true>(vr, vi, c, w);
-    else
-      residue_words<false>(vr, vi, c, w);
+    if constexpr (REAL) {
+      // one plane per modulus (emulate_gemm_real: no imaginary part / Karatsuba sum)
+      uint32_t w0 = 0, w1 = 0;
+      if (wide) {
+        w0 = pack_sym(res_t<true>(vr[0], c), res_t<true>(vr[1], c), res_t<true>(vr[2], c),
+                      res_t<true>(vr[3], c), c.h);
+        w1 = pack_sym(res_t<true>(vr[4], c), res_t<true>(vr[5], c), res_t<true>(vr[6], c),
+                      res_t<true>(vr[7], c), c.h);
+      } else {
+        w0 = pack_sym(res_t<false>(vr[0], c), res_t<false>(vr[1], c), res_t<false>(vr[2], c),
+                      res_t<false>(vr[3], c), c.h);
+        w1 = pack_sym(res_t<false>(vr[4], c), res_t<false>(vr[5], c), res_t<false>(vr[6], c),
+                      res_t<false>(vr[7], c), c.h);
+      }
+      *reinterpret_cast<uint2*>(&stage[0][soff]) = make_uint2(w0, w1);
+      __syncthreads();
+      if (cq == 0)
+        reinterpret_cast<uint4*>(out + int64_t(l) * plane_bytes + goff)[cs] =
+            reinterpret_cast<const uint4*>(stage[0])[cs];
+      __syncthreads();
+    } else {
+      uint32_t w[3][2];
+      if (wide)
+        residue_words<true>(vr, vi, c, w);
+      else
+        residue_words<false>(vr, vi, c, w);
 #pragma unroll
-    for (int pl = 0; pl < 3; ++pl)
-      *reinterpret_cast<uint2*>(&stage[pl][soff]) = make_uint2(w[pl][0], w[pl][1]);
-    __syncthreads();
-    int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
-    reinterpret_cast<uint4*>(base + cq * plane_bytes)[cs] =
-        reinterpret_cast<const uint4*>(stage[cq])[cs];
-    if (cq == 0)
-      reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
-          reinterpret_cast<const uint4*>(stage[2])[cs];
-    __syncthreads();
+      for (int pl = 0; pl < 3; ++pl)
+        *reinterpret_cast<uint2*>(&stage[pl][soff]) = make_uint2(w[pl][0], w[pl][1]);
+      __syncthreads();
+      int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
+      reinterpret_cast<uint4*>(base + cq * plane_bytes)[cs] =
+          reinterpret_cast<const uint4*>(stage[cq])[cs];
+      if (cq == 0)
+        reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
+            reinterpret_cast<const uint4*>(stage[2])[cs];
+      __syncthreads();
+    }
   }
   }  // tile loop
 }
@@ -313,7 +337,7 @@ __global__ void k_unpack_i8(const int8_t* __restrict__ packed, int64_t rows, int
   out[t] = packed[pack_offset(r, h, rb_count)];
 }
 
-template <typename T, int OP, int KIND>
+template <typename T, int OP, int KIND, bool REAL>
 void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t col0,
                 const int32_t* exps, const DevConsts& dc, int8_t* out, int64_t plane_bytes,
                 int64_t rb_count, unsigned long long* overflow, cudaStream_t s, int max_ctas,
@@ -325,13 +349,13 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
     const int n_kb = int((kdim + 127) / 128), n_rt = int((extent + kResRows - 1) / kResRows);
     const int64_t tiles = int64_t(n_kb) * n_rt;
     const unsigned grid = unsigned(max_ctas > 0 && max_ctas < tiles ? max_ctas : tiles);
-    k_residues<T, OP><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows), int(kdim),
+    k_residues<T, OP, REAL><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows), int(kdim),
                                           col0, exps, dc, out, plane_bytes, rb_count, overflow,
                                           n_kb, n_rt, int(row_base));
   } else {
   // cover every padded row of the plane so the GEMM reads zeros there
   dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kTileRows));
-  k_pack<T, OP, KIND><<<grid, kThreads, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),
+  k_pack<T, OP, KIND, REAL><<<grid, kThreads, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),
                                                 int(kdim), col0, exps, dc, out, plane_bytes,
                                                 rb_count, overflow);
   }
@@ -339,27 +363,27 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
 
 }  // namespace
 
-int launch_pack(bool single, int operand, int kind, const void* X, int64_t ldx, int64_t rows,
+int launch_pack(int elem, int operand, int kind, const void* X, int64_t ldx, int64_t rows,
                 int64_t kdim, int64_t col0, const int32_t* exps, const DevConsts& dc,
                 int8_t* out, int64_t plane_bytes, int64_t rb_count,
                 unsigned long long* overflow, cudaStream_t s, int max_ctas, int64_t row_base,
                 int64_t fill_rows) {
   if (rows <= 0 || kdim <= 0) return 0;
-#define CRTG_PACK(T, OP, KIND) \
-  launch_one<T, OP, KIND>(X, ldx, rows, kdim, col0, exps, dc, out, plane_bytes, rb_count, overflow, s, max_ctas, row_base, fill_rows)
-  if (single) {
-    if (operand == 0) {
-      if (kind == PACK_BARS) CRTG_PACK(float, 0, PACK_BARS); else CRTG_PACK(float, 0, PACK_RESIDUE);
-    } else {
-      if (kind == PACK_BARS) CRTG_PACK(float, 1, PACK_BARS); else CRTG_PACK(float, 1, PACK_RESIDUE);
-    }
-  } else {
-    if (operand == 0) {
-      if (kind == PACK_BARS) CRTG_PACK(double, 0, PACK_BARS); else CRTG_PACK(double, 0, PACK_RESIDUE);
-    } else {
-      if (kind == PACK_BARS) CRTG_PACK(double, 1, PACK_BARS); else CRTG_PACK(double, 1, PACK_RESIDUE);
-    }
+#define CRTG_PACK(T, OP, KIND, R) \
+  launch_one<T, OP, KIND, R>(X, ldx, rows, kdim, col0, exps, dc, out, plane_bytes, rb_count, \
+                             overflow, s, max_ctas, row_base, fill_rows)
+#define CRTG_PACK_KIND(T, OP, R) \
+  if (kind == PACK_BARS) CRTG_PACK(T, OP, PACK_BARS, R); else CRTG_PACK(T, OP, PACK_RESIDUE, R);
+#define CRTG_PACK_OP(T, R) \
+  if (operand == 0) { CRTG_PACK_KIND(T, 0, R) } else { CRTG_PACK_KIND(T, 1, R) }
+  switch (elem) {
+    case E_C128: CRTG_PACK_OP(double, false) break;
+    case E_C64: CRTG_PACK_OP(float, false) break;
+    case E_F64: CRTG_PACK_OP(double, true) break;
+    default: CRTG_PACK_OP(float, true) break;
   }
+#undef CRTG_PACK_OP
+#undef CRTG_PACK_KIND
 #undef CRTG_PACK
   return int(cudaGetLastError());
 }

@@ -83,22 +83,21 @@ __device__ __forceinline__ double sq(const Pow2& p, double x) {
   return __dmul_rn(y, y);
 }
 
-template <typename T>
-struct C2;
-template <>
-struct C2<double> {
-  using V = double2;
-};
-template <>
-struct C2<float> {
-  using V = float2;
-};
-
-template <typename T>
-__device__ __forceinline__ void load_c(const T* row, int64_t h, double& re, double& im) {
-  const typename C2<T>::V v = reinterpret_cast<const typename C2<T>::V*>(row)[h];
-  re = double(v.x);
-  im = double(v.y);
+// element h of a row / column: complex (interleaved pairs) or real (im = 0)
+template <typename T, bool REAL>
+__device__ __forceinline__ void load_c(const T* base, int64_t h, double& re, double& im) {
+  if constexpr (REAL) {
+    re = double(base[h]);
+    im = 0.0;
+  } else if constexpr (sizeof(T) == 8) {
+    const double2 v = reinterpret_cast<const double2*>(base)[h];
+    re = v.x;
+    im = v.y;
+  } else {
+    const float2 v = reinterpret_cast<const float2*>(base)[h];
+    re = double(v.x);
+    im = double(v.y);
+  }
 }
 
 __device__ __forceinline__ double block_max(double v, double* red) {
@@ -114,7 +113,7 @@ __device__ __forceinline__ double block_max(double v, double* red) {
 
 // One CTA per row of A.  Pass 1: absmax over both parts; pass 2 (fast mode): the
 // pairwise sums of squares of re and im (numpy order), then the exponent.
-template <typename T>
+template <typename T, bool REAL>
 __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int64_t lda, int k,
                                                    PwTree tree, float p_fast, float delta,
                                                    int fast, int32_t* __restrict__ mu,
@@ -123,13 +122,13 @@ __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int6
   extern __shared__ double vals[];  // [2][nleaves + nnodes]
   __shared__ double red[8];
   const int64_t i = blockIdx.x;
-  const T* row = A + 2 * i * lda;
+  const T* row = A + (REAL ? 1 : 2) * i * lda;
 
   double mx = 0.0;
   int bad = 0;
   for (int h = threadIdx.x; h < k; h += blockDim.x) {
     double re, im;
-    load_c(row, h, re, im);
+    load_c<T, REAL>(row, h, re, im);
     bad |= !(isfinite(re) && isfinite(im));
     mx = fmax(mx, fmax(fabs(re), fabs(im)));
   }
@@ -154,11 +153,11 @@ __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int6
     if (len >= 8) {
       const int full = len - (len & 7);
       double re, im;
-      load_c(row, start + j, re, im);
+      load_c<T, REAL>(row, start + j, re, im);
       sr = sq(sc, re);
       si = sq(sc, im);
       for (int t = 8 + j; t < full; t += 8) {
-        load_c(row, start + t, re, im);
+        load_c<T, REAL>(row, start + t, re, im);
         sr = __dadd_rn(sr, sq(sc, re));
         si = __dadd_rn(si, sq(sc, im));
       }
@@ -173,7 +172,7 @@ __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int6
       // sequential tail (and whole leaf when len < 8: res = 0; res += a[i])
       for (int t = (len >= 8 ? len - (len & 7) : 0); t < len; ++t) {
         double re, im;
-        load_c(row, start + t, re, im);
+        load_c<T, REAL>(row, start + t, re, im);
         sr = __dadd_rn(sr, sq(sc, re));
         si = __dadd_rn(si, sq(sc, im));
       }
@@ -201,7 +200,7 @@ __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int6
 
 // Column absmax of B (k x n row-major complex): one thread per column, rows split
 // in chunks; order-free max merged with an atomic max on the bit pattern.
-template <typename T>
+template <typename T, bool REAL>
 __global__ void __launch_bounds__(128) k_col_absmax(const T* __restrict__ B, int64_t ldb, int k,
                                                     int n, int rows_per_chunk,
                                                     double* __restrict__ colabs,
@@ -215,7 +214,7 @@ __global__ void __launch_bounds__(128) k_col_absmax(const T* __restrict__ B, int
 #pragma unroll 8
     for (int h = h0; h < h1; ++h) {
       double re, im;
-      load_c(B + 2 * int64_t(h) * ldb, j, re, im);
+      load_c<T, REAL>(B + (REAL ? 1 : 2) * int64_t(h) * ldb, j, re, im);
       bad |= !(isfinite(re) && isfinite(im));
       mx = fmax(mx, fmax(fabs(re), fabs(im)));
     }
@@ -229,17 +228,21 @@ __global__ void __launch_bounds__(128) k_col_absmax(const T* __restrict__ B, int
 // Column sums of squares in numpy's axis-0 order: for each column and part a
 // sequential chain over k.  Thread t -> (column t/2, part t%2); a warp reads 16
 // columns x 16 bytes contiguously.
-template <typename T>
+template <typename T, bool REAL>
 __global__ void __launch_bounds__(128) k_col_sumsq(const T* __restrict__ B, int64_t ldb, int k,
                                                    int n, const double* __restrict__ colabs,
                                                    double* __restrict__ colsq) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int j = int(t >> 1), part = int(t & 1);
   if (j >= n) return;
+  if (REAL && part == 1) {  // no imaginary part: its sum of squares is 0
+    colsq[int64_t(n) + j] = 0.0;
+    return;
+  }
   const double mx = colabs[j];
   const Pow2 sc = make_pow2(mx == 0.0 ? 0 : -ilogb(mx));
-  const T* p = B + 2 * int64_t(j) + part;
-  const int64_t stride = 2 * ldb;
+  const T* p = B + (REAL ? 1 : 2) * int64_t(j) + part;
+  const int64_t stride = (REAL ? 1 : 2) * ldb;
   double s = 0.0;
   constexpr int U = 16;
   int h = 0;
@@ -293,51 +296,49 @@ __global__ void k_accurate_exps(const int32_t* __restrict__ maxb, const double* 
 
 }  // namespace
 
-int launch_row_stats(bool single, bool fast, const void* A, int64_t lda, int64_t m, int64_t k,
+#define CRTG_ELEM_DISPATCH(elem, ...)                                                    \
+  switch (elem) {                                                                       \
+    case E_C128: { using T = double; constexpr bool R = false; __VA_ARGS__; } break;     \
+    case E_C64:  { using T = float;  constexpr bool R = false; __VA_ARGS__; } break;     \
+    case E_F64:  { using T = double; constexpr bool R = true;  __VA_ARGS__; } break;     \
+    default:     { using T = float;  constexpr bool R = true;  __VA_ARGS__; } break;     \
+  }
+
+int launch_row_stats(int elem, bool fast, const void* A, int64_t lda, int64_t m, int64_t k,
                      const PwTree& tree, float p_fast, float delta, int32_t* mu, double* rowabs,
                      unsigned long long* diag, cudaStream_t s) {
   if (m <= 0) return 0;
   const size_t smem = fast ? size_t(2) * (tree.nleaves + tree.nnodes) * sizeof(double) : 0;
-  if (single) {
-    cudaFuncSetAttribute(k_row_stats<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CRTG_ELEM_DISPATCH(elem, {
+    cudaFuncSetAttribute(k_row_stats<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem > 48 * 1024 ? smem : 48 * 1024));
-    k_row_stats<float><<<unsigned(m), 256, smem, s>>>(static_cast<const float*>(A), lda, int(k),
-                                                      tree, p_fast, delta, fast, mu, rowabs, diag);
-  } else {
-    cudaFuncSetAttribute(k_row_stats<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem > 48 * 1024 ? smem : 48 * 1024));
-    k_row_stats<double><<<unsigned(m), 256, smem, s>>>(static_cast<const double*>(A), lda,
-                                                       int(k), tree, p_fast, delta, fast, mu,
-                                                       rowabs, diag);
-  }
+    k_row_stats<T, R><<<unsigned(m), 256, smem, s>>>(static_cast<const T*>(A), lda, int(k), tree,
+                                                     p_fast, delta, fast, mu, rowabs, diag);
+  })
   return int(cudaGetLastError());
 }
 
-int launch_col_absmax(bool single, const void* B, int64_t ldb, int64_t k, int64_t n,
+int launch_col_absmax(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
                       double* colabs, unsigned long long* diag, cudaStream_t s) {
   if (n <= 0) return 0;
   const int rows_per_chunk = 1024;
   dim3 grid(unsigned((n + 127) / 128), unsigned((k + rows_per_chunk - 1) / rows_per_chunk));
-  if (single)
-    k_col_absmax<float><<<grid, 128, 0, s>>>(static_cast<const float*>(B), ldb, int(k), int(n),
-                                             rows_per_chunk, colabs, diag);
-  else
-    k_col_absmax<double><<<grid, 128, 0, s>>>(static_cast<const double*>(B), ldb, int(k), int(n),
-                                              rows_per_chunk, colabs, diag);
+  CRTG_ELEM_DISPATCH(elem, {
+    k_col_absmax<T, R><<<grid, 128, 0, s>>>(static_cast<const T*>(B), ldb, int(k), int(n),
+                                            rows_per_chunk, colabs, diag);
+  })
   return int(cudaGetLastError());
 }
 
-int launch_col_fast(bool single, const void* B, int64_t ldb, int64_t k, int64_t n,
+int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
                     const double* colabs, double* colsq, float p_fast, float delta, int32_t* nu,
                     unsigned long long* diag, cudaStream_t s) {
   if (n <= 0) return 0;
   const unsigned grid = unsigned((2 * n + 127) / 128);
-  if (single)
-    k_col_sumsq<float><<<grid, 128, 0, s>>>(static_cast<const float*>(B), ldb, int(k), int(n),
-                                            colabs, colsq);
-  else
-    k_col_sumsq<double><<<grid, 128, 0, s>>>(static_cast<const double*>(B), ldb, int(k), int(n),
-                                             colabs, colsq);
+  CRTG_ELEM_DISPATCH(elem, {
+    k_col_sumsq<T, R><<<grid, 128, 0, s>>>(static_cast<const T*>(B), ldb, int(k), int(n), colabs,
+                                           colsq);
+  })
   k_col_finalize<<<unsigned((n + 127) / 128), 128, 0, s>>>(int(n), colabs, colsq, p_fast, delta,
                                                             nu, diag);
   return int(cudaGetLastError());

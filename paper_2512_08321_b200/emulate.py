@@ -30,7 +30,7 @@ from .errors import ConfigError, DimensionError, DomainError
 from .moduli import ModulusSet, ScalingConstants, device_constants, select_moduli
 
 __all__ = [
-    "ScalingVectors", "emulate_gemm_complex", "gemm", "gemm_i8_i32", "complex_gemm_mod",
+    "ScalingVectors", "emulate_gemm_complex", "emulate_gemm_real", "gemm", "gemm_i8_i32", "complex_gemm_mod",
     "fast_scaling", "accurate_scaling", "quantized_residues", "crt_reconstruct",
 ]
 
@@ -216,6 +216,100 @@ def run_complex(at: torch.Tensor, bt: torch.Tensor, cfg: EmuConfig,
     return out
 
 
+# ----------------------------------------------------------------------------
+# real domain (reference emulate.py:169-190)
+# ----------------------------------------------------------------------------
+def _real_operand(x, name: str, dev, reduce_axis: int):
+    """-> (device tensor holding the data, colmajor flag, leading dim, was_torch).
+
+    The reference keeps a real operand's memory layout (astype(copy=False)), and
+    numpy then sums squares pairwise along the innermost (smallest-stride) axis and
+    sequentially along the other.  The operand is shipped in the layout whose
+    contiguous axis is numpy's inner axis, so the library reproduces the order.
+    """
+    was_torch = isinstance(x, torch.Tensor)
+    if was_torch:
+        if x.dim() != 2:
+            raise DimensionError(f"{name} must be 2-D")
+        if x.is_complex():
+            raise DomainError(f"{name} must be real for real-domain emulation")
+        t = x
+    else:
+        arr = np.asarray(x)
+        if arr.ndim != 2:
+            raise DimensionError(f"{name} must be 2-D")
+        if np.iscomplexobj(arr):
+            raise DomainError(f"{name} must be real for real-domain emulation")
+    shape = tuple(t.shape) if was_torch else arr.shape
+    strides = (tuple(abs(v) for v in t.stride()) if was_torch
+               else tuple(abs(v) // max(arr.itemsize, 1) for v in arr.strides))
+    other = 1 - reduce_axis
+    # numpy's inner loop axis: the non-trivial axis with the smallest stride
+    if shape[reduce_axis] <= 1:
+        inner = other
+    elif shape[other] <= 1:
+        inner = reduce_axis
+    else:
+        inner = 0 if strides[0] < strides[1] else 1
+    colmajor = inner == 0  # axis 0 contiguous -> column-major storage
+    if was_torch:
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+        t = (t.t().contiguous().t() if colmajor else t.contiguous()).to(dev)
+        ld = t.stride(1) if colmajor else t.stride(0)
+        return t, colmajor, max(int(ld), 1), True
+    if arr.dtype not in (np.float32, np.float64):
+        arr = arr.astype(np.float64)
+    arr = np.asfortranarray(arr) if colmajor else np.ascontiguousarray(arr)
+    flat = torch.from_numpy(arr.ravel(order="F" if colmajor else "C"))
+    t = flat.to(dev)
+    ld = arr.shape[0] if colmajor else arr.shape[1]
+    return t, colmajor, max(int(ld), 1), False
+
+
+def emulate_gemm_real(a, b, cfg: EmuConfig | None = None, diagnostics: dict | None = None):
+    """Emulated real matrix product A @ B (reference emulate.py:169-190)."""
+    cfg = cfg or EmuConfig()
+    if cfg.domain != "real":
+        raise ConfigError("config domain must be 'real'")
+    dev = _device()
+    ash = tuple(a.shape) if isinstance(a, torch.Tensor) else np.shape(a)
+    bsh = tuple(b.shape) if isinstance(b, torch.Tensor) else np.shape(b)
+    at, a_col, lda, a_torch = _real_operand(a, "A", dev, 1)
+    bt, b_col, ldb, b_torch = _real_operand(b, "B", dev, 0)
+    if ash[1] != bsh[0]:
+        raise DimensionError(f"inner dimensions differ: {ash} x {bsh}")
+    m, k = ash
+    n = bsh[1]
+    k_cap = MAX_K_REAL if cfg.mode == "fast" else MAX_K_COMPLEX
+    if k > k_cap:
+        raise DimensionError(f"inner dimension {k} exceeds {k_cap}")
+    if at.dtype != bt.dtype:
+        at, bt = at.to(torch.float64), bt.to(torch.float64)
+    nmod = cfg.resolved_moduli
+    prec = nat.SINGLE if cfg.precision == "single" else nat.DOUBLE
+    if at.dtype == torch.float32:
+        prec |= 16  # CRTG_IN_F32
+    mode = nat.FAST if cfg.mode == "fast" else nat.ACCURATE
+    lib = nat.load()
+    ws = _workspace(lib.crtg_real_workspace_size(prec, mode, m, n, k, nmod, cfg.n_block), dev)
+    out = torch.empty((m, n), dtype=torch.float32 if cfg.precision == "single" else torch.float64,
+                      device=dev)
+    diag = torch.zeros(nat.DIAG_LEN, dtype=torch.int64, device=dev)
+    nat.call("crtg_gemm_real", prec, mode, m, n, k, at.data_ptr(), lda, int(a_col),
+             bt.data_ptr(), ldb, int(b_col), out.data_ptr(), out.stride(0),
+             ctypes.byref(device_constants(nmod)), cfg.n_block, ws.data_ptr(), ws.numel(),
+             None, None, diag.data_ptr(), 1, _stream_ptr(dev))
+    if diagnostics is not None:
+        d = diag.cpu().tolist()
+        for key, idx in (("clamped_mu", nat.DIAG_CLAMPED_MU), ("clamped_nu", nat.DIAG_CLAMPED_NU)):
+            if d[idx]:
+                diagnostics[key] = diagnostics.get(key, 0) + int(d[idx])
+    if a_torch and b_torch:
+        return out
+    return out.cpu().numpy()
+
+
 def _colmajor_view(buf, ld, rows, cols, name):
     """Column-major view with leading dimension (reference emulate.py:243-253)."""
     if isinstance(buf, torch.Tensor):
@@ -252,9 +346,9 @@ def gemm(domain: str, precision: str, m: int, n: int, k: int, a, lda: int, b, ld
     bv = _colmajor_view(b, ldb, k, n, "B")
     cv = _colmajor_view(c, ldc, m, n, "C")
     if domain == "real":
-        raise ConfigError("real-domain emulation is outside this build's hot path "
-                          "(emulate_gemm_real); use domain='complex'")
-    result = emulate_gemm_complex(av, bv, cfg)
+        result = emulate_gemm_real(av, bv, cfg)
+    else:
+        result = emulate_gemm_complex(av, bv, cfg)
     if isinstance(cv, torch.Tensor):
         cv.copy_(torch.as_tensor(result).to(cv.device, cv.dtype))
     else:

@@ -142,12 +142,71 @@ def hash_case(tag, m, n, k, phi, seed, precision, mode, N):
     }
 
 
+# real domain (emulate_gemm_real, emulate.py:169-190)
+REAL_CASES = [
+    ("r_fast_15", 37, 29, 53, 0.5, 40, "double", "fast", 15),
+    ("r_fast_20", 33, 40, 150, 4.0, 41, "double", "fast", 20),
+    ("r_accu_15", 35, 41, 67, 1.0, 42, "double", "accurate", 15),
+    ("r_fast_8s", 31, 27, 45, 0.5, 43, "single", "fast", 8),
+    ("r_accu_7s", 25, 26, 70, 1.0, 44, "single", "accurate", 7),
+    ("r_fast_2", 4, 5, 6, 0.0, 45, "double", "fast", 2),
+    ("r_tiny", 1, 1, 1, 0.5, 46, "double", "fast", 15),
+]
+
+
+def real_case(tag, m, n, k, phi, seed, precision, mode, N):
+    a = ref.gen_matrix(ref.GenSpec(m, k, phi, seed, precision, "real"))
+    b = ref.gen_matrix(ref.GenSpec(k, n, phi, seed + 1, precision, "real"))
+    cfg = ref.EmuConfig(precision=precision, domain="real", mode=mode, num_moduli=N)
+    diag = {}
+    c = ref.emulate_gemm_real(a, b, cfg, diag)
+    ms = ref.select_moduli(N)
+    sc = ref.ScalingConstants.from_product(ms.product)
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    sv = (ref.fast_scaling if mode == "fast" else ref.accurate_scaling)(a64, b64, ms, sc)
+    ai = ref.quantize(a64, sv.mu_exp, 0)
+    bi = ref.quantize(b64, sv.nu_exp, 1)
+    ra = ref.residue_decompose(ai, ms).entries
+    rb = ref.residue_decompose(bi, ms).entries
+    e = np.stack([ref.symmetric_mod_int(ref.gemm_i8_i32(ra[i], rb[i]).astype(np.int64), p)
+                  for i, p in enumerate(ms.moduli)]).astype(np.int8)
+    p_ = f"{tag}__"
+    return {
+        p_ + "rmeta": np.array([m, n, k, seed, N, precision == "double", mode == "fast"],
+                               np.int64),
+        p_ + "phi": np.array(phi), p_ + "a_sha": np.array(sha(a)), p_ + "b_sha": np.array(sha(b)),
+        p_ + "mu": sv.mu_exp, p_ + "nu": sv.nu_exp, p_ + "ra": ra, p_ + "rb": rb, p_ + "e": e,
+        p_ + "c": c,
+        p_ + "diag": np.array([diag.get("clamped_mu", 0), diag.get("clamped_nu", 0)]),
+    }
+
+
+REAL_HASH_CASES = [
+    ("real512_fast15", 512, 512, 512, 1.0, 50, "double", "fast", 15),
+    ("real384_accu15", 384, 320, 448, 2.0, 51, "double", "accurate", 15),
+    ("real512_fast8s", 512, 512, 512, 1.0, 52, "single", "fast", 8),
+    ("real_k2pow17_fast", 8, 6, 131072, 1.0, 53, "double", "fast", 15),
+]
+
+
+def real_hash_case(tag, m, n, k, phi, seed, precision, mode, N):
+    a = ref.gen_matrix(ref.GenSpec(m, k, phi, seed, precision, "real"))
+    b = ref.gen_matrix(ref.GenSpec(k, n, phi, seed + 1, precision, "real"))
+    cfg = ref.EmuConfig(precision=precision, domain="real", mode=mode, num_moduli=N)
+    c = ref.emulate_gemm_real(a, b, cfg)
+    return {"m": m, "n": n, "k": k, "phi": phi, "seed": seed, "precision": precision,
+            "mode": mode, "N": N, "domain": "real", "a_sha": sha(a), "b_sha": sha(b),
+            "c_sha": sha(c), "c_head": [float(v) for v in c.reshape(-1)[:4]]}
+
+
 def main():
     fx = {}
     fx.update(moduli_fixture())
     fx.update(log2_fixture())
     for case in SMALL_CASES:
         fx.update(small_case(*case))
+    for case in REAL_CASES:
+        fx.update(real_case(*case))
     # exponents with long pairwise rows (k > 128 blocks, ragged tails)
     for k in (7, 127, 129, 1000, 4100, 70001):
         a = ref.gen_matrix(ref.GenSpec(3, k, 4.0, 100 + k, "double", "complex"))
@@ -161,6 +220,9 @@ def main():
     hashes = {}
     for case in HASH_CASES:
         hashes[case[0]] = hash_case(*case)
+        print("hashed", case[0], file=sys.stderr)
+    for case in REAL_HASH_CASES:
+        hashes[case[0]] = real_hash_case(*case)
         print("hashed", case[0], file=sys.stderr)
     with open(os.path.join(HERE, "golden_hashes.json"), "w") as f:
         json.dump(hashes, f, indent=1)

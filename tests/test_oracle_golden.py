@@ -107,3 +107,36 @@ def test_pairwise_tree_matches_numpy():
             return rec(s, h) + rec(s + h, ln - h)
 
         assert 0.0 + rec(0, k) == np.sum(x[None, :], axis=1)[0]
+
+
+def _real_cases(golden):
+    return sorted({k.split("__")[0] for k in golden.files if k.endswith("__rmeta")})
+
+
+def test_real_small_cases_every_stage(golden):
+    for tag in _real_cases(golden):
+        g = lambda s: golden[f"{tag}__{s}"]  # noqa: E731
+        m, n, k, seed, N, dbl, fast = g("rmeta").tolist()
+        prec = "double" if dbl else "single"
+        mode = "fast" if fast else "accurate"
+        a = orc.gen_matrix(m, k, float(g("phi")), seed, prec, "real")
+        b = orc.gen_matrix(k, n, float(g("phi")), seed + 1, prec, "real")
+        assert _sha(a) == str(g("a_sha")) and _sha(b) == str(g("b_sha")), tag
+        diag = {}
+        c, st = orc.emulate_real(a, b, N, mode, prec, diag, return_stages=True)
+        assert np.array_equal(st["mu"], g("mu")) and np.array_equal(st["nu"], g("nu")), tag
+        for key in ("ra", "rb", "e"):
+            assert np.array_equal(st[key], g(key)), (tag, key)
+        assert c.dtype == g("c").dtype and c.tobytes() == g("c").tobytes(), tag
+        assert [diag.get("clamped_mu", 0), diag.get("clamped_nu", 0)] == g("diag").tolist()
+
+
+@pytest.mark.parametrize("tag", ["real512_fast15", "real384_accu15", "real512_fast8s",
+                                 "real_k2pow17_fast"])
+def test_real_hash_cases(golden_hashes, tag):
+    h = golden_hashes[tag]
+    a = orc.gen_matrix(h["m"], h["k"], h["phi"], h["seed"], h["precision"], "real")
+    b = orc.gen_matrix(h["k"], h["n"], h["phi"], h["seed"] + 1, h["precision"], "real")
+    assert _sha(a) == h["a_sha"] and _sha(b) == h["b_sha"]
+    c = orc.emulate_real(a, b, h["N"], h["mode"], h["precision"])
+    assert _sha(c) == h["c_sha"]
