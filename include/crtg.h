@@ -220,6 +220,23 @@ int crtg_crt_reconstruct(int precision, int64_t m, int64_t n, const int8_t* e_re
                          const int8_t* e_im, const int32_t* mu, const int32_t* nu,
                          const crtg_consts* K, void* C, int64_t ldc, void* stream);
 
+/* ---- accuracy harness ---- */
+
+/* Double-double reference product, bit-identical to the reference's
+ * reference_gemm_dd (oracle.py:60-128): hi + lo per entry (~106 bits), terms of
+ * the stacked real forms in ascending order.  is_complex: A, B, hi, lo are
+ * complex128 (interleaved), else float64.  Row-major, strides in elements. */
+int crtg_dd_gemm(int is_complex, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                 const void* B, int64_t ldb, void* hi, void* lo, int64_t ldo, void* stream);
+
+/* max_relative_error (oracle.py:131-169) of `approx` (complex128/complex64 or
+ * float64/float32 with approx_single) against (hi, lo): *max_bits receives the
+ * IEEE bits of the largest componentwise relative error (atomic max; zero it
+ * first), *zero_count the number of components with a zero reference. */
+int crtg_max_relative_error(int is_complex, int64_t m, int64_t n, const void* approx,
+                            int approx_single, int64_t ld_approx, const void* hi, const void* lo,
+                            int64_t ldo, uint64_t* max_bits, uint64_t* zero_count, void* stream);
+
 /* ---- instrumentation (bench.py) ---- */
 /* total kernels this library has launched in the process */
 uint64_t crtg_launch_count(void);

@@ -57,6 +57,10 @@ SIGNATURES = {
     "crtg_accurate_partial": (_c_int, [_c_int, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp, _c_i64,
                                        _vp, _vp, _sz, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "crtg_accurate_exponents": (_c_int, [_c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "crtg_dd_gemm": (_c_int, [_c_int, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp, _c_i64, _vp,
+                              _vp, _c_i64, _vp]),
+    "crtg_max_relative_error": (_c_int, [_c_int, _c_i64, _c_i64, _vp, _c_int, _c_i64, _vp, _vp,
+                                         _c_i64, _vp, _vp, _vp]),
     "crtg_launch_count": (ctypes.c_uint64, []),
     "crtg_profile_enable": (_c_int, [_c_int]),
     "crtg_profile_read": (_c_int, [_vp, _vp]),

@@ -1397,3 +1397,34 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
   if (sync_check) return check_diag(dg, s);
   return CRTG_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Accuracy harness: reference_gemm_dd + max_relative_error
+// ---------------------------------------------------------------------------
+extern "C" int crtg_dd_gemm(int is_complex, int64_t m, int64_t n, int64_t k, const void* A,
+                            int64_t lda, const void* B, int64_t ldb, void* hi, void* lo,
+                            int64_t ldo, void* stream) {
+  if (m < 1 || n < 1 || k < 1) return fail(CRTG_ERR_DIMENSION, "m, n, k must be positive");
+  if (lda < k || ldb < n || ldo < n) return fail(CRTG_ERR_DIMENSION, "leading dimension too small");
+  g_launches += 1;
+  CRTG_TRY(launch_dd_gemm(is_complex != 0, m, n, k, static_cast<const double*>(A), lda,
+                          static_cast<const double*>(B), ldb, static_cast<double*>(hi),
+                          static_cast<double*>(lo), ldo, static_cast<cudaStream_t>(stream)),
+           "dd gemm");
+  return CRTG_OK;
+}
+
+extern "C" int crtg_max_relative_error(int is_complex, int64_t m, int64_t n, const void* approx,
+                                       int approx_single, int64_t ld_approx, const void* hi,
+                                       const void* lo, int64_t ldo, uint64_t* max_bits,
+                                       uint64_t* zero_count, void* stream) {
+  if (m < 1 || n < 1) return fail(CRTG_ERR_DIMENSION, "empty matrix");
+  g_launches += 1;
+  CRTG_TRY(launch_max_rel_err(is_complex != 0, m, n, approx, approx_single != 0, ld_approx,
+                              static_cast<const double*>(hi), static_cast<const double*>(lo), ldo,
+                              reinterpret_cast<unsigned long long*>(max_bits),
+                              reinterpret_cast<unsigned long long*>(zero_count),
+                              static_cast<cudaStream_t>(stream)),
+           "max relative error");
+  return CRTG_OK;
+}

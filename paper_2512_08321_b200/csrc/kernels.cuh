@@ -65,4 +65,12 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
                int64_t e_plane, int64_t e_ld, const int32_t* mu, const int32_t* nu,
                const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s, int max_ctas = 0);
 
+// ---- accuracy harness (accuracy.cu) ----
+int launch_dd_gemm(bool cplx, int64_t m, int64_t n, int64_t k, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, double* hi, double* lo, int64_t ldo,
+                   cudaStream_t s);
+int launch_max_rel_err(bool cplx, int64_t m, int64_t n, const void* approx, bool approx_single,
+                       int64_t lda_x, const double* hi, const double* lo, int64_t ldo,
+                       unsigned long long* max_bits, unsigned long long* zeros, cudaStream_t s);
+
 }  // namespace crtg

@@ -199,6 +199,28 @@ def real_hash_case(tag, m, n, k, phi, seed, precision, mode, N):
             "c_sha": sha(c), "c_head": [float(v) for v in c.reshape(-1)[:4]]}
 
 
+# double-double reference products (oracle.py:60-128), the accuracy harness's target
+DD_CASES = [
+    ("dd_c1", 20, 30, 40, 0.5, 60, "complex"),
+    ("dd_c2", 7, 5, 300, 4.0, 61, "complex"),
+    ("dd_c3", 33, 17, 129, 2.0, 62, "complex"),
+    ("dd_r1", 19, 23, 77, 1.0, 63, "real"),
+]
+
+
+def dd_case(tag, m, n, k, phi, seed, domain):
+    a = ref.gen_matrix(ref.GenSpec(m, k, phi, seed, "double", domain))
+    b = ref.gen_matrix(ref.GenSpec(k, n, phi, seed + 1, "double", domain))
+    dd = ref.reference_gemm_dd(a, b)
+    approx = a.astype(np.complex64 if domain == "complex" else np.float32) @ \
+        b.astype(np.complex64 if domain == "complex" else np.float32)
+    err, zeros = ref.max_relative_error(approx, dd, return_zero_count=True)
+    p_ = f"{tag}__"
+    return {p_ + "ddmeta": np.array([m, n, k, seed, domain == "complex"], np.int64),
+            p_ + "phi": np.array(phi), p_ + "hi": dd.hi, p_ + "lo": dd.lo,
+            p_ + "approx": approx, p_ + "err": np.array([err, zeros])}
+
+
 def main():
     fx = {}
     fx.update(moduli_fixture())
@@ -207,6 +229,8 @@ def main():
         fx.update(small_case(*case))
     for case in REAL_CASES:
         fx.update(real_case(*case))
+    for case in DD_CASES:
+        fx.update(dd_case(*case))
     # exponents with long pairwise rows (k > 128 blocks, ragged tails)
     for k in (7, 127, 129, 1000, 4100, 70001):
         a = ref.gen_matrix(ref.GenSpec(3, k, 4.0, 100 + k, "double", "complex"))

@@ -140,3 +140,19 @@ def test_real_hash_cases(golden_hashes, tag):
     assert _sha(a) == h["a_sha"] and _sha(b) == h["b_sha"]
     c = orc.emulate_real(a, b, h["N"], h["mode"], h["precision"])
     assert _sha(c) == h["c_sha"]
+
+
+def test_dd_gemm_oracle(golden):
+    tags = sorted({k.split("__")[0] for k in golden.files if k.endswith("__ddmeta")})
+    assert tags
+    for tag in tags:
+        m, n, k, seed, cplx = golden[f"{tag}__ddmeta"].tolist()
+        phi = float(golden[f"{tag}__phi"])
+        dom = "complex" if cplx else "real"
+        a = orc.gen_matrix(m, k, phi, seed, "double", dom)
+        b = orc.gen_matrix(k, n, phi, seed + 1, "double", dom)
+        hi, lo = orc.dd_gemm(a, b)
+        assert hi.tobytes() == golden[f"{tag}__hi"].tobytes(), tag
+        assert lo.tobytes() == golden[f"{tag}__lo"].tobytes(), tag
+        err = orc.max_relative_error(golden[f"{tag}__approx"], hi, lo)
+        assert err == float(golden[f"{tag}__err"][0]), tag
