@@ -124,12 +124,15 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- helpers
 def peaks():
+    """(bf16 burst, bf16 sustained, HBM GB/s, source) from MEASURED_PEAKS.json,
+    else the profiling guide's fallback (1590 burst / ~1400 sustained / 6650)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p.get("bf16_tflops", 1590.0), p.get("hbm_gbs", 6650.0), "measured"
+        return (p.get("bf16_tflops", 1590.0), p.get("bf16_tflops_sustained", 1400.0),
+                p.get("hbm_gbs", 6650.0), "measured")
     except Exception:
-        return 1590.0, 6650.0, "fallback"
+        return 1590.0, 1400.0, 6650.0, "fallback"
 
 
 def profile_traffic():
@@ -276,20 +279,24 @@ def run_ours(a, rank: int, world: int, local_rank: int):
 
     # roofline of the dominant kernel (K3 tcgen05 GEMM): algorithmic INT8 ops per
     # launch = 6 * N * m * n_block * k (3 GEMMs x 2 ops/MAC x N moduli)
-    bf16, hbm, src = peaks()
+    bf16, bf16_sus, hbm, src = peaks()
     launches_gemm = max(1, stage_n["gemm"])
     gemm_ms = stage_ms["gemm"] / launches_gemm
     ops_launch = 6.0 * a.moduli * a.m * a.n * a.k * a.steps / launches_gemm
     achieved = ops_launch / (gemm_ms * 1e-3) / 1e12
-    peak_int8 = 2.0 * bf16
+    # K3 runs inside a long, power-capped step -> the SUSTAINED figure is the
+    # denominator (B200 dense INT8 rate = 2 x dense BF16)
+    peak_int8 = 2.0 * bf16_sus
     traffic = profile_traffic()
     roof = {"bound": "tensor", "kernel": "k_gemm_i8<EPI_KARATSUBA>", "achieved": achieved,
             "peak": peak_int8, "unit": "TOPS", "frac": achieved / peak_int8,
-            "peak_note": f"INT8 dense = 2 x {src} bf16 ({bf16} TF/s, MEASURED_PEAKS.json); "
-                         "spec 4500 TOPS",
-            "frac_of_spec": achieved / 4500.0,
+            "peak_note": f"INT8 dense = 2 x {src} SUSTAINED bf16 ({bf16_sus} TF/s, "
+                         f"MEASURED_PEAKS.json; kernel timed inside a long step); burst 2 x {bf16}; "
+                         "spec 4500",
+            "frac_of_burst": achieved / (2.0 * bf16), "frac_of_spec": achieved / 4500.0,
             "ops_per_launch": ops_launch, "ms_per_launch": gemm_ms,
-            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None}
+            "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+            "traffic_note": traffic.get("config") if traffic else None}
     stages = {k: v / a.steps for k, v in stage_ms.items()}
 
     result = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
