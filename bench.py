@@ -51,9 +51,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--m", type=int, default=16384)
-    ap.add_argument("--n", type=int, default=16384)
-    ap.add_argument("--k", type=int, default=16384)
+    ap.add_argument("--shape", type=int, nargs=3, default=[16384, 16384, 16384],
+                    metavar=("M", "N", "K"), help="per-GPU m n k")
     ap.add_argument("--moduli", type=int, default=15)
     ap.add_argument("--mode", choices=("fast", "accurate"), default="fast")
     ap.add_argument("--precision", choices=("double", "single"), default="double")
@@ -66,7 +65,9 @@ def parse():
                     help="skip the live max-relative-error check (GPU double-double reference)")
     ap.add_argument("--cpu-sample", type=int, default=128,
                     help="rows/cols of the CPU sample block (k kept full)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.m, a.n, a.k = a.shape
+    return a
 
 
 def workload_name(a) -> str:
@@ -109,6 +110,7 @@ class ClockSampler:
         self._stop.set()
         if self._t:
             self._t.join(timeout=10)
+        self.rows = [r for r in self.rows if len(r) >= 9]  # skip error / partial lines
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
@@ -214,10 +216,17 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     import paper_2512_08321_b200 as crt
     from paper_2512_08321_b200 import _native as nat
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local_rank % max(ndev, 1))
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL over NVLink on the box; CRTG_BENCH_BACKEND=gloo lets the multi-rank
+        # logic be exercised with several ranks sharing one GPU (CI only)
+        backend = os.environ.get("CRTG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     # 2-D grid of output tiles for weak scaling
     R = 1 << (int(math.log2(world)) // 2)
     Cc = world // R
@@ -253,7 +262,7 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     nat.profile_enable(True)
     nat.profile_read()  # clear
     launches0 = nat.launch_count()
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev.index)
     sampler.start()
     stream = torch.cuda.current_stream(dev)
     e0 = torch.cuda.Event(enable_timing=True)
@@ -268,11 +277,15 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     launches = nat.launch_count() - launches0
     stage_ms, stage_n = nat.profile_read()
     nat.profile_enable(False)
-    ms_total = e0.elapsed_time(e1)
-    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
-    if world > 1:
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        on_dev = dist.get_backend() == "nccl"
+        t = torch.tensor([x], dtype=torch.float64, device=dev if on_dev else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
+        return float(t.item())
+
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms_total / a.steps
     flops_step = 8.0 * a.m * a.n * a.k * world
     value = flops_step / (ms_step * 1e-3) / 1e12
@@ -288,6 +301,9 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     # denominator (B200 dense INT8 rate = 2 x dense BF16)
     peak_int8 = 2.0 * bf16_sus
     traffic = profile_traffic()
+    if traffic and [traffic.get(k) for k in ("m", "n", "k", "N", "n_block", "mode")] != \
+            [a.m, a.n, a.k, a.moduli, a.n_block, a.mode]:
+        traffic = None  # the committed capture is for another configuration
     roof = {"bound": "tensor", "kernel": "k_gemm_i8<EPI_KARATSUBA>", "achieved": achieved,
             "peak": peak_int8, "unit": "TOPS", "frac": achieved / peak_int8,
             "peak_note": f"INT8 dense = 2 x {src} SUSTAINED bf16 ({bf16_sus} TF/s, "
@@ -308,7 +324,9 @@ def run_ours(a, rank: int, world: int, local_rank: int):
                          "num_moduli": a.moduli, "mode": a.mode, "precision": a.precision,
                          "phi": a.phi, "n_block": a.n_block, "grid": f"{R}x{Cc}",
                          "parallelism": f"output-tile x{world}",
-                         "l2": "inputs (4 GiB each) exceed L2; no flush"},
+                         "l2": f"inputs ({A.numel() * A.element_size() / 2**30:.2f} GiB and "
+                               f"{B.numel() * B.element_size() / 2**30:.2f} GiB) vs 126 MB L2; "
+                               "no flush"},
               "stage_ms_per_step": stages, "gpu_launches": int(launches),
               "roofline": roof, "clocks": clocks}
 
@@ -391,11 +409,7 @@ def run_ours(a, rank: int, world: int, local_rank: int):
         for _ in range(reps):
             e2e_step()
         barrier()
-        dt = (time.perf_counter() - t0) / reps
-        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt = float(tt.item())
+        dt = max_over_ranks((time.perf_counter() - t0) / reps)
         result["e2e"] = {"value": flops_step / dt / 1e12, "unit": UNIT,
                          "h2d_bytes_per_step": int(hA.numel() * hA.element_size()
                                                    + hB.numel() * hB.element_size()),
