@@ -205,6 +205,7 @@ DevConsts make_dev(const crtg_consts& K) {
     rc.magic = mc.magic;
     rc.shift = mc.is_pow2 ? -1 : mc.shift;  // -1 marks p = 256 (mask)
     rc.p = p;
+    rc.neg_p = uint32_t(-p);
     {
       uint64_t c = 1 % uint64_t(p);
       for (int i = 0; i < 6; ++i) {

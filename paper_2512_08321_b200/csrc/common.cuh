@@ -56,6 +56,7 @@ struct ModConst {
 struct ResConst {
   uint32_t c32, c16, k, h, magic, sum_k;  // sum_k = p - h (re + im plane)
   int32_t shift, p;
+  uint32_t neg_p;                          // (uint32)(-p): t = u + q * neg_p
   // wide values (|a'| >= 2^53): v = 2^90 + a' in six 16-bit limbs,
   // u = sum_i limb_i * (2^(16 i) mod p) + kw  ==  a' + h  (mod p)
   uint32_t cw[6], kw;

@@ -155,18 +155,33 @@ __device__ __forceinline__ Val3 split_wide(double q) {
   return {uint32_t(v), uint32_t(v >> 32), uint32_t(v >> 64)};
 }
 
+// explicit single-instruction integer ops (keeps ptxas from re-associating the
+// chains into forms that need register copies of uniform operands)
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t mod_small(uint32_t u, const ResConst& c) {
-  return c.shift < 0 ? (u & 0xFFu) : u - uint32_t(c.p) * (__umulhi(u, c.magic) >> c.shift);
+  if (c.shift < 0) return u & 0xFFu;
+  const uint32_t q = __umulhi(u, c.magic) >> c.shift;
+  return mad_lo(q, c.neg_p, u);  // u - q*p
 }
 
 template <bool WIDE>
 __device__ __forceinline__ uint32_t res_t(const Val3& v, const ResConst& c) {
   uint32_t u;
   if (WIDE) {
-    u = (v.w0 & 0xFFFFu) + (v.w0 >> 16) * c.cw[1] + (v.w1 & 0xFFFFu) * c.cw[2] +
-        (v.w1 >> 16) * c.cw[3] + (v.w2 & 0xFFFFu) * c.cw[4] + (v.w2 >> 16) * c.cw[5] + c.kw;
+    u = (v.w0 & 0xFFFFu) + c.kw;
+    u = mad_lo(v.w0 >> 16, c.cw[1], u);
+    u = mad_lo(v.w1 & 0xFFFFu, c.cw[2], u);
+    u = mad_lo(v.w1 >> 16, c.cw[3], u);
+    u = mad_lo(v.w2 & 0xFFFFu, c.cw[4], u);
+    u = mad_lo(v.w2 >> 16, c.cw[5], u);
   } else {
-    u = v.w0 * c.c32 + v.w1 * c.c16 + v.w2 + c.k;
+    // ll + k, then + lh*(2^16 mod p), then + hi*(2^32 mod p)
+    u = mad_lo(v.w0, c.c32, mad_lo(v.w1, c.c16, v.w2 + c.k));
   }
   return mod_small(u, c);  // t = (a' + h) mod p
 }
@@ -282,12 +297,28 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
         w1 = pack_sym(res_t<false>(vr[4], c), res_t<false>(vr[5], c), res_t<false>(vr[6], c),
                       res_t<false>(vr[7], c), c.h);
       }
-      *reinterpret_cast<uint2*>(&stage[0][soff]) = make_uint2(w0, w1);
-      __syncthreads();
-      if (cq == 0)
-        reinterpret_cast<uint4*>(out + int64_t(l) * plane_bytes + goff)[cs] =
-            reinterpret_cast<const uint4*>(stage[0])[cs];
-      __syncthreads();
+      if (OPERAND == 0) {
+        *reinterpret_cast<uint2*>(out + int64_t(l) * plane_bytes + goff + soff) = make_uint2(w0, w1);
+      } else {
+        *reinterpret_cast<uint2*>(&stage[0][soff]) = make_uint2(w0, w1);
+        __syncthreads();
+        if (cq == 0)
+          reinterpret_cast<uint4*>(out + int64_t(l) * plane_bytes + goff)[cs] =
+              reinterpret_cast<const uint4*>(stage[0])[cs];
+        __syncthreads();
+      }
+    } else if (OPERAND == 0) {
+      // A rows: the 16 lanes of a row cover its whole 128-byte line of the plane,
+      // so a warp store is already two full lines — no staging needed
+      uint32_t w[3][2];
+      if (wide)
+        residue_words<true>(vr, vi, c, w);
+      else
+        residue_words<false>(vr, vi, c, w);
+      int8_t* base = out + int64_t(3 * l) * plane_bytes + goff + soff;
+#pragma unroll
+      for (int pl = 0; pl < 3; ++pl)
+        *reinterpret_cast<uint2*>(base + pl * plane_bytes) = make_uint2(w[pl][0], w[pl][1]);
     } else {
       uint32_t w[3][2];
       if (wide)
