@@ -121,7 +121,17 @@ bool pair_enabled() {
   return on;
 }
 
-int run_gemm(int mode, const GemmArgs& g, cudaStream_t s) {
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
+
+// CRTG_GROUP_M: raster experiment knob (default 16 row tiles per column
+// sweep; 8 / 32 read 20-30% more DRAM, profiles/r01_gemm_raster_experiment.json)
+int run_gemm(int mode, const GemmArgs& g0, cudaStream_t s) {
+  GemmArgs g = g0;
+  static const int group_m = env_int("CRTG_GROUP_M", 0);
+  g.group_m = group_m;
   if (pair_enabled() && mode != EPI_BOUND && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
     return launch_gemm_pair(mode, g, sm_count(), s);
   return launch_gemm(mode, g, sm_count(), s);

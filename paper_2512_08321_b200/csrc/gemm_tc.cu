@@ -61,10 +61,11 @@ __device__ __forceinline__ void decode_tile(int t, const GemmArgs& g, int& l, in
   const int per = g.mt * g.nt;
   l = t / per;
   const int r = t - l * per;
-  const int grp = r / (kGroupM * g.nt);
-  const int first = grp * kGroupM;
-  const int gm = min(kGroupM, g.mt - first);
-  const int in = r - grp * kGroupM * g.nt;
+  const int G = g.group_m > 0 ? g.group_m : kGroupM;
+  const int grp = r / (G * g.nt);
+  const int first = grp * G;
+  const int gm = min(G, g.mt - first);
+  const int in = r - grp * G * g.nt;
   tm = first + in % gm + g.mt0;
   tn = in / gm;
 }

@@ -29,6 +29,7 @@ struct GemmArgs {
   int32_t* row_max;  // BOUND: [mt*128]
   int32_t* col_max;  // BOUND: [nt*256]
   unsigned long long* overflow;  // REAL: int32 accumulator overflow (kernel.py:33-34)
+  int group_m;       // raster: row tiles per column sweep (0 -> 16)
   ModConst mc[CRTG_MAX_MODULI];
 };
 
