@@ -11,14 +11,28 @@ from .emulate import (ScalingVectors, accurate_scaling, complex_gemm_mod, crt_re
                       emulate_gemm_complex, emulate_gemm_real, fast_scaling, gemm, gemm_i8_i32,
                       quantized_residues, run_complex)
 from .errors import ConfigError, DimensionError, DomainError
+from .gen import GenSpec, gen_matrix
+from .matfile import read_matrix, write_matrix
 from .moduli import ModulusSet, ScalingConstants, select_moduli
+from .perfmodel import PerfParams, heatmap_csv, heatmap_grid, predict_time, predicted_tflops
+
+
+def __getattr__(name):
+    # the accuracy harness imports torch-side helpers lazily
+    if name in ("DDMatrix", "reference_gemm_dd", "max_relative_error", "run_accuracy_sweep",
+                "sweep_csv"):
+        from . import accuracy
+        return getattr(accuracy, name)
+    raise AttributeError(name)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ConfigError", "DEFAULT_N_BLOCK", "DimensionError", "DomainError", "EmuConfig",
-    "MAX_K_COMPLEX", "MAX_K_REAL", "ModulusSet", "STRATEGIES", "ScalingConstants",
-    "ScalingVectors", "accurate_scaling", "complex_gemm_mod", "crt_reconstruct",
-    "emulate_gemm_complex", "emulate_gemm_real", "fast_scaling", "gemm", "gemm_i8_i32", "quantized_residues",
-    "run_complex", "select_moduli",
+    "ConfigError", "DDMatrix", "DEFAULT_N_BLOCK", "DimensionError", "DomainError", "EmuConfig",
+    "GenSpec", "MAX_K_COMPLEX", "MAX_K_REAL", "ModulusSet", "PerfParams", "STRATEGIES",
+    "ScalingConstants", "ScalingVectors", "accurate_scaling", "complex_gemm_mod",
+    "crt_reconstruct", "emulate_gemm_complex", "emulate_gemm_real", "fast_scaling", "gemm",
+    "gemm_i8_i32", "gen_matrix", "heatmap_csv", "heatmap_grid", "max_relative_error",
+    "predict_time", "predicted_tflops", "quantized_residues", "read_matrix", "reference_gemm_dd",
+    "run_accuracy_sweep", "run_complex", "select_moduli", "sweep_csv", "write_matrix",
 ]

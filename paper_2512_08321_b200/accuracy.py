@@ -55,12 +55,29 @@ def reference_gemm_dd(a, b) -> DDMatrix:
     return DDMatrix(hi, lo)
 
 
-def max_relative_error(approx, reference: DDMatrix, return_zero_count: bool = False):
-    dev = reference.hi.device
-    cplx = reference.hi.is_complex()
+def _as_dd(reference, cplx_hint: bool, dev) -> DDMatrix:
+    if isinstance(reference, DDMatrix):
+        return reference
+    # a plain array is a reference with lo = 0 (oracle.py:144-146)
+    t = reference if isinstance(reference, torch.Tensor) else \
+        torch.from_numpy(np.ascontiguousarray(reference))
+    cplx = t.is_complex() or cplx_hint
+    hi = t.to(torch.complex128 if cplx else torch.float64).to(dev).contiguous()
+    return DDMatrix(hi, torch.zeros_like(hi))
+
+
+def max_relative_error(approx, reference, return_zero_count: bool = False):
+    """Largest componentwise relative error (oracle.py:131-169): |(x - hi) - lo| /
+    |hi + lo| over the real and imaginary parts separately, zero references
+    excluded (and counted when `return_zero_count`)."""
     x = approx if isinstance(approx, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(approx))
+    dev = reference.hi.device if isinstance(reference, DDMatrix) else _device()
+    reference = _as_dd(reference, x.is_complex(), dev)
     if tuple(x.shape) != tuple(reference.hi.shape):
         raise DimensionError("shape mismatch between approximation and reference")
+    cplx = reference.hi.is_complex() or x.is_complex()
+    if cplx and not reference.hi.is_complex():
+        reference = DDMatrix(reference.hi.to(torch.complex128), reference.lo.to(torch.complex128))
     single = x.dtype in (torch.complex64, torch.float32)
     want = (torch.complex64 if single else torch.complex128) if cplx else \
         (torch.float32 if single else torch.float64)
@@ -72,3 +89,43 @@ def max_relative_error(approx, reference: DDMatrix, return_zero_count: bool = Fa
     bits, zeros = out.cpu().tolist()
     worst = float(np.array([bits], np.int64).view(np.float64)[0])
     return (worst, int(zeros)) if return_zero_count else worst
+
+
+def run_accuracy_sweep(dims, moduli_counts, phis, mode="accurate", precision="double",
+                       domain="complex", seeds=(0,)) -> list:
+    """(N, phi, seed, max_rel_error) rows ordered by (N, phi, seed) (bench.py:73-104).
+
+    Inputs are the reference's generator (`gen_matrix`, seed and seed+1), the
+    double-double reference of each (phi, seed) is computed once on the device
+    and shared across moduli counts, and the emulation runs through the public
+    `emulate_gemm_complex` / `emulate_gemm_real`.
+    """
+    from .config import EmuConfig
+    from .emulate import emulate_gemm_complex, emulate_gemm_real
+    from .gen import GenSpec, gen_matrix
+
+    m, n, k = dims
+    refs, inputs = {}, {}
+    for phi in phis:
+        for seed in seeds:
+            a = gen_matrix(GenSpec(m, k, phi, seed, precision, domain))
+            b = gen_matrix(GenSpec(k, n, phi, seed + 1, precision, domain))
+            inputs[(phi, seed)] = (a, b)
+            refs[(phi, seed)] = reference_gemm_dd(a, b)
+    rows = []
+    for count in moduli_counts:
+        cfg = EmuConfig(precision=precision, domain=domain, mode=mode, num_moduli=count)
+        for phi in phis:
+            for seed in seeds:
+                a, b = inputs[(phi, seed)]
+                run = emulate_gemm_complex if domain == "complex" else emulate_gemm_real
+                err = max_relative_error(run(a, b, cfg), refs[(phi, seed)])
+                rows.append((count, float(phi), int(seed), err))
+    return rows
+
+
+def sweep_csv(rows) -> str:
+    """`N,phi,seed,max_rel_error` CSV (bench.py:107-113)."""
+    lines = ["N,phi,seed,max_rel_error"]
+    lines += [f"{count},{phi!r},{seed},{err!r}" for count, phi, seed, err in rows]
+    return "\n".join(lines) + "\n"

@@ -218,10 +218,14 @@ DevConsts make_dev(const crtg_consts& K) {
     rc.neg_p = uint32_t(-p);
     {
       uint64_t c = 1 % uint64_t(p);
+      uint32_t cw[6];
       for (int i = 0; i < 6; ++i) {
-        rc.cw[i] = uint32_t(c);
+        cw[i] = uint32_t(c);  // < p <= 256
         c = (c << 16) % uint64_t(p);
       }
+      rc.dn = cw[0] | (cw[1] << 8);
+      rc.dw0123 = cw[0] | (cw[1] << 8) | (cw[2] << 16) | (cw[3] << 24);
+      rc.dw45 = cw[4] | (cw[5] << 8);
       // 2^90 mod p
       uint64_t t = 1 % uint64_t(p);
       for (int i = 0; i < 90; ++i) t = (t * 2) % uint64_t(p);

@@ -57,9 +57,12 @@ struct ResConst {
   uint32_t c32, c16, k, h, magic, sum_k;  // sum_k = p - h (re + im plane)
   int32_t shift, p;
   uint32_t neg_p;                          // (uint32)(-p): t = u + q * neg_p
-  // wide values (|a'| >= 2^53): v = 2^90 + a' in six 16-bit limbs,
-  // u = sum_i limb_i * (2^(16 i) mod p) + kw  ==  a' + h  (mod p)
-  uint32_t cw[6], kw;
+  // dp2a byte tables (each 2^(16 i) mod p < 256 fits a byte):
+  //  narrow: dn = (1, 2^16 mod p) for the two halves of the low word of 2^53 + a'
+  //  wide (|a'| >= 2^53): v = 2^90 + a' as three words = six 16-bit limbs,
+  //  u = sum_i limb_i * (2^(16 i) mod p) + kw  ==  a' + h  (mod p);
+  //  dw0123 = bytes (c0, c16, c32, c48), dw45 = (c64, c80)
+  uint32_t dn, dw0123, dw45, kw;
 };
 
 struct DevConsts {

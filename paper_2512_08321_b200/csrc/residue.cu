@@ -112,11 +112,13 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
 // ---------------------------------------------------------------------------
 constexpr int kResRows = 16;
 
-// Value representations (3 registers each), read straight from the IEEE bits:
-//  narrow (|a'| < 2^53): v = 2^53 + a' as (v >> 32, (v >> 16) & 0xffff, v & 0xffff)
-//      u = hi*(2^32 mod p) + lh*(2^16 mod p) + ll + k           (< 2^31)
-//  wide (some |a'| >= 2^53 in the thread): v = 2^90 + a' (< 2^91) as six 16-bit
-//      limbs packed two per register, u = sum limb_i*(2^(16i) mod p) + kw (< 2^27)
+// Value representations, read straight from the IEEE bits:
+//  narrow (|a'| < 2^53): v = 2^53 + a' (< 2^54) as w0 = v >> 32 (22 bits),
+//      w1 = low word; u = dp2a(w1 halves, (1, 2^16 mod p)) + k + w0*(2^32 mod p)
+//      (< 2^31): 2 instructions
+//  wide (some |a'| >= 2^53 in the thread): v = 2^90 + a' (< 2^91) as three words
+//      = six 16-bit limbs; u = sum limb_i*(2^(16i) mod p) + kw (< 2^27) as three
+//      dp2a (16-bit x 8-bit pair dot products): 3 instructions
 // Both give u == a' + floor(p/2) (mod p); one magic reduction -> t in [0,p).
 struct Val3 {
   uint32_t w0, w1, w2;
@@ -142,7 +144,7 @@ __device__ __forceinline__ Val3 split_narrow(double q) {
   int s;
   int_parts(q, M, s);
   const uint64_t v = (q < 0.0) ? (uint64_t(1) << 53) - M : (uint64_t(1) << 53) + M;
-  return {uint32_t(v >> 32), uint32_t(v) >> 16, uint32_t(v) & 0xFFFFu};
+  return {uint32_t(v >> 32), uint32_t(v), 0u};
 }
 
 __device__ __forceinline__ Val3 split_wide(double q) {
@@ -163,6 +165,19 @@ __device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
   return d;
 }
 
+// c + a.h0 * b.byte0 + a.h1 * b.byte1   (lo)   /  ... b.byte2, b.byte3   (hi)
+__device__ __forceinline__ uint32_t dp2a_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("dp2a.lo.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t dp2a_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("dp2a.hi.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t mod_small(uint32_t u, const ResConst& c) {
   if (c.shift < 0) return u & 0xFFu;
   const uint32_t q = __umulhi(u, c.magic) >> c.shift;
@@ -173,15 +188,11 @@ template <bool WIDE>
 __device__ __forceinline__ uint32_t res_t(const Val3& v, const ResConst& c) {
   uint32_t u;
   if (WIDE) {
-    u = (v.w0 & 0xFFFFu) + c.kw;
-    u = mad_lo(v.w0 >> 16, c.cw[1], u);
-    u = mad_lo(v.w1 & 0xFFFFu, c.cw[2], u);
-    u = mad_lo(v.w1 >> 16, c.cw[3], u);
-    u = mad_lo(v.w2 & 0xFFFFu, c.cw[4], u);
-    u = mad_lo(v.w2 >> 16, c.cw[5], u);
+    u = dp2a_lo(v.w0, c.dw0123, c.kw);
+    u = dp2a_hi(v.w1, c.dw0123, u);
+    u = dp2a_lo(v.w2, c.dw45, u);
   } else {
-    // ll + k, then + lh*(2^16 mod p), then + hi*(2^32 mod p)
-    u = mad_lo(v.w0, c.c32, mad_lo(v.w1, c.c16, v.w2 + c.k));
+    u = mad_lo(v.w0, c.c32, dp2a_lo(v.w1, c.dn, c.k));
   }
   return mod_small(u, c);  // t = (a' + h) mod p
 }
@@ -264,6 +275,9 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
     if (!(fabs(qi[t]) < 0x1p90)) { bad = 1; qi[t] = 0.0; }
     wide |= fabs(qr[t]) >= 0x1p53 || fabs(qi[t]) >= 0x1p53;
   }
+  // warp-uniform representation (the wide form is valid for every value): a
+  // warp that mixed both would execute both per-modulus paths
+  wide = __any_sync(0xffffffffu, wide);
   Val3 vr[8], vi[8];
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
