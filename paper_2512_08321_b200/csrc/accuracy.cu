@@ -171,7 +171,7 @@ int launch_dd_gemm(bool cplx, int64_t m, int64_t n, int64_t k, const double* A, 
     k_dd_gemm<true><<<grid, kT * kT, 0, s>>>(A, lda, B, ldb, int(m), int(n), int(k), hi, lo, ldo);
   else
     k_dd_gemm<false><<<grid, kT * kT, 0, s>>>(A, lda, B, ldb, int(m), int(n), int(k), hi, lo, ldo);
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 int launch_max_rel_err(bool cplx, int64_t m, int64_t n, const void* approx, bool approx_single,
@@ -181,7 +181,7 @@ int launch_max_rel_err(bool cplx, int64_t m, int64_t n, const void* approx, bool
   if (total <= 0) return 0;
   k_max_rel_err<<<unsigned((total + 255) / 256), 256, 0, s>>>(
       m, n, cplx ? 2 : 1, approx, approx_single ? 1 : 0, lda_x, hi, lo, ldo, max_bits, zeros);
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 }  // namespace crtg

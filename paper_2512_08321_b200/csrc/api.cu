@@ -49,6 +49,11 @@ int cuda_check(int err, const char* where) {
 
 // ---- instrumentation: launch counter and per-stage CUDA-event timers ----
 std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void crtg::note_launches(int n) { g_launches += uint64_t(n); }
+
+namespace {
 std::mutex g_prof_mu;
 bool g_prof_on = false;
 struct ProfRec {
@@ -61,8 +66,7 @@ struct StageTimer {
   int stage;
   cudaStream_t s;
   cudaEvent_t a = nullptr, b = nullptr;
-  int kernels;
-  StageTimer(int st, cudaStream_t str, int nkernels) : stage(st), s(str), kernels(nkernels) {
+  StageTimer(int st, cudaStream_t str) : stage(st), s(str) {
     if (g_prof_on) {
       cudaEventCreate(&a);
       cudaEventCreate(&b);
@@ -70,7 +74,6 @@ struct StageTimer {
     }
   }
   ~StageTimer() {
-    g_launches += uint64_t(kernels);
     if (a) {
       cudaEventRecord(b, s);
       std::lock_guard<std::mutex> lk(g_prof_mu);
@@ -423,7 +426,7 @@ int accurate_partial(const Plan& P, int precision, const void* A, int64_t lda, c
   CRTG_TRY(cudaMemsetAsync(colabs, 0, P.colabs.bytes, s), "memset");
   CRTG_TRY(cudaMemsetAsync(rowmax, 0, P.rowmax.bytes, s), "memset");
   CRTG_TRY(cudaMemsetAsync(colmax, 0, P.colmax.bytes, s), "memset");
-  StageTimer timer(CRTG_STAGE_SCALING, s, 7);
+  StageTimer timer(CRTG_STAGE_SCALING, s);
   PwTree tree{};
   CRTG_TRY(launch_row_stats(single ? E_C64 : E_C128, false, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, nullptr,
                             rowabs, diag, s),
@@ -491,14 +494,12 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
     tree.nodes = reinterpret_cast<const int2*>(tb + lb);
     tree.level_start = reinterpret_cast<const int*>(tb + lb + nb);
     {
-      StageTimer timer(CRTG_STAGE_SCALING, s, 1);
+      StageTimer timer(CRTG_STAGE_SCALING, s);
       CRTG_TRY(launch_row_stats(single ? E_C64 : E_C128, true, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu,
                                 rowabs, diag, s),
                "row stats");
     }
-    StageTimer timer(CRTG_STAGE_SCALING, side, 3);
-    CRTG_TRY(cudaMemsetAsync(colabs, 0, P.colabs.bytes, side), "memset");
-    CRTG_TRY(launch_col_absmax(single ? E_C64 : E_C128, B, ldb, P.k, P.n, colabs, diag, side), "col absmax");
+    StageTimer timer(CRTG_STAGE_SCALING, side);
     CRTG_TRY(launch_col_fast(single ? E_C64 : E_C128, B, ldb, P.k, P.n, colabs, at<double>(ws, P.colsq), dc.p_fast,
                              dc.delta, nu, diag, side),
              "col sumsq");
@@ -506,7 +507,7 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
   }
   // accurate mode (scaling.py:229-274)
   if (int e = accurate_partial(P, precision, A, lda, B, ldb, dc, ws, diag, s)) return e;
-  StageTimer timer(CRTG_STAGE_SCALING, s, 2);
+  StageTimer timer(CRTG_STAGE_SCALING, s);
   CRTG_TRY(launch_accurate_exps(at<int32_t>(ws, P.rowmax), rowabs, at<int32_t>(ws, P.bar_mu), P.m,
                                 dc.p_accu, dc.delta, mu, diag + CRTG_DIAG_CLAMPED_MU, s),
            "accurate mu");
@@ -537,7 +538,7 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
   const int64_t a_plane = P.m_pad * P.k_pad;
   int8_t* apack = at<int8_t>(ws, P.a_pack);
   {
-    StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
+    StageTimer timer(CRTG_STAGE_RESIDUE_A, s);
     CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 0, PACK_RESIDUE, A, lda, m, k, 0, mu, dc, apack, a_plane,
                          P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s),
              "residues A");
@@ -552,7 +553,7 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
   auto eim = [&](int64_t j) { return at<int8_t>(ws, P.e_im) + (j % nbuf) * ebuf; };
   auto residues_b = [&](int64_t j, int max_ctas) -> int {
     const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
-    StageTimer timer(CRTG_STAGE_RESIDUE_B, side, 1);
+    StageTimer timer(CRTG_STAGE_RESIDUE_B, side);
     CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack(j),
                          w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, side, max_ctas),
              "residues B");
@@ -586,14 +587,14 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
     g.e_plane = m * P.nb_pad;
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
     {
-      StageTimer timer(CRTG_STAGE_GEMM, s, 1);
+      StageTimer timer(CRTG_STAGE_GEMM, s);
       CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
     }
     ev_g[j] = E.get();
     CRTG_TRY(cudaEventRecord(ev_g[j], s), "record");
     CRTG_TRY(cudaStreamWaitEvent(side, ev_g[j], 0), "wait");
     {
-      StageTimer timer(CRTG_STAGE_CRT, side, 1);
+      StageTimer timer(CRTG_STAGE_CRT, side);
       CRTG_TRY(launch_crt(single, false, m, w, ere(j), eim(j), g.e_plane, g.e_ld, mu, nu + j0, dc,
                           static_cast<char*>(C) + j0 * csz, ldc, side,
                           j + 1 < nblk ? nsm : 0),
@@ -737,7 +738,6 @@ int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim, const 
   CRTG_TRY(launch_pack((precision & CRTG_IN_C64) ? E_C64 : E_C128, operand, PACK_RESIDUE, X, ldx, rows, kdim, 0,
                        exps, dc, packed, plane, r_pad / 128, ovf, s),
            "residues");
-  g_launches += uint64_t(1 + 3 * N);
   for (int q = 0; q < 3 * N; ++q)
     CRTG_TRY(launch_unpack_i8(packed + q * plane, rows, kdim, r_pad / 128, out + q * rows * kdim, s),
              "unpack");
@@ -766,7 +766,6 @@ int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A, const int
   int8_t* ap = static_cast<int8_t*>(ws);
   int8_t* bp = ap + round_up(m_pad * k_pad, 256);
   int32_t* raw = reinterpret_cast<int32_t*>(bp + round_up(n_pad * k_pad, 256));
-  g_launches += 3;
   CRTG_TRY(launch_pack_i8(A, 0, m, k, ap, m_pad / 128, s), "pack A");
   CRTG_TRY(launch_pack_i8(B, 1, n, k, bp, n_pad / 128, s), "pack B");
   GemmArgs g{};
@@ -822,11 +821,10 @@ extern "C" int crtg_complex_gemm_mod(int64_t m, int64_t n, int64_t k, const int8
   int8_t* eo = bp + round_up(3 * b_plane, 256);  // [2][m][n_pad]
   int8_t* sums = eo + round_up(m * n_pad * 4, 256);
   const ModConst mc = make_mod(p);
-  g_launches += 9;
   // Karatsuba operand sums sa = sym(ar + ai), sb = sym(br + bi)  (kernel.py:101-103)
   k_mod_sum<<<unsigned((m * k + 255) / 256), 256, 0, s>>>(ar, ai, m * k, mc, sums);
   k_mod_sum<<<unsigned((k * n + 255) / 256), 256, 0, s>>>(br, bi, k * n, mc, sums + m * k);
-  CRTG_TRY(int(cudaGetLastError()), "mod sum");
+  CRTG_TRY(launched(2), "mod sum");
   CRTG_TRY(launch_pack_i8(ar, 0, m, k, ap, m_pad / 128, s), "pack");
   CRTG_TRY(launch_pack_i8(ai, 0, m, k, ap + a_plane, m_pad / 128, s), "pack");
   CRTG_TRY(launch_pack_i8(sums, 0, m, k, ap + 2 * a_plane, m_pad / 128, s), "pack");
@@ -866,7 +864,6 @@ extern "C" int crtg_crt_reconstruct(int precision, int64_t m, int64_t n, const i
   if (int e = check_consts(K, &N)) return e;
   if (m < 1 || n < 1 || ldc < n) return fail(CRTG_ERR_DIMENSION, "bad shape");
   const DevConsts dc = make_dev(*K);
-  g_launches += 1;
   CRTG_TRY(launch_crt((precision & CRTG_SINGLE) != 0, false, m, n, e_re, e_im, m * n, n, mu, nu, dc, C, ldc,
                       static_cast<cudaStream_t>(stream)),
            "crt");
@@ -973,7 +970,6 @@ extern "C" int crtg_accurate_exponents(int64_t count, const int32_t* maxb, const
   int N = 0;
   if (int e = check_consts(K, &N)) return e;
   if (count < 1) return fail(CRTG_ERR_DIMENSION, "empty exponent vector");
-  g_launches += 1;
   CRTG_TRY(launch_accurate_exps(maxb, absval, bar, count, K->p_accu, K->delta, out,
                                 reinterpret_cast<unsigned long long*>(clamp_counter),
                                 static_cast<cudaStream_t>(stream)),
@@ -1130,12 +1126,12 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
         CRTG_TRY(cudaStreamWaitEvent(s, evA[i], 0), "wait");
         const char* Ai = dA + size_t(i0) * k * esz;
         if (mode == CRTG_FAST) {
-          StageTimer timer(CRTG_STAGE_SCALING, s, 1);
+          StageTimer timer(CRTG_STAGE_SCALING, s);
           CRTG_TRY(launch_row_stats(in32 ? E_C64 : E_C128, true, Ai, k, h, k, tree, dc.p_fast, dc.delta, mu + i0,
                                     at<double>(ws, P.rowabs) + i0, dg, s),
                    "row stats");
         }
-        StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
+        StageTimer timer(CRTG_STAGE_RESIDUE_A, s);
         CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 0, PACK_RESIDUE, Ai, k, h, k, 0, mu + i0, dc, apack, a_plane,
                              P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s, 0, i0,
                              last_rows ? P.m_pad - i0 : h),
@@ -1144,15 +1140,14 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
       if (i == 0) {  // B block j: statistics (fast) and residues, once
         CRTG_TRY(cudaStreamWaitEvent(s, evB[j], 0), "wait");
         if (mode == CRTG_FAST) {
-          StageTimer timer(CRTG_STAGE_SCALING, s, 3);
+          StageTimer timer(CRTG_STAGE_SCALING, s);
           const char* Bj = dB + j0 * esz;
           double* cabs = at<double>(ws, P.colabs) + j0;
-          CRTG_TRY(launch_col_absmax(in32 ? E_C64 : E_C128, Bj, n, k, w, cabs, dg, s), "col absmax");
           CRTG_TRY(launch_col_fast(in32 ? E_C64 : E_C128, Bj, n, k, w, cabs, at<double>(ws, P.colsq) + 2 * j0,
                                    dc.p_fast, dc.delta, nu + j0, dg, s),
                    "col sumsq");
         }
-        StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
+        StageTimer timer(CRTG_STAGE_RESIDUE_B, s);
         CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 1, PACK_RESIDUE, dB, n, w, k, j0, nu + j0, dc, bpack,
                              w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
                  "residues B");
@@ -1179,13 +1174,13 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
       g.e_plane = m * P.nb_pad;
       for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
       {
-        StageTimer timer(CRTG_STAGE_GEMM, s, 1);
+        StageTimer timer(CRTG_STAGE_GEMM, s);
         CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
       }
       if (tile >= 2) CRTG_TRY(cudaStreamWaitEvent(s, evD[tile - 2], 0), "wait");
       char* cblk = dC + (tile & 1) * cbuf;
       {
-        StageTimer timer(CRTG_STAGE_CRT, s, 1);
+        StageTimer timer(CRTG_STAGE_CRT, s);
         CRTG_TRY(launch_crt(single, false, h, w, g.e_re + i0 * g.e_ld, g.e_im + i0 * g.e_ld, g.e_plane,
                             g.e_ld, mu + i0, nu + j0, dc, cblk, w, s),
                  "crt");
@@ -1278,7 +1273,7 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
   // diag offsets: the row kernels report into (NONFINITE_A, CLAMPED_MU), the column
   // kernels into (NONFINITE_B, CLAMPED_NU); +-1 re-targets them to the other operand.
   {
-    StageTimer timer(CRTG_STAGE_SCALING, s, mode == CRTG_FAST ? 6 : 11);
+    StageTimer timer(CRTG_STAGE_SCALING, s);
     PwTree tree{};
     if (mode == CRTG_FAST) {
       if (int e = load_tree(P, ws, s, tree)) return e;
@@ -1286,12 +1281,10 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
         CRTG_TRY(launch_row_stats(elem, true, A, lda, m, k, tree, dc.p_fast, dc.delta, mu, rowabs,
                                   dg, s), "row stats");
       } else {
-        CRTG_TRY(launch_col_absmax(elem, A, lda, k, m, rowabs, dg - 1, s), "col absmax");
         CRTG_TRY(launch_col_fast(elem, A, lda, k, m, rowabs, at<double>(ws, P.rowsq), dc.p_fast,
                                  dc.delta, mu, dg - 1, s), "col sumsq");
       }
       if (!b_colmajor) {
-        CRTG_TRY(launch_col_absmax(elem, B, ldb, k, n, colabs, dg, s), "col absmax");
         CRTG_TRY(launch_col_fast(elem, B, ldb, k, n, colabs, at<double>(ws, P.colsq), dc.p_fast,
                                  dc.delta, nu, dg, s), "col sumsq");
       } else {
@@ -1355,7 +1348,7 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
   const int64_t a_plane = P.m_pad * P.k_pad;
   int8_t* apack = at<int8_t>(ws, P.a_pack);
   {
-    StageTimer timer(CRTG_STAGE_RESIDUE_A, s, 1);
+    StageTimer timer(CRTG_STAGE_RESIDUE_A, s);
     CRTG_TRY(launch_pack(elem, a_colmajor ? 1 : 0, PACK_RESIDUE, A, lda, m, k, 0, mu, dc, apack,
                          a_plane, P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s), "residues A");
   }
@@ -1365,7 +1358,7 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
   for (int64_t j0 = 0; j0 < n; j0 += P.nb) {
     const int64_t w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
     {
-      StageTimer timer(CRTG_STAGE_RESIDUE_B, s, 1);
+      StageTimer timer(CRTG_STAGE_RESIDUE_B, s);
       if (!b_colmajor)
         CRTG_TRY(launch_pack(elem, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack,
                              w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
@@ -1397,11 +1390,11 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
     g.overflow = dg + CRTG_DIAG_INT32_OVERFLOW;
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
     {
-      StageTimer timer(CRTG_STAGE_GEMM, s, 1);
+      StageTimer timer(CRTG_STAGE_GEMM, s);
       CRTG_TRY(launch_gemm(EPI_REAL, g, sm_count(), s), "real gemm");
     }
     {
-      StageTimer timer(CRTG_STAGE_CRT, s, 1);
+      StageTimer timer(CRTG_STAGE_CRT, s);
       CRTG_TRY(launch_crt(single, true, m, w, ere, nullptr, g.e_plane, g.e_ld, mu, nu + j0, dc,
                           static_cast<char*>(C) + j0 * csz, ldc, s),
                "crt");
@@ -1421,7 +1414,6 @@ extern "C" int crtg_dd_gemm(int is_complex, int64_t m, int64_t n, int64_t k, con
                             int64_t ldo, void* stream) {
   if (m < 1 || n < 1 || k < 1) return fail(CRTG_ERR_DIMENSION, "m, n, k must be positive");
   if (lda < k || ldb < n || ldo < n) return fail(CRTG_ERR_DIMENSION, "leading dimension too small");
-  g_launches += 1;
   CRTG_TRY(launch_dd_gemm(is_complex != 0, m, n, k, static_cast<const double*>(A), lda,
                           static_cast<const double*>(B), ldb, static_cast<double*>(hi),
                           static_cast<double*>(lo), ldo, static_cast<cudaStream_t>(stream)),
@@ -1434,7 +1426,6 @@ extern "C" int crtg_max_relative_error(int is_complex, int64_t m, int64_t n, con
                                        const void* lo, int64_t ldo, uint64_t* max_bits,
                                        uint64_t* zero_count, void* stream) {
   if (m < 1 || n < 1) return fail(CRTG_ERR_DIMENSION, "empty matrix");
-  g_launches += 1;
   CRTG_TRY(launch_max_rel_err(is_complex != 0, m, n, approx, approx_single != 0, ld_approx,
                               static_cast<const double*>(hi), static_cast<const double*>(lo), ldo,
                               reinterpret_cast<unsigned long long*>(max_bits),

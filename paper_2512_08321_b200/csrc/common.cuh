@@ -18,6 +18,14 @@
 
 namespace crtg {
 
+// kernel-launch accounting for crtg_launch_count (defined in api.cu); every
+// launcher reports the kernels it enqueued
+void note_launches(int n);
+inline int launched(int n) {
+  note_launches(n);
+  return int(cudaGetLastError());
+}
+
 constexpr int kBlockRows = 128;
 constexpr int kBlockK = 128;                    // bytes
 constexpr int kBlockBytes = kBlockRows * kBlockK;  // 16 KiB

@@ -218,7 +218,7 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
     else { if (limbs) CRTG_CRT(false, true, false); else CRTG_CRT(false, false, false); }
   }
 #undef CRTG_CRT
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 }  // namespace crtg

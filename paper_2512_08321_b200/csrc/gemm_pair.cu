@@ -243,7 +243,7 @@ int launch_gemm_pair(int mode, const GemmArgs& g, int num_sms, cudaStream_t stre
     if (err != cudaSuccess) return int(err);
     k_gemm_i8_pair<EPI_KARATSUBA><<<grid, 256, smem, stream>>>(g, map_a, map_b);
   }
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 }  // namespace crtg

@@ -272,7 +272,7 @@ int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {
       k_gemm_i8<EPI_BOUND><<<grid, 256, smem, stream>>>(g);
       break;
   }
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 }  // namespace crtg

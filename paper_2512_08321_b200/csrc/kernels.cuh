@@ -30,8 +30,9 @@ int launch_row_stats(int elem, bool fast, const void* A, int64_t lda, int64_t m,
 int launch_col_absmax(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
                       double* colabs, unsigned long long* diag, cudaStream_t s);
 // B columns: sequential sums of squares (numpy axis-0 order) and the exponent.
+// fast-mode column stats: absmax -> colabs, exponents -> nu (one pass)
 int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
-                    const double* colabs, double* colsq, float p_fast, float delta, int32_t* nu,
+                    double* colabs, double* colsq, float p_fast, float delta, int32_t* nu,
                     unsigned long long* diag, cudaStream_t s);
 // accurate mode: bar = 5 - floor_log2(absmax) (0 for zero rows/cols)
 int launch_bar(const double* absval, int64_t count, int32_t* bar, cudaStream_t s);

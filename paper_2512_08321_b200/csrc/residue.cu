@@ -430,7 +430,7 @@ int launch_pack(int elem, int operand, int kind, const void* X, int64_t ldx, int
 #undef CRTG_PACK_OP
 #undef CRTG_PACK_KIND
 #undef CRTG_PACK
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 int launch_pack_i8(const int8_t* X, int trans, int64_t rows, int64_t kdim, int8_t* out,
@@ -441,7 +441,7 @@ int launch_pack_i8(const int8_t* X, int trans, int64_t rows, int64_t kdim, int8_
   if (total <= 0) return 0;
   k_pack_i8<<<unsigned((total + 255) / 256), 256, 0, s>>>(X, trans, rows, kdim, kpad, out, rb_count,
                                                           total);
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 int launch_unpack_i8(const int8_t* packed, int64_t rows, int64_t kdim, int64_t rb_count,
@@ -449,7 +449,7 @@ int launch_unpack_i8(const int8_t* packed, int64_t rows, int64_t kdim, int64_t r
   const int64_t total = rows * kdim;
   if (total <= 0) return 0;
   k_unpack_i8<<<unsigned((total + 255) / 256), 256, 0, s>>>(packed, rows, kdim, rb_count, out);
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 }  // namespace crtg

@@ -111,39 +111,58 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return r;
 }
 
-// One CTA per row of A.  Pass 1: absmax over both parts; pass 2 (fast mode): the
-// pairwise sums of squares of re and im (numpy order), then the exponent.
+__device__ __forceinline__ double block_min(double v, double* red) {
+  for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double r = INFINITY;
+  for (int i = 0; i < int(blockDim.x >> 5); ++i) r = fmin(r, red[i]);
+  __syncthreads();
+  return r;
+}
+
+// Single-pass sums of squares.  The reference squares x * 2^-fl (fl = floor
+// log2 absmax), which needs absmax first — a second read of the operand.  But a
+// power-of-two scale commutes with every rounding while all values stay
+// normal, so sum((x 2^-fl)^2) == 2^-2fl * sum(x^2) bit for bit when
+//   every nonzero x^2 and (x 2^-fl)^2 is >= 2^-1022   (min |x| != 0 >= 2^-511,
+//                                                     and >= 2^(fl-511))
+//   no partial sum overflows                          (absmax <= 2^500, k <= 2^18)
+// (nonzero partial sums are >= the smallest nonzero square).  Kernels sum the
+// unscaled squares in the reference's order and scale once; when the check
+// fails they fall back to the two-pass form.
+__device__ __forceinline__ bool unscaled_ok(double absmax, double minnz) {
+  if (absmax == 0.0) return true;
+  if (!(absmax <= 0x1p500)) return false;  // also rejects inf / nan
+  if (minnz == INFINITY) return true;       // no nonzero values besides absmax's
+  return minnz >= 0x1p-511 && ilogb(minnz) - ilogb(absmax) >= -511;
+}
+
+// 2^-2fl * s as two exact multiplies (2^-2fl itself may not be representable)
+__device__ __forceinline__ double unscale_sq(double s, const Pow2& sc) {
+  return apply(sc, apply(sc, s));
+}
+
+// One CTA per row of A.  Fast mode: ONE pass over the row computes absmax, the
+// smallest nonzero |x|, finiteness and the numpy-pairwise leaf sums of the
+// UNSCALED squares of re and im; the tree combine and a 2^-2fl scale then give
+// the reference's sums (see unscaled_ok), else a second, scaled pass runs.
+// Accurate mode: absmax only.
 template <typename T, bool REAL>
-__global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int64_t lda, int k,
-                                                   PwTree tree, float p_fast, float delta,
-                                                   int fast, int32_t* __restrict__ mu,
-                                                   double* __restrict__ rowabs,
-                                                   unsigned long long* __restrict__ diag) {
-  extern __shared__ double vals[];  // [2][nleaves + nnodes]
-  __shared__ double red[8];
-  const int64_t i = blockIdx.x;
-  const T* row = A + (REAL ? 1 : 2) * i * lda;
-
-  double mx = 0.0;
-  int bad = 0;
-  for (int h = threadIdx.x; h < k; h += blockDim.x) {
-    double re, im;
-    load_c<T, REAL>(row, h, re, im);
-    bad |= !(isfinite(re) && isfinite(im));
-    mx = fmax(mx, fmax(fabs(re), fabs(im)));
-  }
-  bad = __syncthreads_or(bad);
-  const double absmax = block_max(mx, red);
-  if (threadIdx.x == 0) {
-    rowabs[i] = absmax;
-    if (bad) atomicAdd(diag + CRTG_DIAG_NONFINITE_A, 1ull);
-  }
-  if (!fast) return;
-  const bool zero = absmax == 0.0;
-  const Pow2 sc = make_pow2(zero ? 0 : -ilogb(absmax));
-
-  const int nv = tree.nleaves + tree.nnodes;
+__device__ void row_leaf_sums(const T* row, const PwTree& tree, double* vals, int nv,
+                              const Pow2* sc, double& mx, double& mn, int& bad) {
   const int grp = threadIdx.x >> 3, j = threadIdx.x & 7;
+  auto term = [&](double x) -> double {
+    if (sc == nullptr) {
+      const double ax = fabs(x);
+      bad |= !isfinite(x);
+      mx = fmax(mx, ax);
+      if (ax != 0.0) mn = fmin(mn, ax);
+      return __dmul_rn(x, x);
+    }
+    return sq(*sc, x);
+  };
   for (int base = 0; base < tree.nleaves; base += int(blockDim.x >> 3)) {
     const int lf = base + grp;
     const bool active = lf < tree.nleaves;
@@ -154,12 +173,12 @@ __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int6
       const int full = len - (len & 7);
       double re, im;
       load_c<T, REAL>(row, start + j, re, im);
-      sr = sq(sc, re);
-      si = sq(sc, im);
+      sr = term(re);
+      si = term(im);
       for (int t = 8 + j; t < full; t += 8) {
         load_c<T, REAL>(row, start + t, re, im);
-        sr = __dadd_rn(sr, sq(sc, re));
-        si = __dadd_rn(si, sq(sc, im));
+        sr = __dadd_rn(sr, term(re));
+        si = __dadd_rn(si, term(im));
       }
     }
     // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) inside each 8-lane group
@@ -173,8 +192,8 @@ __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int6
       for (int t = (len >= 8 ? len - (len & 7) : 0); t < len; ++t) {
         double re, im;
         load_c<T, REAL>(row, start + t, re, im);
-        sr = __dadd_rn(sr, sq(sc, re));
-        si = __dadd_rn(si, sq(sc, im));
+        sr = __dadd_rn(sr, term(re));
+        si = __dadd_rn(si, term(im));
       }
       vals[lf] = sr;
       vals[nv + lf] = si;
@@ -190,9 +209,55 @@ __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int6
     }
     __syncthreads();
   }
+}
+
+template <typename T, bool REAL>
+__global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int64_t lda, int k,
+                                                   PwTree tree, float p_fast, float delta,
+                                                   int fast, int32_t* __restrict__ mu,
+                                                   double* __restrict__ rowabs,
+                                                   unsigned long long* __restrict__ diag) {
+  extern __shared__ double vals[];  // [2][nleaves + nnodes]
+  __shared__ double red[8];
+  const int64_t i = blockIdx.x;
+  const T* row = A + (REAL ? 1 : 2) * i * lda;
+
+  double mx = 0.0, mn = INFINITY;
+  int bad = 0;
+  const int nv = tree.nleaves + tree.nnodes;
+  if (!fast) {
+    for (int h = threadIdx.x; h < k; h += blockDim.x) {
+      double re, im;
+      load_c<T, REAL>(row, h, re, im);
+      bad |= !(isfinite(re) && isfinite(im));
+      mx = fmax(mx, fmax(fabs(re), fabs(im)));
+    }
+  } else {
+    row_leaf_sums<T, REAL>(row, tree, vals, nv, nullptr, mx, mn, bad);
+  }
+  bad = __syncthreads_or(bad);
+  const double absmax = block_max(mx, red);
   if (threadIdx.x == 0) {
-    const int root = nv - 1;
-    double sumsq = __dadd_rn(__dadd_rn(0.0, vals[root]), vals[nv + root]);
+    rowabs[i] = absmax;
+    if (bad) atomicAdd(diag + CRTG_DIAG_NONFINITE_A, 1ull);
+  }
+  if (!fast) return;
+  const double minnz = block_min(mn, red);
+  const bool zero = absmax == 0.0;
+  const Pow2 sc = make_pow2(zero ? 0 : -ilogb(absmax));
+  const int root = nv - 1;
+  double sr, si;
+  if (unscaled_ok(absmax, minnz)) {
+    sr = unscale_sq(vals[root], sc);
+    si = unscale_sq(vals[nv + root], sc);
+  } else {
+    __syncthreads();  // everyone has read the unscaled root
+    row_leaf_sums<T, REAL>(row, tree, vals, nv, &sc, mx, mn, bad);
+    sr = vals[root];
+    si = vals[nv + root];
+  }
+  if (threadIdx.x == 0) {
+    double sumsq = __dadd_rn(__dadd_rn(0.0, sr), si);
     if (zero) sumsq = 1.0;
     mu[i] = fast_exponent(absmax, sumsq, p_fast, delta, diag + CRTG_DIAG_CLAMPED_MU);
   }
@@ -257,6 +322,130 @@ __global__ void __launch_bounds__(128) k_col_sumsq(const T* __restrict__ B, int6
   colsq[int64_t(part) * n + j] = s;
 }
 
+// ---------------------------------------------------------------------------
+// Fast-mode column statistics in ONE pass (k_col_stats): per column j of B (and
+// per part) the sequential numpy axis-0 chain of UNSCALED squares, the absmax,
+// the smallest nonzero |x| and finiteness; then the exponent in-kernel when
+// unscaled_ok, else nu[j] = kNuPending and k_col_fallback re-runs that column's
+// chains scaled.  Memory-level parallelism comes from a cp.async ring: a CTA
+// owns 32 components (16 complex columns x (re, im), or 32 real columns) = one
+// 256-byte (128 for float) segment per row of B, and keeps kColS stages of
+// kColR rows in flight while warp 0 runs the 32 chains out of shared memory —
+// the per-column chains are inherently sequential, so with few columns (n =
+// 4096 at k = 65536) a register-only loop cannot cover the DRAM latency.
+// ---------------------------------------------------------------------------
+constexpr int kColR = 64;  // rows per stage
+constexpr int kColS = 4;   // stages
+constexpr int32_t kNuPending = INT32_MIN;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename T, bool REAL>
+__global__ void __launch_bounds__(128) k_col_stats(const T* __restrict__ B, int64_t ldb, int k,
+                                                   int n, float p_fast, float delta,
+                                                   int32_t* __restrict__ nu,
+                                                   double* __restrict__ colabs,
+                                                   unsigned long long* __restrict__ diag) {
+  constexpr int kParts = REAL ? 1 : 2;
+  constexpr int kCols = 32 / kParts;            // columns per CTA
+  constexpr int kSeg = 32 * int(sizeof(T));     // bytes per row segment
+  constexpr int kChunks = kSeg / 16;            // 16-byte chunks per row segment
+  extern __shared__ __align__(16) uint8_t ring[];  // [kColS][kColR][kSeg]
+  const int j0 = blockIdx.x * kCols;
+  const int64_t row_bytes = int64_t(kParts) * ldb * int64_t(sizeof(T));
+  const char* base = reinterpret_cast<const char*>(B) + int64_t(j0) * kParts * int64_t(sizeof(T));
+  const int valid = min(kCols, n - j0) * kParts * int(sizeof(T));  // bytes of a row segment in range
+  const int nst = (k + kColR - 1) / kColR;
+  const uint32_t ring_u32 = smem_u32(ring);
+
+  auto issue = [&](int st) {
+    if (st < nst) {
+      const uint32_t dst0 = ring_u32 + (st % kColS) * (kColR * kSeg);
+      for (int c = threadIdx.x; c < kColR * kChunks; c += blockDim.x) {
+        const int r = c / kChunks, q = c % kChunks;
+        const int h = st * kColR + r;
+        const int bytes = h < k ? max(0, min(16, valid - 16 * q)) : 0;
+        const char* src = bytes ? base + h * row_bytes + 16 * q : base;
+        cp_async16(dst0 + r * kSeg + 16 * q, src, bytes);
+      }
+    }
+    cp_async_commit();  // possibly empty: keeps the group count uniform
+  };
+
+#pragma unroll
+  for (int st = 0; st < kColS - 1; ++st) issue(st);
+  double sum = 0.0, mx = 0.0, mn = INFINITY;
+  int bad = 0;
+  const int lane = threadIdx.x & 31;
+  for (int st = 0; st < nst; ++st) {
+    issue(st + kColS - 1);
+    cp_async_wait<kColS - 1>();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const T* seg = reinterpret_cast<const T*>(ring + (st % kColS) * (kColR * kSeg));
+      const int nr = min(kColR, k - st * kColR);
+      for (int r = 0; r < nr; ++r) {
+        const double x = double(seg[r * 32 + lane]);
+        const double ax = fabs(x);
+        bad |= !isfinite(x);
+        mx = fmax(mx, ax);
+        if (ax != 0.0) mn = fmin(mn, ax);
+        sum = __dadd_rn(sum, __dmul_rn(x, x));
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x >= 32) return;
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicAdd(diag + CRTG_DIAG_NONFINITE_B, 1ull);
+  double other = 0.0;
+  if (!REAL) {  // lanes (2c, 2c+1) = (re, im) of column c
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+    other = __shfl_xor_sync(0xffffffffu, sum, 1);
+  }
+  const int j = j0 + (REAL ? lane : lane >> 1);
+  if (j >= n || (!REAL && (lane & 1))) return;
+  colabs[j] = mx;
+  if (!unscaled_ok(mx, mn)) {
+    nu[j] = kNuPending;
+    return;
+  }
+  const bool zero = mx == 0.0;
+  const Pow2 sc = make_pow2(zero ? 0 : -ilogb(mx));
+  double sumsq = __dadd_rn(__dadd_rn(0.0, unscale_sq(sum, sc)), unscale_sq(other, sc));
+  if (zero) sumsq = 1.0;
+  nu[j] = fast_exponent(mx, sumsq, p_fast, delta, diag + CRTG_DIAG_CLAMPED_NU);
+}
+
+// the two-pass form for the columns k_col_stats could not take unscaled
+template <typename T, bool REAL>
+__global__ void k_col_fallback(const T* __restrict__ B, int64_t ldb, int k, int n, float p_fast,
+                               float delta, const double* __restrict__ colabs,
+                               int32_t* __restrict__ nu, unsigned long long* __restrict__ diag) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || nu[j] != kNuPending) return;
+  const double mx = colabs[j];
+  const Pow2 sc = make_pow2(mx == 0.0 ? 0 : -ilogb(mx));
+  const T* p = B + (REAL ? 1 : 2) * int64_t(j);
+  const int64_t stride = (REAL ? 1 : 2) * ldb;
+  double sr = 0.0, si = 0.0;
+  for (int h = 0; h < k; ++h) {
+    sr = __dadd_rn(sr, sq(sc, double(p[h * stride])));
+    if (!REAL) si = __dadd_rn(si, sq(sc, double(p[h * stride + 1])));
+  }
+  double sumsq = __dadd_rn(__dadd_rn(0.0, sr), si);
+  if (mx == 0.0) sumsq = 1.0;
+  nu[j] = fast_exponent(mx, sumsq, p_fast, delta, diag + CRTG_DIAG_CLAMPED_NU);
+}
+
 __global__ void k_col_finalize(int n, const double* __restrict__ colabs,
                                const double* __restrict__ colsq, float p_fast, float delta,
                                int32_t* __restrict__ nu, unsigned long long* __restrict__ diag) {
@@ -296,6 +485,12 @@ __global__ void k_accurate_exps(const int32_t* __restrict__ maxb, const double* 
 
 }  // namespace
 
+#define CRTG_TRY_L(expr)          \
+  do {                            \
+    const int _e = int(expr);     \
+    if (_e) return _e;            \
+  } while (0)
+
 #define CRTG_ELEM_DISPATCH(elem, ...)                                                    \
   switch (elem) {                                                                       \
     case E_C128: { using T = double; constexpr bool R = false; __VA_ARGS__; } break;     \
@@ -315,7 +510,7 @@ int launch_row_stats(int elem, bool fast, const void* A, int64_t lda, int64_t m,
     k_row_stats<T, R><<<unsigned(m), 256, smem, s>>>(static_cast<const T*>(A), lda, int(k), tree,
                                                      p_fast, delta, fast, mu, rowabs, diag);
   })
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 int launch_col_absmax(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
@@ -327,27 +522,46 @@ int launch_col_absmax(int elem, const void* B, int64_t ldb, int64_t k, int64_t n
     k_col_absmax<T, R><<<grid, 128, 0, s>>>(static_cast<const T*>(B), ldb, int(k), int(n),
                                             rows_per_chunk, colabs, diag);
   })
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
-int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
-                    const double* colabs, double* colsq, float p_fast, float delta, int32_t* nu,
+// Fast-mode column statistics: writes colabs and nu (colsq is scratch for the
+// two-pass path, used when B's rows are not 16-byte aligned for cp.async)
+int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n, double* colabs,
+                    double* colsq, float p_fast, float delta, int32_t* nu,
                     unsigned long long* diag, cudaStream_t s) {
   if (n <= 0) return 0;
-  const unsigned grid = unsigned((2 * n + 127) / 128);
+  const int esz = (elem == E_C128) ? 16 : (elem == E_C64 || elem == E_F64) ? 8 : 4;
+  const bool aligned = (reinterpret_cast<uintptr_t>(B) % 16 == 0) && ((ldb * esz) % 16 == 0);
+  if (!aligned) {
+    CRTG_TRY_L(cudaMemsetAsync(colabs, 0, size_t(n) * sizeof(double), s));
+    CRTG_TRY_L(launch_col_absmax(elem, B, ldb, k, n, colabs, diag, s));
+    const unsigned grid = unsigned((2 * n + 127) / 128);
+    CRTG_ELEM_DISPATCH(elem, {
+      k_col_sumsq<T, R><<<grid, 128, 0, s>>>(static_cast<const T*>(B), ldb, int(k), int(n), colabs,
+                                             colsq);
+    })
+    k_col_finalize<<<unsigned((n + 127) / 128), 128, 0, s>>>(int(n), colabs, colsq, p_fast, delta,
+                                                              nu, diag);
+    return launched(2);
+  }
   CRTG_ELEM_DISPATCH(elem, {
-    k_col_sumsq<T, R><<<grid, 128, 0, s>>>(static_cast<const T*>(B), ldb, int(k), int(n), colabs,
-                                           colsq);
+    constexpr int parts = R ? 1 : 2;
+    constexpr int cols = 32 / parts;
+    const size_t smem = size_t(kColS) * kColR * 32 * sizeof(T);
+    cudaFuncSetAttribute(k_col_stats<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_col_stats<T, R><<<unsigned((n + cols - 1) / cols), 128, smem, s>>>(
+        static_cast<const T*>(B), ldb, int(k), int(n), p_fast, delta, nu, colabs, diag);
+    k_col_fallback<T, R><<<unsigned((n + 127) / 128), 128, 0, s>>>(
+        static_cast<const T*>(B), ldb, int(k), int(n), p_fast, delta, colabs, nu, diag);
   })
-  k_col_finalize<<<unsigned((n + 127) / 128), 128, 0, s>>>(int(n), colabs, colsq, p_fast, delta,
-                                                            nu, diag);
-  return int(cudaGetLastError());
+  return launched(2);
 }
 
 int launch_bar(const double* absval, int64_t count, int32_t* bar, cudaStream_t s) {
   if (count <= 0) return 0;
   k_bar<<<unsigned((count + 255) / 256), 256, 0, s>>>(absval, count, bar);
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 int launch_accurate_exps(const int32_t* maxb, const double* absval, const int32_t* bar,
@@ -356,7 +570,7 @@ int launch_accurate_exps(const int32_t* maxb, const double* absval, const int32_
   if (count <= 0) return 0;
   k_accurate_exps<<<unsigned((count + 255) / 256), 256, 0, s>>>(maxb, absval, bar, count, p_accu,
                                                                  delta, out, clamp_counter);
-  return int(cudaGetLastError());
+  return launched(1);
 }
 
 }  // namespace crtg
