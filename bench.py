@@ -416,7 +416,7 @@ def run_ours(a, rank: int, world: int, local_rank: int):
                          "d2h_bytes_per_step": int(hC.numel() * hC.element_size()),
                          "ms_per_step": dt * 1e3,
                          "api": "paper_2512_08321_b200.emulate_gemm_complex(pinned host tensors)"
-                                " -> crtg_gemm_complex_host (B/C blocks streamed on copy engines)"}
+                                " -> crtg_gemm_complex_host (A row chunks / B column blocks streamed in a staircase, C tiles back, on the copy engines)"}
 
     if rank == 0 and world == 1 and not a.no_cpu:
         result["cpu_baseline"] = cpu_sample(a, reps=1)

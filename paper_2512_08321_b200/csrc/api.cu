@@ -999,18 +999,32 @@ struct HostChunks {
   int64_t cols;  // columns per B block (= plan nb)
 };
 
+// Staircase streaming: A in row chunks and B in column blocks of about 1/8 of
+// the matrix each, transferred interleaved (A0 B0 A1 B1 ...).  After the first
+// pair lands, every new piece releases a whole row or column of output tiles,
+// so the GPU runs back to back while the rest of the inputs stream in; the last
+// piece leaves only 1/8 of a row of tiles to compute after the final transfer.
 HostChunks host_chunks(const Plan& P) {
   HostChunks h;
-  h.rows = P.m >= 2048 ? round_up((P.m + 3) / 4, 256) : P.m;
+  h.rows = P.m >= 4096 ? round_up((P.m + 7) / 8, 256) : P.m;
   h.cols = P.nb;
   return h;
 }
 
 Plan host_plan(int mode, int64_t m, int64_t n, int64_t k, int N, int64_t n_block) {
-  // column blocks of at most n/4 (>= 1024) so transfers and compute interleave
   int64_t nb = n_block < 1 ? n : n_block;
-  if (n >= 4096) nb = std::min(nb, std::max<int64_t>(1024, round_up((n + 3) / 4, 256)));
+  if (n >= 4096) nb = std::min(nb, std::max<int64_t>(512, round_up((n + 7) / 8, 256)));
   return make_plan(mode, m, n, k, N, nb);
+}
+
+namespace {
+int load_tree(const Plan& P, void* ws, cudaStream_t s, PwTree& tree);  // below
+}  // namespace
+
+// bytes of the packed B residues of every column block (all stay resident)
+size_t host_bpack_bytes(const Plan& P) {
+  const int64_t nblk = (P.n + P.nb - 1) / P.nb;
+  return size_t(nblk) * size_t(3 * P.N) * size_t(P.nb_pad) * size_t(P.k_pad);
 }
 
 extern "C" size_t crtg_host_workspace_size(int precision, int mode, int64_t m, int64_t n,
@@ -1021,7 +1035,7 @@ extern "C" size_t crtg_host_workspace_size(int precision, int mode, int64_t m, i
   const size_t csz = (precision & CRTG_SINGLE) ? 8 : 16;
   auto r = [](size_t x) { return (x + 255) & ~size_t(255); };
   return P.total + r(size_t(m) * k * esz) + r(size_t(k) * n * esz) +
-         2 * r(size_t(hc.rows) * P.nb * csz);
+         2 * r(size_t(hc.rows) * P.nb * csz) + r(host_bpack_bytes(P));
 }
 
 // End-to-end entry on HOST buffers (pinned for full overlap).  Transfers are
@@ -1087,10 +1101,19 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     evB[j] = E.get();
     return int(cudaEventRecord(evB[j], h2d));
   };
-  CRTG_TRY(copy_a(0), "record");
-  CRTG_TRY(copy_b(0), "record");
-  for (int64_t i = 1; i < nrc; ++i) CRTG_TRY(copy_a(i), "record");
-  for (int64_t j = 1; j < nblk; ++j) CRTG_TRY(copy_b(j), "record");
+  // transfer order: A0 B0 A1 B1 ... (the longer list's tail last)
+  for (int64_t t = 0; t < std::max(nrc, nblk); ++t) {
+    if (t < nrc) CRTG_TRY(copy_a(t), "record");
+    if (t < nblk) CRTG_TRY(copy_b(t), "record");
+  }
+  // tile order: as pieces land (fast mode); accurate mode has all inputs first
+  std::vector<std::pair<int64_t, int64_t>> order;
+  for (int64_t t = 0; t < std::max(nrc, nblk); ++t) {
+    if (t < nrc)
+      for (int64_t j = 0; j < std::min(t, nblk); ++j) order.push_back({t, j});
+    if (t < nblk)
+      for (int64_t i = 0; i <= std::min(t, nrc - 1); ++i) order.push_back({i, t});
+  }
 
   int32_t* mu = at<int32_t>(ws, P.mu);
   int32_t* nu = at<int32_t>(ws, P.nu);
@@ -1100,100 +1123,96 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     CRTG_TRY(cudaStreamWaitEvent(s, evB[nblk - 1], 0), "wait");
     if (int e = run_scaling(P, precision, mode, dA, k, dB, n, dc, ws, dg, s, s)) return e;
   } else {
-    const HostTree& ht = pairwise_tree(P.k);
-    char* tb = at<char>(ws, P.tree);
-    const size_t lb = ht.leaves.size() * sizeof(int2), nbt = ht.nodes.size() * sizeof(int2),
-                 sb = ht.level_start.size() * sizeof(int);
-    CRTG_TRY(cudaMemcpyAsync(tb, ht.leaves.data(), lb, cudaMemcpyHostToDevice, s), "tree copy");
-    if (nbt) CRTG_TRY(cudaMemcpyAsync(tb + lb, ht.nodes.data(), nbt, cudaMemcpyHostToDevice, s), "tree copy");
-    CRTG_TRY(cudaMemcpyAsync(tb + lb + nbt, ht.level_start.data(), sb, cudaMemcpyHostToDevice, s),
-             "tree copy");
-    tree = PwTree{int(ht.leaves.size()), int(ht.nodes.size()), int(ht.level_start.size()) - 1,
-                  reinterpret_cast<const int2*>(tb), reinterpret_cast<const int2*>(tb + lb),
-                  reinterpret_cast<const int*>(tb + lb + nbt)};
+    if (int e = load_tree(P, ws, s, tree)) return e;
   }
   const int64_t a_plane = P.m_pad * P.k_pad;
+  const int64_t bblk = int64_t(3 * N) * P.nb_pad * P.k_pad;  // packed bytes per B block
   int8_t* apack = at<int8_t>(ws, P.a_pack);
-  int8_t* bpack = at<int8_t>(ws, P.b_pack);
+  int8_t* bpack = reinterpret_cast<int8_t*>(dC + 2 * cbuf);
+  std::vector<char> a_done(nrc, 0), b_done(nblk, 0);
   std::vector<cudaEvent_t> evD;
   int64_t tile = 0;
-  for (int64_t j = 0; j < nblk; ++j) {
+  for (const auto& ij : order) {
+    const int64_t i = ij.first, j = ij.second;
+    const int64_t i0 = i * hc.rows, h = std::min(hc.rows, m - i0);
     const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
-    for (int64_t i = 0; i < nrc; ++i, ++tile) {
-      const int64_t i0 = i * hc.rows, h = std::min(hc.rows, m - i0);
-      const bool last_rows = i == nrc - 1;
-      if (j == 0) {  // A chunk i: statistics (fast) and residues, once
-        CRTG_TRY(cudaStreamWaitEvent(s, evA[i], 0), "wait");
-        const char* Ai = dA + size_t(i0) * k * esz;
-        if (mode == CRTG_FAST) {
-          StageTimer timer(CRTG_STAGE_SCALING, s);
-          CRTG_TRY(launch_row_stats(in32 ? E_C64 : E_C128, true, Ai, k, h, k, tree, dc.p_fast, dc.delta, mu + i0,
-                                    at<double>(ws, P.rowabs) + i0, dg, s),
-                   "row stats");
-        }
-        StageTimer timer(CRTG_STAGE_RESIDUE_A, s);
-        CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 0, PACK_RESIDUE, Ai, k, h, k, 0, mu + i0, dc, apack, a_plane,
-                             P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s, 0, i0,
-                             last_rows ? P.m_pad - i0 : h),
-                 "residues A");
+    const bool last_rows = i == nrc - 1;
+    int8_t* bpj = bpack + j * bblk;
+    if (!a_done[i]) {  // A chunk i: statistics (fast) and residues, once
+      a_done[i] = 1;
+      CRTG_TRY(cudaStreamWaitEvent(s, evA[i], 0), "wait");
+      const char* Ai = dA + size_t(i0) * k * esz;
+      if (mode == CRTG_FAST) {
+        StageTimer timer(CRTG_STAGE_SCALING, s);
+        CRTG_TRY(launch_row_stats(in32 ? E_C64 : E_C128, true, Ai, k, h, k, tree, dc.p_fast,
+                                  dc.delta, mu + i0, at<double>(ws, P.rowabs) + i0, dg, s),
+                 "row stats");
       }
-      if (i == 0) {  // B block j: statistics (fast) and residues, once
-        CRTG_TRY(cudaStreamWaitEvent(s, evB[j], 0), "wait");
-        if (mode == CRTG_FAST) {
-          StageTimer timer(CRTG_STAGE_SCALING, s);
-          const char* Bj = dB + j0 * esz;
-          double* cabs = at<double>(ws, P.colabs) + j0;
-          CRTG_TRY(launch_col_fast(in32 ? E_C64 : E_C128, Bj, n, k, w, cabs, at<double>(ws, P.colsq) + 2 * j0,
-                                   dc.p_fast, dc.delta, nu + j0, dg, s),
-                   "col sumsq");
-        }
-        StageTimer timer(CRTG_STAGE_RESIDUE_B, s);
-        CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 1, PACK_RESIDUE, dB, n, w, k, j0, nu + j0, dc, bpack,
-                             w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
-                 "residues B");
-      }
-      GemmArgs g{};
-      g.a = apack;
-      g.b = bpack;
-      g.a_plane = a_plane;
-      g.b_plane = w_pad * P.k_pad;
-      g.a_rb = int(P.m_pad / 128);
-      g.b_rb = int(w_pad / 128);
-      g.mt0 = int(i0 / 128);
-      g.mt = int((last_rows ? P.m_pad - i0 : h) / 128);
-      g.nt = int(w_pad / 256);
-      g.kb = int(P.k_pad / 128);
-      g.nl = N;
-      g.planes_per_l = 3;
-      g.nphase = 3;
-      g.m = int(i0 + h);
-      g.n = int(w);
-      g.e_re = at<int8_t>(ws, P.e_re);
-      g.e_im = at<int8_t>(ws, P.e_im);
-      g.e_ld = P.nb_pad;
-      g.e_plane = m * P.nb_pad;
-      for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
-      {
-        StageTimer timer(CRTG_STAGE_GEMM, s);
-        CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
-      }
-      if (tile >= 2) CRTG_TRY(cudaStreamWaitEvent(s, evD[tile - 2], 0), "wait");
-      char* cblk = dC + (tile & 1) * cbuf;
-      {
-        StageTimer timer(CRTG_STAGE_CRT, s);
-        CRTG_TRY(launch_crt(single, false, h, w, g.e_re + i0 * g.e_ld, g.e_im + i0 * g.e_ld, g.e_plane,
-                            g.e_ld, mu + i0, nu + j0, dc, cblk, w, s),
-                 "crt");
-      }
-      cudaEvent_t evC = E.get();
-      CRTG_TRY(cudaEventRecord(evC, s), "record");
-      CRTG_TRY(cudaStreamWaitEvent(d2h, evC, 0), "wait");
-      CRTG_TRY(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(i0) * ldc + j0) * csz, ldc * csz,
-                                 cblk, w * csz, w * csz, h, cudaMemcpyDeviceToHost, d2h),
-               "D2H C");
-      evD.push_back(E.get());
-      CRTG_TRY(cudaEventRecord(evD.back(), d2h), "record");
+      StageTimer timer(CRTG_STAGE_RESIDUE_A, s);
+      CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 0, PACK_RESIDUE, Ai, k, h, k, 0, mu + i0, dc,
+                           apack, a_plane, P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s, 0, i0,
+                           last_rows ? P.m_pad - i0 : h),
+               "residues A");
     }
+    if (!b_done[j]) {  // B block j: statistics (fast) and residues, once
+      b_done[j] = 1;
+      CRTG_TRY(cudaStreamWaitEvent(s, evB[j], 0), "wait");
+      if (mode == CRTG_FAST) {
+        StageTimer timer(CRTG_STAGE_SCALING, s);
+        const char* Bj = dB + j0 * esz;
+        double* cabs = at<double>(ws, P.colabs) + j0;
+        CRTG_TRY(launch_col_fast(in32 ? E_C64 : E_C128, Bj, n, k, w, cabs,
+                                 at<double>(ws, P.colsq) + 2 * j0, dc.p_fast, dc.delta, nu + j0,
+                                 dg, s),
+                 "col stats");
+      }
+      StageTimer timer(CRTG_STAGE_RESIDUE_B, s);
+      CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 1, PACK_RESIDUE, dB, n, w, k, j0, nu + j0, dc,
+                           bpj, w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
+               "residues B");
+    }
+    GemmArgs g{};
+    g.a = apack;
+    g.b = bpj;
+    g.a_plane = a_plane;
+    g.b_plane = w_pad * P.k_pad;
+    g.a_rb = int(P.m_pad / 128);
+    g.b_rb = int(w_pad / 128);
+    g.mt0 = int(i0 / 128);
+    g.mt = int((last_rows ? P.m_pad - i0 : h) / 128);
+    g.nt = int(w_pad / 256);
+    g.kb = int(P.k_pad / 128);
+    g.nl = N;
+    g.planes_per_l = 3;
+    g.nphase = 3;
+    g.m = int(i0 + h);
+    g.n = int(w);
+    g.e_re = at<int8_t>(ws, P.e_re);
+    g.e_im = at<int8_t>(ws, P.e_im);
+    g.e_ld = P.nb_pad;
+    g.e_plane = m * P.nb_pad;
+    for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
+    {
+      StageTimer timer(CRTG_STAGE_GEMM, s);
+      CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
+    }
+    if (tile >= 2) CRTG_TRY(cudaStreamWaitEvent(s, evD[tile - 2], 0), "wait");
+    char* cblk = dC + (tile & 1) * cbuf;
+    {
+      StageTimer timer(CRTG_STAGE_CRT, s);
+      CRTG_TRY(launch_crt(single, false, h, w, g.e_re + i0 * g.e_ld, g.e_im + i0 * g.e_ld,
+                          g.e_plane, g.e_ld, mu + i0, nu + j0, dc, cblk, w, s),
+               "crt");
+    }
+    cudaEvent_t evC = E.get();
+    CRTG_TRY(cudaEventRecord(evC, s), "record");
+    CRTG_TRY(cudaStreamWaitEvent(d2h, evC, 0), "wait");
+    CRTG_TRY(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(i0) * ldc + j0) * csz, ldc * csz,
+                               cblk, w * csz, w * csz, h, cudaMemcpyDeviceToHost, d2h),
+             "D2H C");
+    evD.push_back(E.get());
+    CRTG_TRY(cudaEventRecord(evD.back(), d2h), "record");
+    ++tile;
   }
   CRTG_TRY(cudaStreamWaitEvent(s, evD.back(), 0), "wait");
   if (sync_check) return check_diag(dg, s);
