@@ -21,13 +21,16 @@ __device__ __forceinline__ uint32_t ep_pack4(uint32_t a, uint32_t b, uint32_t c,
 
 __device__ __forceinline__ uint32_t ep_byte(uint32_t w, int i) { return (w >> (8 * i)) & 0xFF; }
 
-template <int MODE>
+// NCH chunks of 32 columns per thread (8 = the whole 256-column tile, 4 = one
+// half when two warps share a TMEM lane quarter).  The Karatsuba path double-
+// buffers the TMEM loads: chunk c+1 is in flight while chunk c is reduced.
+template <int MODE, int NCH>
 __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr, int s, int l,
                                                int row, bool row_ok, int col_base,
-                                               const ModConst& mc, uint32_t (&st)[64]) {
+                                               const ModConst& mc, uint32_t (&st)[NCH * 8]) {
   if (MODE == EPI_RAW) {
 #pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < NCH; ++c) {
       uint32_t v[32];
       tmem_ld32(taddr + c * 32, v);
       tmem_wait_ld();
@@ -48,7 +51,7 @@ __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr
     int8_t* dst = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
     bool wrapped = false;
 #pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
+    for (int c = 0; c < NCH; ++c) {
       uint32_t v[32];
       tmem_ld32(taddr + c * 32, v);
       tmem_wait_ld();
@@ -75,17 +78,19 @@ __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr
   int8_t* dst_base = nullptr;
   if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
   if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  uint32_t v[2][32];
+  tmem_ld32(taddr, v[0]);
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    uint32_t v[32];
-    tmem_ld32(taddr + c * 32, v);
-    tmem_wait_ld();
+  for (int c = 0; c < NCH; ++c) {
+    tmem_wait_ld();  // chunk c has landed (the only load in flight)
+    if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
+    const uint32_t (&cv)[32] = v[c & 1];
     uint32_t out[8];
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
       uint32_t r[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) r[j] = mod_i32(int32_t(v[4 * w + j]), mc);
+      for (int j = 0; j < 4; ++j) r[j] = mod_i32(int32_t(cv[4 * w + j]), mc);
       if (s == 0) {
         st[c * 8 + w] = ep_pack4(r[0], r[1], r[2], r[3]);
       } else if (s == 1) {

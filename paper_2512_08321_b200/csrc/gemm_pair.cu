@@ -174,7 +174,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         const uint32_t buf = gslot & 1;
         mbar_wait(smem_u32(&tfull_bar[buf]), (gslot >> 1) & 1);
         tc_fence_after();
-        epilogue_phase<MODE>(g, lane_addr + buf * 256, s, l, row, row_ok, col_base, mc, st);
+        epilogue_phase<MODE, 8>(g, lane_addr + buf * 256, s, l, row, row_ok, col_base, mc, st);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty0 + buf * 8);

@@ -35,6 +35,8 @@ constexpr uint32_t kStageB = 32768;  // 256 rows x 128 B
 constexpr uint32_t kStageBytes = kStageA + kStageB;
 constexpr int kStages = 4;
 constexpr int kTmemCols = 512;
+constexpr int kEpiThreads = 256;            // 8 epilogue warps
+constexpr int kThreads = 128 + kEpiThreads;  // producer, MMA, TMEM alloc, spare + epilogue
 constexpr int kGroupM = 16;  // rasterisation: 16 row tiles share each column sweep
 
 struct Seg {
@@ -73,7 +75,7 @@ __device__ __forceinline__ void decode_tile(int t, const GemmArgs& g, int& l, in
 }  // namespace
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 1) k_gemm_i8(const __grid_constant__ GemmArgs g) {
+__global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__ GemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kStages];
   __shared__ __align__(8) uint64_t empty_bar[kStages];
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(256, 1) k_gemm_i8(const __grid_constant__ Gemm
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(smem_u32(&tfull_bar[b]), 1);
-      mbar_init(smem_u32(&tempty_bar[b]), 128);
+      mbar_init(smem_u32(&tempty_bar[b]), kEpiThreads);
     }
     fence_mbar_init();
   }
@@ -174,19 +176,20 @@ __global__ void __launch_bounds__(256, 1) k_gemm_i8(const __grid_constant__ Gemm
       if (MODE == EPI_BOUND) gslot += 2;
     }
   } else if (warp >= 4) {
-    // ---------------- epilogue (128 threads, one TMEM lane each) ----------------
+    // ------- epilogue (8 warps: lane quarter warp % 4, column half (warp - 4) / 4) -------
     const int q = warp & 3;
-    const uint32_t lane_addr = tmem + (uint32_t(32 * q) << 16);
+    const int half = (warp - 4) >> 2;
+    const uint32_t lane_addr = tmem + (uint32_t(32 * q) << 16) + uint32_t(128 * half);
     uint32_t gslot = 0;
-    uint32_t st[64];  // packed per-column state across the three Karatsuba phases
+    uint32_t st[32];  // packed per-column state across the three Karatsuba phases
 #pragma unroll
-    for (int i = 0; i < 64; ++i) st[i] = 0;
+    for (int i = 0; i < 32; ++i) st[i] = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm, tn;
       decode_tile(t, g, l, tm, tn);
       const int row = tm * 128 + 32 * q + lane;
       const bool row_ok = row < g.m;
-      const int col_base = tn * 256;
+      const int col_base = tn * 256 + 128 * half;
       if (MODE == EPI_BOUND) {
         const uint32_t par = (gslot >> 1) & 1;
         mbar_wait(smem_u32(&tfull_bar[0]), par);
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(256, 1) k_gemm_i8(const __grid_constant__ Gemm
         tc_fence_after();
         int32_t rmax = 0;
 #pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 4; ++c) {
           uint32_t cr[32], df[32];
           tmem_ld32(lane_addr + c * 32, cr);
           tmem_ld32(lane_addr + 256 + c * 32, df);
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(256, 1) k_gemm_i8(const __grid_constant__ Gemm
         const uint32_t buf = gslot & 1;
         mbar_wait(smem_u32(&tfull_bar[buf]), (gslot >> 1) & 1);
         tc_fence_after();
-        epilogue_phase<MODE>(g, lane_addr + buf * 256, s, l, row, row_ok, col_base, mc, st);
+        epilogue_phase<MODE, 4>(g, lane_addr + buf * 256, s, l, row, row_ok, col_base, mc, st);
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty_bar[buf]));
         ++gslot;
@@ -251,25 +254,25 @@ int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_KARATSUBA>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (err != cudaSuccess) return int(err);
-      k_gemm_i8<EPI_KARATSUBA><<<grid, 256, smem, stream>>>(g);
+      k_gemm_i8<EPI_KARATSUBA><<<grid, kThreads, smem, stream>>>(g);
       break;
     case EPI_RAW:
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem));
       if (err != cudaSuccess) return int(err);
-      k_gemm_i8<EPI_RAW><<<grid, 256, smem, stream>>>(g);
+      k_gemm_i8<EPI_RAW><<<grid, kThreads, smem, stream>>>(g);
       break;
     case EPI_REAL:
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_REAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem));
       if (err != cudaSuccess) return int(err);
-      k_gemm_i8<EPI_REAL><<<grid, 256, smem, stream>>>(g);
+      k_gemm_i8<EPI_REAL><<<grid, kThreads, smem, stream>>>(g);
       break;
     default:
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_BOUND>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (err != cudaSuccess) return int(err);
-      k_gemm_i8<EPI_BOUND><<<grid, 256, smem, stream>>>(g);
+      k_gemm_i8<EPI_BOUND><<<grid, kThreads, smem, stream>>>(g);
       break;
   }
   return launched(1);

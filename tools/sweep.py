@@ -16,11 +16,14 @@ import paper_2512_08321_b200 as crt  # noqa: E402
 from bench import synth  # noqa: E402
 
 CONFIGS = [
+    # cfg1: ZGEMM 1024^3 N=14 (the reference's CPU-runnable case)
+    ("zgemm", 1024, 1024, 1024, 14, "fast", 0.5),
+    ("zgemm", 1024, 1024, 1024, 14, "accurate", 0.5),
     # cfg2: CGEMM 8192^3, N 6..10, fast
     *[("cgemm", 8192, 8192, 8192, N, "fast", 1.0) for N in (6, 7, 8, 9, 10)],
     ("cgemm", 8192, 8192, 8192, 7, "accurate", 1.0),
     # cfg3: ZGEMM 16384^3, N 12..20, fast vs accurate
-    *[("zgemm", 16384, 16384, 16384, N, "fast", 0.5) for N in (12, 14, 16, 18, 20)],
+    *[("zgemm", 16384, 16384, 16384, N, "fast", 0.5) for N in (12, 14, 15, 16, 18, 20)],
     *[("zgemm", 16384, 16384, 16384, N, "accurate", 0.5) for N in (13, 15, 17)],
     # cfg4: skinny ZGEMM m=n=4096, k=65536, wide exponent range
     *[("zgemm", 4096, 4096, 65536, N, "fast", 4.0) for N in (14, 17, 20)],
