@@ -197,6 +197,9 @@ ModConst make_mod(int p) {
   c.c32 = uint32_t((uint64_t(1) << 32) % p);
   const int64_t q = ((int64_t(1) << 30) + p - 1) / p;
   c.bias = int32_t(q * p);
+  c.neg_p = uint32_t(-p);
+  c.h = uint32_t(p / 2);
+  c.bias_h = uint32_t(c.bias) + c.h;
   return c;
 }
 

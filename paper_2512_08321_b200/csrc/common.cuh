@@ -55,6 +55,9 @@ struct ModConst {
   uint32_t c32;      // 2^32 mod p
   int32_t bias;      // p * ceil(2^30 / p): makes |x| <= 2^30 non-negative
   int32_t is_pow2;
+  uint32_t neg_p;    // (uint32)(-p): u - q*p as one IMAD
+  uint32_t bias_h;   // bias + floor(p/2): sym(x) = ((x + bias_h) mod p) - floor(p/2)
+  uint32_t h;        // floor(p/2)
 };
 
 // Residue-kernel constants.  With v = 2^53 + x (x = +-M, M < 2^53) split as

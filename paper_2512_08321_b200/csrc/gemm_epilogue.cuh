@@ -21,6 +21,77 @@ __device__ __forceinline__ uint32_t ep_pack4(uint32_t a, uint32_t b, uint32_t c,
 
 __device__ __forceinline__ uint32_t ep_byte(uint32_t w, int i) { return (w >> (8 * i)) & 0xFF; }
 
+// u mod p for 0 <= u < 2^31 + 2^23 (shift = floor(log2 p) keeps the magic exact
+// there), or u mod 2^j for a power-of-two modulus (wrapping u is then harmless)
+template <bool POW2>
+__device__ __forceinline__ uint32_t ep_red(uint32_t u, const ModConst& c) {
+  if (POW2) return u & uint32_t(c.p - 1);
+  const uint32_t q = __umulhi(u, c.magic) >> c.shift;
+  uint32_t r;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(q), "r"(c.neg_p), "r"(u));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t ep_pack_bytes(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+
+// Karatsuba phases (kernel.py:45-51) with every combination folded into ONE
+// biased reduction (|D|, |E|, |F| <= k*127^2 < 2^30 for p < 256; bias >= 2^30 is
+// a multiple of p, h = floor(p/2)):
+//   phase 0 (D):  dm   = (D + bias) mod p                     -> st
+//   phase 1 (E):  e_R  = ((dm - E + bias + h) mod p) - h       -> out
+//                 keep = (dm + E + bias) mod p                 -> st
+//   phase 2 (F):  e_I  = ((F - keep + bias + h) mod p) - h     -> out
+// ((x + h) mod p) - h is the symmetric residue in [-floor(p/2), ceil(p/2) - 1].
+template <int NCH, bool POW2>
+__device__ __forceinline__ void karatsuba_phase(const GemmArgs& g, uint32_t taddr, int s, int l,
+                                                int row, bool row_ok, int col_base,
+                                                const ModConst& mc, uint32_t (&st)[NCH * 8]) {
+  int8_t* dst_base = nullptr;
+  if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  const uint32_t bias = uint32_t(mc.bias), bias_h = mc.bias_h, h = mc.h;
+  uint32_t v[2][32];
+  tmem_ld32(taddr, v[0]);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    tmem_wait_ld();  // chunk c has landed (the only load in flight)
+    if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
+    const uint32_t (&cv)[32] = v[c & 1];
+    uint32_t out[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint32_t a[4], b[4];
+      const uint32_t sw = st[c * 8 + w];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t x = cv[4 * w + j];
+        const uint32_t prev = __byte_perm(sw, 0, 0x4440 + j);  // byte j of the state
+        if (s == 0) {
+          a[j] = ep_red<POW2>(x + bias, mc);
+        } else if (s == 1) {
+          a[j] = ep_red<POW2>(prev - x + bias_h, mc) - h;
+          b[j] = ep_red<POW2>(prev + x + bias, mc);
+        } else {
+          a[j] = ep_red<POW2>(x - prev + bias_h, mc) - h;
+        }
+      }
+      if (s == 0) {
+        st[c * 8 + w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
+      } else {
+        out[w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
+        if (s == 1) st[c * 8 + w] = ep_pack_bytes(b[0], b[1], b[2], b[3]);
+      }
+    }
+    if (s != 0 && row_ok) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst_base + c * 32);
+      d4[0] = make_uint4(out[0], out[1], out[2], out[3]);
+      d4[1] = make_uint4(out[4], out[5], out[6], out[7]);
+    }
+  }
+}
+
 // NCH chunks of 32 columns per thread (8 = the whole 256-column tile, 4 = one
 // half when two warps share a TMEM lane quarter).  The Karatsuba path double-
 // buffers the TMEM loads: chunk c+1 is in flight while chunk c is reduced.
@@ -75,55 +146,10 @@ __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr
     if (wrapped && row_ok && g.overflow) atomicAdd(g.overflow, 1ull);
     return;
   }
-  int8_t* dst_base = nullptr;
-  if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
-  if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
-  uint32_t v[2][32];
-  tmem_ld32(taddr, v[0]);
-#pragma unroll
-  for (int c = 0; c < NCH; ++c) {
-    tmem_wait_ld();  // chunk c has landed (the only load in flight)
-    if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
-    const uint32_t (&cv)[32] = v[c & 1];
-    uint32_t out[8];
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      uint32_t r[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) r[j] = mod_i32(int32_t(cv[4 * w + j]), mc);
-      if (s == 0) {
-        st[c * 8 + w] = ep_pack4(r[0], r[1], r[2], r[3]);
-      } else if (s == 1) {
-        uint32_t o[4], keep[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int32_t dm = int32_t(ep_byte(st[c * 8 + w], j));
-          int32_t x = dm - int32_t(r[j]);
-          x += (x < 0) ? mc.p : 0;
-          o[j] = uint32_t(to_sym(uint32_t(x), mc));
-          int32_t y = dm + int32_t(r[j]);
-          y -= (y >= mc.p) ? mc.p : 0;
-          keep[j] = uint32_t(y);
-        }
-        out[w] = ep_pack4(o[0], o[1], o[2], o[3] & 0xFF);
-        st[c * 8 + w] = ep_pack4(keep[0], keep[1], keep[2], keep[3]);
-      } else {
-        uint32_t o[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          int32_t x = int32_t(r[j]) - int32_t(ep_byte(st[c * 8 + w], j));
-          x += (x < 0) ? mc.p : 0;
-          o[j] = uint32_t(to_sym(uint32_t(x), mc));
-        }
-        out[w] = ep_pack4(o[0], o[1], o[2], o[3] & 0xFF);
-      }
-    }
-    if (s != 0 && row_ok) {
-      uint4* d4 = reinterpret_cast<uint4*>(dst_base + c * 32);
-      d4[0] = make_uint4(out[0], out[1], out[2], out[3]);
-      d4[1] = make_uint4(out[4], out[5], out[6], out[7]);
-    }
-  }
+  if (mc.is_pow2)
+    karatsuba_phase<NCH, true>(g, taddr, s, l, row, row_ok, col_base, mc, st);
+  else
+    karatsuba_phase<NCH, false>(g, taddr, s, l, row, row_ok, col_base, mc, st);
 }
 
 }  // namespace crtg
