@@ -93,12 +93,15 @@ class NativeError(RuntimeError):
     """CUDA-side failure of the native library (no CPU fallback exists)."""
 
 
-def load(path: str = LIB_PATH) -> ctypes.CDLL:
-    """Load libcrtg.so and bind every declared symbol; raises if absent."""
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load libcrtg.so and bind every declared symbol; raises if absent.
+    CRTG_LIB=/path/to/libcrtg.so selects another build of the same library
+    (A/B timing of kernel variants, tools/ab.py)."""
     global _lib
     with _lock:
         if _lib is not None:
             return _lib
+        path = path or os.environ.get("CRTG_LIB") or LIB_PATH
         if not os.path.exists(path):
             raise NativeError(
                 f"{path} is missing: build it with `python -m paper_2512_08321_b200.build` "

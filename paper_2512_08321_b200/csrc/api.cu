@@ -264,6 +264,10 @@ DevConsts make_dev(const crtg_consts& K) {
     d.hi_limb[l][2] = int32_t(H >> 32);
   }
   d.hi_scale = limbs_ok ? std::ldexp(1.0, g) : 0.0;  // 0 -> kernel keeps the f64 S1 sum
+  for (int l = 0; l < d.n; l += 2)
+    for (int t = 0; t < 3; ++t)
+      d.limb_pair[l / 2][t] = uint32_t(d.hi_limb[l][t]) |
+                              (l + 1 < d.n ? uint32_t(d.hi_limb[l + 1][t]) << 16 : 0u);
   {
     const double c = 134217729.0 * d.p_hi;
     d.p_split_hi = c - (c - d.p_hi);

@@ -88,6 +88,8 @@ struct DevConsts {
   // limbs (integer-pipe accumulation of the exact S1 sum), Dekker split of p_hi
   // and its reciprocal (division-free quotient with an exact fallback).
   int32_t hi_limb[CRTG_MAX_MODULI][3];
+  // limb k of moduli (2i, 2i+1) as two unsigned 16-bit halves (dp2a operand)
+  uint32_t limb_pair[CRTG_MAX_MODULI / 2][3];
   double hi_scale;  // 2^hi_shift
   double p_split_hi, p_split_lo, inv_p;
 };

@@ -82,6 +82,19 @@ __device__ __forceinline__ double reduce_single(double s, const DevConsts& dc) {
   return __dsub_rn(__dsub_rn(s, __dmul_rn(z, dc.p_hi)), __dmul_rn(z, dc.p_lo));
 }
 
+// c + a.h0 * b.b0 + a.h1 * b.b1 (lo: bytes 0,1 / hi: bytes 2,3); a unsigned 16-bit
+// halves, b signed bytes
+__device__ __forceinline__ int32_t dp2a_lo(uint32_t a, uint32_t b, int32_t c) {
+  int32_t d;
+  asm("dp2a.lo.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ int32_t dp2a_hi(uint32_t a, uint32_t b, int32_t c) {
+  int32_t d;
+  asm("dp2a.hi.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t load_word(const int8_t* p, bool aligned, int64_t j0, int64_t n) {
   if (aligned) return *reinterpret_cast<const uint32_t*>(p);
   uint32_t w = 0;
@@ -113,8 +126,10 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
   double s1r[4] = {0, 0, 0, 0}, s1i[4] = {0, 0, 0, 0};
   double s2r[4] = {0, 0, 0, 0}, s2i[4] = {0, 0, 0, 0};
   // residue words are loaded in batches of kB moduli ahead of the arithmetic
-  // (latency-bound otherwise); terms are still added in ascending l
-  constexpr int kB = 5;
+  // (latency-bound otherwise); S2 terms are still added in ascending l, and the
+  // exact integer S1 limbs take two moduli per dp2a (16-bit limb pair x the
+  // residue bytes of both moduli)
+  constexpr int kB = 6;
   for (int l0 = 0; l0 < dc.n; l0 += kB) {
     uint32_t wr[kB], wi[kB];
 #pragma unroll
@@ -125,25 +140,46 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
         if (!REAL) wi[b] = load_word(pi + (l0 + b) * e_plane, aligned, j0, n);
       }
     }
+    if constexpr (LIMBS) {
+#pragma unroll
+      for (int b = 0; b < kB; b += 2) {
+        if (l0 + b >= dc.n) break;
+        // bytes (e_l[q], e_l+1[q]) for q = 0,1 and q = 2,3
+        const uint32_t r01 = __byte_perm(wr[b], wr[b + 1], 0x5140);
+        const uint32_t r23 = __byte_perm(wr[b], wr[b + 1], 0x7362);
+        const uint32_t i01 = __byte_perm(wi[b], wi[b + 1], 0x5140);
+        const uint32_t i23 = __byte_perm(wi[b], wi[b + 1], 0x7362);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const uint32_t hp = dc.limb_pair[(l0 + b) >> 1][t];
+          tr[t][0] = dp2a_lo(hp, r01, tr[t][0]);
+          tr[t][1] = dp2a_hi(hp, r01, tr[t][1]);
+          tr[t][2] = dp2a_lo(hp, r23, tr[t][2]);
+          tr[t][3] = dp2a_hi(hp, r23, tr[t][3]);
+          if (!REAL) {
+            ti[t][0] = dp2a_lo(hp, i01, ti[t][0]);
+            ti[t][1] = dp2a_hi(hp, i01, ti[t][1]);
+            ti[t][2] = dp2a_lo(hp, i23, ti[t][2]);
+            ti[t][3] = dp2a_hi(hp, i23, ti[t][3]);
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int b = 0; b < kB; ++b) {
       const int l = l0 + b;
       if (l >= dc.n) break;
       const double cl = dc.coeff_lo[l];
-      const int32_t h0 = dc.hi_limb[l][0], h1 = dc.hi_limb[l][1], h2 = dc.hi_limb[l][2];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int32_t er = int32_t(int8_t(wr[b] >> (8 * q)));
         const int32_t ei = int32_t(int8_t(wi[b] >> (8 * q)));
-        if constexpr (LIMBS) {
-          tr[0][q] += h0 * er; tr[1][q] += h1 * er; tr[2][q] += h2 * er;
-          ti[0][q] += h0 * ei; ti[1][q] += h1 * ei; ti[2][q] += h2 * ei;
-        } else {
+        if constexpr (!LIMBS) {
           s1r[q] = __dadd_rn(s1r[q], __dmul_rn(dc.coeff_hi[l], double(er)));
           s1i[q] = __dadd_rn(s1i[q], __dmul_rn(dc.coeff_hi[l], double(ei)));
         }
         s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, double(er)));
-        s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, double(ei)));
+        if (!REAL) s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, double(ei)));
       }
     }
   }

@@ -257,9 +257,10 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
   const double scale = __longlong_as_double(e >= -1022 ? int64_t(e + 1023) << 52
                                                        : int64_t(1) << (e + 1074));
 
+  // q = x * 2^e exactly (quantize, scaling.py:277-293); a' = trunc(q)
   double qr[8], qi[8];
   int bad = 0;
-  bool wide = false;
+  bool wide = false, huge = false;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int h = h0 + t;
@@ -269,20 +270,42 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
                                   : X + (REAL ? 1 : 2) * (int64_t(h) * ldx + col0 + row);
       load_c<T, REAL>(p, re, im);
     }
-    qr[t] = trunc(__dmul_rn(re, scale));
-    qi[t] = trunc(__dmul_rn(im, scale));
+    qr[t] = __dmul_rn(re, scale);
+    qi[t] = __dmul_rn(im, scale);
     if (!(fabs(qr[t]) < 0x1p90)) { bad = 1; qr[t] = 0.0; }
     if (!(fabs(qi[t]) < 0x1p90)) { bad = 1; qi[t] = 0.0; }
-    wide |= fabs(qr[t]) >= 0x1p53 || fabs(qi[t]) >= 0x1p53;
+    const double mq = fmax(fabs(qr[t]), fabs(qi[t]));
+    wide |= mq >= 0x1p53;  // (q >= 2^53 is an integer, so this is |trunc q| >= 2^53)
+    huge |= mq >= 0x1p63;
   }
   // warp-uniform representation (the wide form is valid for every value): a
   // warp that mixed both would execute both per-modulus paths
   wide = __any_sync(0xffffffffu, wide);
+  huge = __any_sync(0xffffffffu, huge);
   Val3 vr[8], vi[8];
+  if (!huge) {
+    // |a'| < 2^63: one truncating conversion gives a' as int64; then
+    //   narrow: v = 2^53 + a' -> (v >> 32, low word)
+    //   wide:   2^90 + a' (96-bit) = (lo(a'), hi(a'), 2^26 + sign(a'))
 #pragma unroll
-  for (int t = 0; t < 8; ++t) {
-    vr[t] = wide ? split_wide(qr[t]) : split_narrow(qr[t]);
-    vi[t] = wide ? split_wide(qi[t]) : split_narrow(qi[t]);
+    for (int t = 0; t < 8; ++t) {
+      const long long ar = __double2ll_rz(qr[t]), ai = __double2ll_rz(qi[t]);
+      if (wide) {
+        vr[t] = {uint32_t(ar), uint32_t(uint64_t(ar) >> 32), (1u << 26) + uint32_t(ar >> 63)};
+        vi[t] = {uint32_t(ai), uint32_t(uint64_t(ai) >> 32), (1u << 26) + uint32_t(ai >> 63)};
+      } else {
+        const uint64_t wr = uint64_t(ar) + (uint64_t(1) << 53);
+        const uint64_t wi = uint64_t(ai) + (uint64_t(1) << 53);
+        vr[t] = {uint32_t(wr >> 32), uint32_t(wr), 0u};
+        vi[t] = {uint32_t(wi >> 32), uint32_t(wi), 0u};
+      }
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      vr[t] = split_wide(trunc(qr[t]));
+      vi[t] = split_wide(trunc(qi[t]));
+    }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(overflow, 1ull);
 
