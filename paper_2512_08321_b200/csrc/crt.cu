@@ -109,11 +109,12 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
                                              const int32_t* __restrict__ nu,
                                              const __grid_constant__ DevConsts dc, void* C,
                                              int64_t ldc) {
+  // 2-D: x = quads of 4 columns, y strides over rows (no division per element)
   const int64_t nq = (n + 3) >> 2;
-  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < m * nq;
-       t += int64_t(gridDim.x) * blockDim.x) {
-  const int64_t i = t / nq;
-  const int64_t j0 = (t - i * nq) * 4;
+  const int64_t jq = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (jq >= nq) return;
+  const int64_t j0 = jq * 4;
+  for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
   const int8_t* pr = e_re + i * e_ld + j0;
   const int8_t* pi = e_im + i * e_ld + j0;
   const bool aligned = ((reinterpret_cast<uintptr_t>(pr) |
@@ -238,11 +239,13 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
                const int8_t* e_im, int64_t e_plane, int64_t e_ld, const int32_t* mu,
                const int32_t* nu, const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s,
                int max_ctas) {
-  const int64_t total = m * ((n + 3) / 4);
-  if (total <= 0) return 0;
-  int64_t g = (total + 255) / 256;
-  if (max_ctas > 0 && max_ctas < g) g = max_ctas;
-  const unsigned grid = unsigned(g);
+  const int64_t nq = (n + 3) / 4;
+  if (m <= 0 || nq <= 0) return 0;
+  const unsigned gx = unsigned((nq + 255) / 256);
+  int64_t gy = std::min<int64_t>(m, 65535);
+  // max_ctas (side-stream runs beside the GEMM): cap the total CTA count
+  if (max_ctas > 0) gy = std::max<int64_t>(1, std::min<int64_t>(gy, max_ctas / int64_t(gx)));
+  const dim3 grid(gx, unsigned(gy));
   const bool limbs = dc.hi_scale != 0.0;
 #define CRTG_CRT(S, L, R) \
   k_crt<S, L, R><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
