@@ -79,11 +79,8 @@ def _to_device_matrix(x, name: str, dev, complex_out: bool = True):
         raise DimensionError(f"{name} must be 2-D")
     if complex_out and arr.dtype not in (np.complex64, np.complex128):
         arr = arr.astype(np.complex128)
-    arr = np.ascontiguousarray(arr)
-    t = torch.from_numpy(arr)
-    if t.numel() * t.element_size() >= (1 << 20):
-        t = t.pin_memory()
-    return t.to(dev, non_blocking=True), False
+    # pageable upload (11 GB/s) beats copying into a fresh pinned buffer first
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(dev), False
 
 
 def _workspace(nbytes: int, dev) -> torch.Tensor:
@@ -103,10 +100,14 @@ def emulate_gemm_complex(a, b, cfg: EmuConfig | None = None,
     on_dev = [isinstance(x, torch.Tensor) and x.is_cuda for x in (a, b)]
     if not any(on_dev):
         # host operands: stream them through the copy engines (crtg_gemm_complex_host)
-        ha, a_torch = _host_matrix(a, "A")
-        hb, b_torch = _host_matrix(b, "B")
-        _check_shapes(ha, hb)
-        out = run_complex_host(ha, hb, cfg, diagnostics, dev)
+        pins = _HostPins()
+        try:
+            ha, a_torch = _host_matrix(a, "A", pins)
+            hb, b_torch = _host_matrix(b, "B", pins)
+            _check_shapes(ha, hb)
+            out = run_complex_host(ha, hb, cfg, diagnostics, dev)  # synchronous
+        finally:
+            pins.release()
         return out if (a_torch and b_torch) else out.numpy()
     at, a_torch = _to_device_matrix(a, "A", dev)
     bt, b_torch = _to_device_matrix(b, "B", dev)
@@ -124,8 +125,38 @@ def _check_shapes(at, bt):
         raise DimensionError(f"inner dimension {at.shape[1]} exceeds {MAX_K_COMPLEX}")
 
 
-def _host_matrix(x, name: str):
-    """-> (contiguous pinned CPU complex tensor, was_torch)."""
+_REGISTER_MIN_BYTES = 32 << 20
+
+
+class _HostPins:
+    """Page-locks large numpy operands IN PLACE (cudaHostRegister) for the
+    duration of a host-path call.  Copying a 4 GiB array into a fresh pinned
+    buffer (`Tensor.pin_memory`) takes ~2.7 s on the B200 boxes; registering the
+    caller's pages takes ~0.33 s, and the copy engines then stream at full PCIe
+    rate (50 GB/s vs 11 GB/s from pageable memory)."""
+
+    def __init__(self):
+        self.ptrs = []
+
+    def pin(self, arr: np.ndarray):
+        if arr.nbytes < _REGISTER_MIN_BYTES:
+            return torch.from_numpy(arr)
+        cr = torch.cuda.cudart()
+        err = cr.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+        if int(err) == 0:
+            self.ptrs.append(arr.ctypes.data)
+        # already registered / not registrable: the copies still work (pageable)
+        return torch.from_numpy(arr)
+
+    def release(self):
+        cr = torch.cuda.cudart()
+        for ptr in self.ptrs:
+            cr.cudaHostUnregister(ptr)
+        self.ptrs.clear()
+
+
+def _host_matrix(x, name: str, pins: _HostPins):
+    """-> (contiguous CPU complex tensor, page-locked while the call runs, was_torch)."""
     if isinstance(x, torch.Tensor):
         t = x
         if t.dim() != 2:
@@ -133,13 +164,15 @@ def _host_matrix(x, name: str):
         if t.dtype not in (torch.complex64, torch.complex128):
             t = t.to(torch.complex128)
         t = t.contiguous()
-        return (t if t.is_pinned() else t.pin_memory()), True
+        if t.is_pinned():
+            return t, True
+        return pins.pin(t.numpy()), True
     arr = np.asarray(x)
     if arr.ndim != 2:
         raise DimensionError(f"{name} must be 2-D")
     if arr.dtype not in (np.complex64, np.complex128):
         arr = arr.astype(np.complex128)
-    return torch.from_numpy(np.ascontiguousarray(arr)).pin_memory(), False
+    return pins.pin(np.ascontiguousarray(arr)), False
 
 
 def run_complex_host(ha: torch.Tensor, hb: torch.Tensor, cfg: EmuConfig,
@@ -147,8 +180,8 @@ def run_complex_host(ha: torch.Tensor, hb: torch.Tensor, cfg: EmuConfig,
     """Host (pinned) operands in, pinned host result out; H2D of B's column blocks
     and D2H of C's blocks overlap the GPU work (crtg_gemm_complex_host)."""
     dev = dev or _device()
-    if ha.dtype != hb.dtype:
-        ha, hb = ha.to(torch.complex128).pin_memory(), hb.to(torch.complex128).pin_memory()
+    if ha.dtype != hb.dtype:  # mixed complex64 / complex128: widen the narrow one
+        ha, hb = ha.to(torch.complex128), hb.to(torch.complex128)
     m, k = ha.shape
     n = hb.shape[1]
     nmod = cfg.resolved_moduli

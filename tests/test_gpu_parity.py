@@ -299,7 +299,8 @@ def test_subblock_parity_large(crt):
 
 
 @pytest.mark.parametrize("mode", ["fast", "accurate"])
-@pytest.mark.parametrize("shape", [(4352, 4608, 300), (4100, 300, 260), (300, 8300, 129)])
+@pytest.mark.parametrize("shape", [(4352, 4608, 300), (4100, 300, 260), (300, 8300, 129),
+                                   (4100, 260, 1100)])  # A = 72 MB: page-locked in place
 def test_host_streaming_equals_device_path(crt, mode, shape):
     """crtg_gemm_complex_host (numpy in/out, A row chunks x B column blocks
     streamed in a staircase over the copy engines) is bitwise the device path,
