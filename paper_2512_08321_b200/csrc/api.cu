@@ -200,10 +200,55 @@ ModConst make_mod(int p) {
   c.neg_p = uint32_t(-p);
   c.h = uint32_t(p / 2);
   c.bias_h = uint32_t(c.bias) + c.h;
+  c.nphase = 3;
   return c;
 }
 
-DevConsts make_dev(const crtg_consts& K) {
+// smallest j in [1, p) with j^2 == -1 (mod p), or 0.  Exists iff p is odd (or
+// 2) and every prime factor of p is 1 mod 4: then Z[i]/p splits and a complex
+// product mod p is two independent products (U U', V V') instead of three.
+int sqrt_minus_one(int p) {
+  if (p % 2 == 0) return 0;
+  for (int j = 1; j < p; ++j)
+    if ((j * j + 1) % p == 0) return j;
+  return 0;
+}
+
+int inv_mod(int a, int p) {
+  for (int x = 1; x < p; ++x)
+    if ((a * x) % p == 1) return x;
+  return 0;
+}
+
+// CRTG_SPLIT=0 forces the 3-product Karatsuba form for every modulus (A/B
+// experiments; the results are bit-identical either way)
+bool split_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CRTG_SPLIT");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+// switch modulus l of the pipeline constants to the split (2-product) form
+void make_split(ModConst& mc, ResConst& rc, int p) {
+  const int j = sqrt_minus_one(p);
+  if (j == 0) return;
+  const int h = p / 2;
+  mc.nphase = 2;
+  mc.inv2 = uint32_t(inv_mod(2, p));
+  mc.inv2j = uint32_t(inv_mod((2 * j) % p, p));
+  rc.split = 1;
+  rc.gj = uint32_t(j);
+  rc.gjn = uint32_t(p - j);
+  rc.gku = uint32_t((p - (j * h) % p) % p);
+  rc.gkv = uint32_t((p - ((p - j) * h) % p) % p);
+}
+
+// split = true: moduli with a square root of -1 use the 2-product form (the
+// production pipeline); false keeps the reference's [re, im, re+im] planes for
+// every modulus (the crtg_residues parity hook unpacks them)
+DevConsts make_dev(const crtg_consts& K, bool split = true) {
   DevConsts d{};
   d.n = K.num_moduli;
   for (int l = 0; l < d.n; ++l) {
@@ -237,6 +282,7 @@ DevConsts make_dev(const crtg_consts& K) {
       for (int i = 0; i < 90; ++i) t = (t * 2) % uint64_t(p);
       rc.kw = uint32_t((h + uint32_t(p) - uint32_t(t)) % uint32_t(p));
     }
+    if (split && split_enabled()) make_split(d.mc[l], rc, p);
     d.coeff_hi[l] = K.coeff_hi[l];
     d.coeff_lo[l] = K.coeff_lo[l];
   }
@@ -738,7 +784,7 @@ int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim, const 
   const int64_t plane = r_pad * k_pad;
   if (ws_bytes < size_t(3 * N) * plane) return fail(CRTG_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const DevConsts dc = make_dev(*K);
+  const DevConsts dc = make_dev(*K, false);
   int8_t* packed = static_cast<int8_t*>(ws);
   unsigned long long* ovf = reinterpret_cast<unsigned long long*>(diag) +
                             (operand == 0 ? CRTG_DIAG_OVERFLOW_A : CRTG_DIAG_OVERFLOW_B);
@@ -758,7 +804,8 @@ size_t crtg_i8_workspace_size(int64_t m, int64_t n, int64_t k, int nplanes) {
   t += round_up(size_t(nplanes) * n_pad * k_pad, 256);
   t += round_up(size_t(m) * n_pad * 4, 256);
   t += round_up(size_t(m) * n_pad * 2, 256);
-  t += round_up(size_t(m_pad) * k_pad + size_t(n_pad) * k_pad, 256);  // Karatsuba sums
+  // Karatsuba sums, or the split-modulus U and V planes
+  t += 2 * round_up(size_t(m_pad) * k_pad + size_t(n_pad) * k_pad, 256);
   return t;
 }
 
@@ -809,6 +856,15 @@ __global__ void k_mod_sum(const int8_t* __restrict__ x, const int8_t* __restrict
   const uint32_t r = mod_i32(int32_t(x[i]) + int32_t(y[i]), mc);
   out[i] = int8_t(to_sym(r, mc));
 }
+
+// split-modulus planes: sym(x + c y mod p)  (U: c = j, V: c = p - j)
+__global__ void k_mod_lin(const int8_t* __restrict__ x, const int8_t* __restrict__ y, int c,
+                          int64_t count, ModConst mc, int8_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint32_t r = mod_i32(int32_t(x[i]) + c * int32_t(y[i]), mc);
+  out[i] = int8_t(to_sym(r, mc));
+}
 }  // namespace
 
 extern "C" int crtg_complex_gemm_mod(int64_t m, int64_t n, int64_t k, const int8_t* ar,
@@ -827,17 +883,36 @@ extern "C" int crtg_complex_gemm_mod(int64_t m, int64_t n, int64_t k, const int8
   int8_t* bp = ap + round_up(3 * a_plane, 256);
   int8_t* eo = bp + round_up(3 * b_plane, 256);  // [2][m][n_pad]
   int8_t* sums = eo + round_up(m * n_pad * 4, 256);
-  const ModConst mc = make_mod(p);
-  // Karatsuba operand sums sa = sym(ar + ai), sb = sym(br + bi)  (kernel.py:101-103)
-  k_mod_sum<<<unsigned((m * k + 255) / 256), 256, 0, s>>>(ar, ai, m * k, mc, sums);
-  k_mod_sum<<<unsigned((k * n + 255) / 256), 256, 0, s>>>(br, bi, k * n, mc, sums + m * k);
-  CRTG_TRY(launched(2), "mod sum");
-  CRTG_TRY(launch_pack_i8(ar, 0, m, k, ap, m_pad / 128, s), "pack");
-  CRTG_TRY(launch_pack_i8(ai, 0, m, k, ap + a_plane, m_pad / 128, s), "pack");
-  CRTG_TRY(launch_pack_i8(sums, 0, m, k, ap + 2 * a_plane, m_pad / 128, s), "pack");
-  CRTG_TRY(launch_pack_i8(br, 1, n, k, bp, n_pad / 128, s), "pack");
-  CRTG_TRY(launch_pack_i8(bi, 1, n, k, bp + b_plane, n_pad / 128, s), "pack");
-  CRTG_TRY(launch_pack_i8(sums + m * k, 1, n, k, bp + 2 * b_plane, n_pad / 128, s), "pack");
+  ModConst mc = make_mod(p);
+  const int j = split_enabled() ? sqrt_minus_one(p) : 0;
+  const unsigned ga = unsigned((m * k + 255) / 256), gb = unsigned((k * n + 255) / 256);
+  if (j) {
+    // split modulus: U = sym(re + j im), V = sym(re - j im), two products
+    ResConst unused{};
+    make_split(mc, unused, p);
+    int8_t* u = sums;                   // [U_a | U_b]
+    int8_t* v = sums + m * k + k * n;   // [V_a | V_b]
+    k_mod_lin<<<ga, 256, 0, s>>>(ar, ai, j, m * k, mc, u);
+    k_mod_lin<<<gb, 256, 0, s>>>(br, bi, j, k * n, mc, u + m * k);
+    k_mod_lin<<<ga, 256, 0, s>>>(ar, ai, p - j, m * k, mc, v);
+    k_mod_lin<<<gb, 256, 0, s>>>(br, bi, p - j, k * n, mc, v + m * k);
+    CRTG_TRY(launched(4), "split planes");
+    CRTG_TRY(launch_pack_i8(u, 0, m, k, ap, m_pad / 128, s), "pack");
+    CRTG_TRY(launch_pack_i8(v, 0, m, k, ap + a_plane, m_pad / 128, s), "pack");
+    CRTG_TRY(launch_pack_i8(u + m * k, 1, n, k, bp, n_pad / 128, s), "pack");
+    CRTG_TRY(launch_pack_i8(v + m * k, 1, n, k, bp + b_plane, n_pad / 128, s), "pack");
+  } else {
+    // Karatsuba operand sums sa = sym(ar + ai), sb = sym(br + bi)  (kernel.py:101-103)
+    k_mod_sum<<<ga, 256, 0, s>>>(ar, ai, m * k, mc, sums);
+    k_mod_sum<<<gb, 256, 0, s>>>(br, bi, k * n, mc, sums + m * k);
+    CRTG_TRY(launched(2), "mod sum");
+    CRTG_TRY(launch_pack_i8(ar, 0, m, k, ap, m_pad / 128, s), "pack");
+    CRTG_TRY(launch_pack_i8(ai, 0, m, k, ap + a_plane, m_pad / 128, s), "pack");
+    CRTG_TRY(launch_pack_i8(sums, 0, m, k, ap + 2 * a_plane, m_pad / 128, s), "pack");
+    CRTG_TRY(launch_pack_i8(br, 1, n, k, bp, n_pad / 128, s), "pack");
+    CRTG_TRY(launch_pack_i8(bi, 1, n, k, bp + b_plane, n_pad / 128, s), "pack");
+    CRTG_TRY(launch_pack_i8(sums + m * k, 1, n, k, bp + 2 * b_plane, n_pad / 128, s), "pack");
+  }
   GemmArgs g{};
   g.a = ap;
   g.b = bp;

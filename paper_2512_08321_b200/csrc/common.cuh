@@ -58,6 +58,13 @@ struct ModConst {
   uint32_t neg_p;    // (uint32)(-p): u - q*p as one IMAD
   uint32_t bias_h;   // bias + floor(p/2): sym(x) = ((x + bias_h) mod p) - floor(p/2)
   uint32_t h;        // floor(p/2)
+  // Karatsuba epilogue: 3 phases (D = Ar*Br, E = Ai*Bi, F = As*Bs).  Split
+  // moduli (some j with j^2 == -1 mod p): 2 phases, X = U*U', Y = V*V' on the
+  // planes U = sym(re + j im), V = sym(re - j im); then
+  //   e_R = (X + Y) / 2,  e_I = (X - Y) / (2 j)   (mod p)
+  int32_t nphase;    // 3, or 2 for a split modulus
+  uint32_t inv2;     // 2^-1 mod p        (split moduli)
+  uint32_t inv2j;    // (2 j)^-1 mod p    (split moduli)
 };
 
 // Residue-kernel constants.  With v = 2^53 + x (x = +-M, M < 2^53) split as
@@ -74,6 +81,10 @@ struct ResConst {
   //  u = sum_i limb_i * (2^(16 i) mod p) + kw  ==  a' + h  (mod p);
   //  dw0123 = bytes (c0, c16, c32, c48), dw45 = (c64, c80)
   uint32_t dn, dw0123, dw45, kw;
+  // split moduli (ModConst::nphase == 2): planes U, V instead of re, im, re+im;
+  // t_U = (t_re + j t_im + ku) mod p, t_V = (t_re + (p - j) t_im + kv) mod p
+  // (ku = -j h, kv = j h mod p keep the +h bias of the t form)
+  uint32_t split, gj, gjn, gku, gkv;
 };
 
 struct DevConsts {

@@ -92,6 +92,71 @@ __device__ __forceinline__ void karatsuba_phase(const GemmArgs& g, uint32_t tadd
   }
 }
 
+// Split modulus (ModConst::nphase == 2, j^2 == -1 mod p):
+//   phase 0 (X = U*U'):  xm  = (X + bias) mod p                  -> st
+//   phase 1 (Y = V*V'):  ym  = (Y + bias) mod p
+//                        e_R = (((xm + ym) inv2 + h) mod p) - h        -> out
+//                        e_I = (((xm - ym + p) inv2j + h) mod p) - h   -> out
+// X == CR + j CI and Y == CR - j CI (mod p), so e_R, e_I are the same residues
+// the three Karatsuba products give.  Operands of the last two reductions are
+// below 2p^2 + p < 2^17.
+template <int NCH>
+__device__ __forceinline__ void split_phase(const GemmArgs& g, uint32_t taddr, int s, int l,
+                                            int row, bool row_ok, int col_base,
+                                            const ModConst& mc, uint32_t (&st)[NCH * 8]) {
+  int8_t* dre = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  int8_t* dim = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  const uint32_t bias = uint32_t(mc.bias), h = mc.h, p = uint32_t(mc.p);
+  const uint32_t inv2 = mc.inv2, inv2j = mc.inv2j;
+  uint32_t v[2][32];
+  tmem_ld32(taddr, v[0]);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    tmem_wait_ld();
+    if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
+    const uint32_t (&cv)[32] = v[c & 1];
+    uint32_t ore[8], oim[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint32_t a[4], b[4];
+      const uint32_t sw = st[c * 8 + w];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t x = cv[4 * w + j];
+        if (s == 0) {
+          a[j] = ep_red<false>(x + bias, mc);
+        } else {
+          const uint32_t xm = __byte_perm(sw, 0, 0x4440 + j);
+          const uint32_t ym = ep_red<false>(x + bias, mc);
+          a[j] = ep_red<false>((xm + ym) * inv2 + h, mc) - h;
+          b[j] = ep_red<false>((xm + p - ym) * inv2j + h, mc) - h;
+        }
+      }
+      if (s == 0) {
+        st[c * 8 + w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
+      } else {
+        ore[w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
+        oim[w] = ep_pack_bytes(b[0], b[1], b[2], b[3]);
+      }
+    }
+    if (s != 0 && row_ok) {
+      uint4* r4 = reinterpret_cast<uint4*>(dre + c * 32);
+      r4[0] = make_uint4(ore[0], ore[1], ore[2], ore[3]);
+      r4[1] = make_uint4(ore[4], ore[5], ore[6], ore[7]);
+      uint4* i4 = reinterpret_cast<uint4*>(dim + c * 32);
+      i4[0] = make_uint4(oim[0], oim[1], oim[2], oim[3]);
+      i4[1] = make_uint4(oim[4], oim[5], oim[6], oim[7]);
+    }
+  }
+}
+
+// segments (K loops) of one output tile: the Karatsuba / split count of its
+// modulus, or the launch's fixed count (RAW, REAL)
+template <int MODE>
+__device__ __forceinline__ int tile_segments(const GemmArgs& g, int l) {
+  return MODE == EPI_KARATSUBA ? g.mc[l].nphase : g.nphase;
+}
+
 // NCH chunks of 32 columns per thread (8 = the whole 256-column tile, 4 = one
 // half when two warps share a TMEM lane quarter).  The Karatsuba path double-
 // buffers the TMEM loads: chunk c+1 is in flight while chunk c is reduced.
@@ -146,7 +211,9 @@ __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr
     if (wrapped && row_ok && g.overflow) atomicAdd(g.overflow, 1ull);
     return;
   }
-  if (mc.is_pow2)
+  if (mc.nphase == 2)
+    split_phase<NCH>(g, taddr, s, l, row, row_ok, col_base, mc, st);
+  else if (mc.is_pow2)
     karatsuba_phase<NCH, true>(g, taddr, s, l, row, row_ok, col_base, mc, st);
   else
     karatsuba_phase<NCH, false>(g, taddr, s, l, row, row_ok, col_base, mc, st);

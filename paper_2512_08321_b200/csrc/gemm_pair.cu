@@ -95,7 +95,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   const uint32_t tmem = tmem_slot;
 
   const int total = g.nl * (g.mt >> 1) * g.nt;
-  const int nseg = g.nphase;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
@@ -106,6 +105,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     for (int t = cid; t < total; t += ncl) {
       int l, tm2, tn;
       decode_pair(t, g, l, tm2, tn);
+      const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         // rows of the [bytes/128][128] view: one 16 KiB block = 128 rows
         const int64_t a_row0 = (int64_t)(l * g.planes_per_l + s) * (g.a_plane >> 7);
@@ -132,6 +132,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       constexpr uint32_t idesc = idesc_i8(256, 256);
       uint32_t stage = 0, phase = 0, gslot = 0;
       for (int t = cid; t < total; t += ncl) {
+        int l, tm2, tn;
+        decode_pair(t, g, l, tm2, tn);
+        const int nseg = tile_segments<MODE>(g, l);
         for (int s = 0; s < nseg; ++s) {
           const uint32_t buf = gslot & 1;
           mbar_wait_cluster(smem_u32(&tempty_bar[buf]), ((gslot >> 1) & 1) ^ 1);
@@ -170,6 +173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const bool row_ok = row < g.m;
       const int col_base = tn * 256;
       const ModConst mc = g.mc[l];
+      const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const uint32_t buf = gslot & 1;
         mbar_wait(smem_u32(&tfull_bar[buf]), (gslot >> 1) & 1);

@@ -43,10 +43,6 @@ struct Seg {
   int a_plane, b_plane, buf, accumulate;
 };
 
-template <int MODE>
-__device__ __forceinline__ int num_segs(const GemmArgs& g) {
-  return MODE == EPI_BOUND ? 3 : g.nphase;
-}
 
 template <int MODE>
 __device__ __forceinline__ Seg seg_of(int s) {
@@ -106,7 +102,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
   const uint32_t tmem = tmem_slot;
 
   const int total = g.nl * g.mt * g.nt;
-  const int nseg = num_segs<MODE>(g);
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer ----------------
@@ -114,6 +109,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm, tn;
       decode_tile(t, g, l, tm, tn);
+      const int nseg = MODE == EPI_BOUND ? 3 : tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const Seg sg = seg_of<MODE>(s);
         const int8_t* a = g.a + (int64_t)(l * g.planes_per_l + sg.a_plane) * g.a_plane;
@@ -134,6 +130,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
     constexpr uint32_t idesc = idesc_i8(128, 256);
     uint32_t stage = 0, phase = 0, gslot = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int l, tm, tn;
+      decode_tile(t, g, l, tm, tn);
+      const int nseg = MODE == EPI_BOUND ? 3 : tile_segments<MODE>(g, l);
       if (MODE == EPI_BOUND) {
         const uint32_t par = ((gslot >> 1) & 1) ^ 1;
         mbar_wait(smem_u32(&tempty_bar[0]), par);
@@ -221,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
         continue;
       }
       const ModConst mc = g.mc[l];
+      const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const uint32_t buf = gslot & 1;
         mbar_wait(smem_u32(&tfull_bar[buf]), (gslot >> 1) & 1);

@@ -205,6 +205,8 @@ __device__ __forceinline__ uint32_t pack_sym(uint32_t a, uint32_t b, uint32_t c,
   return __byte_perm(lo, hi, 0x5410);
 }
 
+// planes of one modulus: [re, im, re+im] (Karatsuba), or [U, V] = [re + j im,
+// re - j im] for a split modulus (c.split; w[2] is then not written)
 template <bool WIDE>
 __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&im)[8],
                                               const ResConst& c, uint32_t (&w)[3][2]) {
@@ -215,12 +217,26 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
     for (int j = 0; j < 4; ++j) {
       tr[j] = res_t<WIDE>(re[4 * half + j], c);
       ti[j] = res_t<WIDE>(im[4 * half + j], c);
-      // (re + im) + h = (tr - h) + (ti - h) + h  (mod p)
-      ts[j] = mod_small(tr[j] + ti[j] + c.sum_k, c);
     }
-    w[0][half] = pack_sym(tr[0], tr[1], tr[2], tr[3], c.h);
-    w[1][half] = pack_sym(ti[0], ti[1], ti[2], ti[3], c.h);
-    w[2][half] = pack_sym(ts[0], ts[1], ts[2], ts[3], c.h);
+    if (c.split) {
+      uint32_t tu[4], tv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // (re + j im) + h = (tr - h) + j (ti - h) + h  (mod p); likewise with p - j
+        tu[j] = mod_small(mad_lo(ti[j], c.gj, tr[j] + c.gku), c);
+        tv[j] = mod_small(mad_lo(ti[j], c.gjn, tr[j] + c.gkv), c);
+      }
+      w[0][half] = pack_sym(tu[0], tu[1], tu[2], tu[3], c.h);
+      w[1][half] = pack_sym(tv[0], tv[1], tv[2], tv[3], c.h);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        // (re + im) + h = (tr - h) + (ti - h) + h  (mod p)
+        ts[j] = mod_small(tr[j] + ti[j] + c.sum_k, c);
+      w[0][half] = pack_sym(tr[0], tr[1], tr[2], tr[3], c.h);
+      w[1][half] = pack_sym(ti[0], ti[1], ti[2], ti[3], c.h);
+      w[2][half] = pack_sym(ts[0], ts[1], ts[2], ts[3], c.h);
+    }
   }
 }
 
@@ -354,8 +370,10 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
         residue_words<false>(vr, vi, c, w);
       int8_t* base = out + int64_t(3 * l) * plane_bytes + goff + soff;
 #pragma unroll
-      for (int pl = 0; pl < 3; ++pl)
+      for (int pl = 0; pl < 2; ++pl)
         *reinterpret_cast<uint2*>(base + pl * plane_bytes) = make_uint2(w[pl][0], w[pl][1]);
+      if (!c.split)
+        *reinterpret_cast<uint2*>(base + 2 * plane_bytes) = make_uint2(w[2][0], w[2][1]);
     } else {
       uint32_t w[3][2];
       if (wide)
@@ -363,13 +381,14 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
       else
         residue_words<false>(vr, vi, c, w);
 #pragma unroll
-      for (int pl = 0; pl < 3; ++pl)
+      for (int pl = 0; pl < 2; ++pl)
         *reinterpret_cast<uint2*>(&stage[pl][soff]) = make_uint2(w[pl][0], w[pl][1]);
+      if (!c.split) *reinterpret_cast<uint2*>(&stage[2][soff]) = make_uint2(w[2][0], w[2][1]);
       __syncthreads();
       int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
       reinterpret_cast<uint4*>(base + cq * plane_bytes)[cs] =
           reinterpret_cast<const uint4*>(stage[cq])[cs];
-      if (cq == 0)
+      if (cq == 0 && !c.split)
         reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
             reinterpret_cast<const uint4*>(stage[2])[cs];
       __syncthreads();

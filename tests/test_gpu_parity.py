@@ -72,7 +72,8 @@ def test_gemm_i8_i32_max_k(crt):
 
 
 # ------------------------------------------------------- K3: Karatsuba mod product
-@pytest.mark.parametrize("p", [256, 255, 251, 239, 199, 173])
+# 241, 233, 197, 173 have a square root of -1: the split (2-product) form
+@pytest.mark.parametrize("p", [256, 255, 251, 241, 239, 233, 199, 197, 173])
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (40, 33, 70), (256, 512, 384), (131, 260, 1000)])
 def test_complex_gemm_mod(crt, p, m, n, k):
     rng = np.random.default_rng(p + m + n + k)
@@ -88,6 +89,45 @@ def test_complex_gemm_mod_hand_case(crt):
     # (1+2i)(3+4i) = -5+10i (reference tests/test_kernel.py:58-66)
     er, ei = crt.complex_gemm_mod([[1]], [[2]], [[3]], [[4]], 251)
     assert int(er[0, 0]) == -5 and int(ei[0, 0]) == 10
+
+
+def test_complex_gemm_mod_split_hand_case(crt):
+    # split modulus 241 (j = 64): (1+2i)(3+4i) = -5+10i, and a sum over k
+    er, ei = crt.complex_gemm_mod([[1]], [[2]], [[3]], [[4]], 241)
+    assert int(er[0, 0]) == -5 and int(ei[0, 0]) == 10
+    ar, ai = np.array([[120, -120]], np.int8), np.array([[-120, 7]], np.int8)
+    br, bi = np.array([[120], [-3]], np.int8), np.array([[120], [-120]], np.int8)
+    er, ei = crt.complex_gemm_mod(ar, ai, br, bi, 241)
+    xr, xi = orc.karatsuba_mod(ar, ai, br, bi, 241)
+    assert np.array_equal(er, xr) and np.array_equal(ei, xi)
+
+
+def test_split_moduli_equal_karatsuba_form(crt, tmp_path):
+    """The split (2-product) form for moduli with sqrt(-1) and the 3-product
+    Karatsuba form give bit-identical results (CRTG_SPLIT=0 forces the latter)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, hashlib, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "import paper_2512_08321_b200 as crt\n"
+        "from oracle import ozaki2 as orc\n"
+        "out = []\n"
+        "for prec, N, mode in (('double', 20, 'fast'), ('double', 16, 'accurate'), ('single', 8, 'fast')):\n"
+        "    a = orc.gen_matrix(300, 700, 1.0, 3, prec); b = orc.gen_matrix(700, 520, 1.0, 4, prec)\n"
+        "    cfg = crt.EmuConfig(precision=prec, domain='complex', mode=mode, num_moduli=N)\n"
+        "    out.append(hashlib.sha256(crt.emulate_gemm_complex(a, b, cfg).tobytes()).hexdigest())\n"
+        "print(' '.join(out))\n")
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, CRTG_SPLIT=flag)
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        res[flag] = r.stdout.strip().split()[-3:]
+    assert res["0"] == res["1"]
 
 
 def test_complex_gemm_mod_full_range_k_cap(crt):
