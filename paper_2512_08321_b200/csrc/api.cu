@@ -234,15 +234,52 @@ bool split_enabled() {
 void make_split(ModConst& mc, ResConst& rc, int p) {
   const int j = sqrt_minus_one(p);
   if (j == 0) return;
-  const int h = p / 2;
   mc.nphase = 2;
   mc.inv2 = uint32_t(inv_mod(2, p));
   mc.inv2j = uint32_t(inv_mod((2 * j) % p, p));
+  const int off = int(rc.off) % p;
   rc.split = 1;
   rc.gj = uint32_t(j);
   rc.gjn = uint32_t(p - j);
-  rc.gku = uint32_t((p - (j * h) % p) % p);
-  rc.gkv = uint32_t((p - ((p - j) * h) % p) % p);
+  rc.gku = uint32_t((p - (j * off) % p) % p);
+  rc.gkv = uint32_t((p - ((p - j) * off) % p) % p);
+}
+
+// residue-kernel constants of modulus p for the stored representative t - off
+ResConst make_res(int p, uint32_t off) {
+  ResConst rc{};
+  const uint64_t P = uint64_t(p);
+  const bool pow2 = (p & (p - 1)) == 0;
+  int sh = 0;
+  while ((2 << sh) <= p) ++sh;  // floor(log2 p)
+  if (pow2) {
+    rc.magic = uint32_t(uint64_t(1) << (32 - sh));  // umulhi(u, 2^(32-s)) = u >> s
+    rc.shift = 0;
+  } else {
+    const unsigned __int128 num = (unsigned __int128)1 << (32 + sh);
+    rc.magic = uint32_t((num + P - 1) / P);
+    rc.shift = sh;
+  }
+  rc.neg_p = uint32_t(-p);
+  rc.off = off;
+  uint32_t cw[6];
+  uint64_t c = 1 % P;
+  for (int i = 0; i < 6; ++i) {
+    cw[i] = uint32_t(c);  // < p <= 256
+    c = (c << 16) % P;
+  }
+  rc.dw0123 = cw[0] | (cw[1] << 8) | (cw[2] << 16) | (cw[3] << 24);
+  rc.dw45 = cw[4] | (cw[5] << 8);
+  auto pow2_mod = [&](int e) {
+    uint64_t t = 1 % P;
+    for (int i = 0; i < e; ++i) t = (t * 2) % P;
+    return t;
+  };
+  const uint64_t o = off % P;
+  rc.k63 = uint32_t((o + P - pow2_mod(63)) % P);
+  rc.kw = uint32_t((o + P - pow2_mod(90)) % P);
+  rc.sum_k = uint32_t((P - o) % P);
+  return rc;
 }
 
 // split = true: moduli with a square root of -1 use the 2-product form (the
@@ -255,34 +292,12 @@ DevConsts make_dev(const crtg_consts& K, bool split = true) {
     const int p = K.moduli[l];
     d.mc[l] = make_mod(p);
     const ModConst& mc = d.mc[l];
-    ResConst& rc = d.rc[l];
-    const uint32_t h = uint32_t(p / 2);
-    const uint32_t c53 = uint32_t((uint64_t(1) << 53) % uint64_t(p));
-    rc.c32 = mc.c32;
-    rc.c16 = mc.c16;
-    rc.h = h;
-    rc.k = uint32_t((h + uint32_t(p) - c53) % uint32_t(p));
-    rc.sum_k = uint32_t(p) - h;
-    rc.magic = mc.magic;
-    rc.shift = mc.is_pow2 ? -1 : mc.shift;  // -1 marks p = 256 (mask)
-    rc.p = p;
-    rc.neg_p = uint32_t(-p);
-    {
-      uint64_t c = 1 % uint64_t(p);
-      uint32_t cw[6];
-      for (int i = 0; i < 6; ++i) {
-        cw[i] = uint32_t(c);  // < p <= 256
-        c = (c << 16) % uint64_t(p);
-      }
-      rc.dn = cw[0] | (cw[1] << 8);
-      rc.dw0123 = cw[0] | (cw[1] << 8) | (cw[2] << 16) | (cw[3] << 24);
-      rc.dw45 = cw[4] | (cw[5] << 8);
-      // 2^90 mod p
-      uint64_t t = 1 % uint64_t(p);
-      for (int i = 0; i < 90; ++i) t = (t * 2) % uint64_t(p);
-      rc.kw = uint32_t((h + uint32_t(p) - uint32_t(t)) % uint32_t(p));
+    d.rc[l] = make_res(p, uint32_t(p / 2));
+    d.rx[l] = make_res(p, 128u);
+    if (split && split_enabled()) {
+      make_split(d.mc[l], d.rc[l], p);
+      make_split(d.mc[l], d.rx[l], p);
     }
-    if (split && split_enabled()) make_split(d.mc[l], rc, p);
     d.coeff_hi[l] = K.coeff_hi[l];
     d.coeff_lo[l] = K.coeff_lo[l];
   }
@@ -784,7 +799,8 @@ int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim, const 
   const int64_t plane = r_pad * k_pad;
   if (ws_bytes < size_t(3 * N) * plane) return fail(CRTG_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const DevConsts dc = make_dev(*K, false);
+  DevConsts dc = make_dev(*K, false);
+  dc.sym = 1;  // the reference's symmetric residues (crt.py:136-151)
   int8_t* packed = static_cast<int8_t*>(ws);
   unsigned long long* ovf = reinterpret_cast<unsigned long long*>(diag) +
                             (operand == 0 ? CRTG_DIAG_OVERFLOW_A : CRTG_DIAG_OVERFLOW_B);
@@ -857,13 +873,14 @@ __global__ void k_mod_sum(const int8_t* __restrict__ x, const int8_t* __restrict
   out[i] = int8_t(to_sym(r, mc));
 }
 
-// split-modulus planes: sym(x + c y mod p)  (U: c = j, V: c = p - j)
+// split-modulus planes x + c y (U: c = j, V: c = p - j) in the pipeline's
+// 128-offset representative ((v + 128) mod p) - 128 in [-128, p - 129]
 __global__ void k_mod_lin(const int8_t* __restrict__ x, const int8_t* __restrict__ y, int c,
                           int64_t count, ModConst mc, int8_t* __restrict__ out) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const uint32_t r = mod_i32(int32_t(x[i]) + c * int32_t(y[i]), mc);
-  out[i] = int8_t(to_sym(r, mc));
+  const uint32_t r = mod_i32(int32_t(x[i]) + c * int32_t(y[i]) + 128, mc);
+  out[i] = int8_t(int32_t(r) - 128);
 }
 }  // namespace
 

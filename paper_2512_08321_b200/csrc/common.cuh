@@ -67,30 +67,34 @@ struct ModConst {
   uint32_t inv2j;    // (2 j)^-1 mod p    (split moduli)
 };
 
-// Residue-kernel constants.  With v = 2^53 + x (x = +-M, M < 2^53) split as
-// v = hi*2^32 + lo_h*2^16 + lo_l, u = hi*c32 + lo_h*c16 + lo_l + k is
-// congruent to x + h (h = floor(p/2)) and below 2^31, so one magic reduction gives
-// t = (x + h) mod p and the symmetric residue is t - h.
+// Residue-kernel constants for one modulus and one stored representative
+// (off = floor(p/2): the symmetric residue t - off; off = 128: t ^ 0x80).
+// A value a' is read as 16-bit limbs of v = a' + 2^63 (four limbs) or 2^90 + a'
+// (six); u = sum_i limb_i * (2^(16 i) mod p) + k is congruent to a' + off and
+// below 2^27, so one magic reduction gives t = (a' + off) mod p.
 struct ResConst {
-  uint32_t c32, c16, k, h, magic, sum_k;  // sum_k = p - h (re + im plane)
-  int32_t shift, p;
-  uint32_t neg_p;                          // (uint32)(-p): t = u + q * neg_p
+  uint32_t magic;   // ceil(2^(32+shift) / p), or 2^(32 - log2 p) with shift 0 for p = 2^s
+  int32_t shift;
+  uint32_t neg_p;   // (uint32)(-p): t = u + q * neg_p
+  uint32_t off;     // floor(p/2) (symmetric) or 128
   // dp2a byte tables (each 2^(16 i) mod p < 256 fits a byte):
-  //  narrow: dn = (1, 2^16 mod p) for the two halves of the low word of 2^53 + a'
-  //  wide (|a'| >= 2^53): v = 2^90 + a' as three words = six 16-bit limbs,
-  //  u = sum_i limb_i * (2^(16 i) mod p) + kw  ==  a' + h  (mod p);
   //  dw0123 = bytes (c0, c16, c32, c48), dw45 = (c64, c80)
-  uint32_t dn, dw0123, dw45, kw;
+  uint32_t dw0123, dw45;
+  uint32_t k63;     // (off - 2^63) mod p
+  uint32_t kw;      // (off - 2^90) mod p
+  uint32_t sum_k;   // (-off) mod p: t_s = (t_re + t_im + sum_k) mod p
   // split moduli (ModConst::nphase == 2): planes U, V instead of re, im, re+im;
-  // t_U = (t_re + j t_im + ku) mod p, t_V = (t_re + (p - j) t_im + kv) mod p
-  // (ku = -j h, kv = j h mod p keep the +h bias of the t form)
+  // t_U = (t_re + j t_im + gku) mod p, t_V = (t_re + (p - j) t_im + gkv) mod p
+  // with gku = (-j off) mod p, gkv = (-(p - j) off) mod p
   uint32_t split, gj, gjn, gku, gkv;
 };
 
 struct DevConsts {
   int32_t n;
   ModConst mc[CRTG_MAX_MODULI];
-  ResConst rc[CRTG_MAX_MODULI];
+  ResConst rc[CRTG_MAX_MODULI];  // symmetric representative
+  ResConst rx[CRTG_MAX_MODULI];  // 128-offset representative (complex pipeline)
+  int32_t sym;                   // 1: the complex pipeline stores symmetric residues too
   double coeff_hi[CRTG_MAX_MODULI];
   double coeff_lo[CRTG_MAX_MODULI];
   double p_hi, p_lo;

@@ -31,12 +31,6 @@ __device__ __forceinline__ DD quick_two_sum(double a, double b) {
   return {s, __dsub_rn(b, __dsub_rn(s, a))};
 }
 
-__device__ __forceinline__ DD split(double a) {
-  const double c = __dmul_rn(134217729.0, a);
-  const double hi = __dsub_rn(c, __dsub_rn(c, a));
-  return {hi, __dsub_rn(a, hi)};
-}
-
 // two_prod(p_hi, z) (ddarith.py:36-44).  Dekker's error term is EXACT here
 // (no overflow, |z| < 2^13, p_hi < 2^1000), so it equals the single-rounding
 // fma(p_hi, z, -p) bit for bit — signed zeros included (z = +-0 gives +0 both
@@ -58,11 +52,29 @@ __device__ __forceinline__ DD dd_add(double ahi, double alo, double bhi, double 
 // z = ceil(q - 0.5) with q = fl(s / p_hi) (crt.py:166-167).  The quotient is
 // formed with the reciprocal; whenever q - 0.5 lies within a few ulps of an
 // integer (where the two roundings could disagree) the exact division is used.
+// |q| < 2^13 here, so rounding to an integer is the 1.5*2^52 magic-number add
+// (two DADDs on the FP64 pipe instead of the slower FRND).
+__device__ __forceinline__ double rint_small(double d) {
+  return __dsub_rn(__dadd_rn(d, 0x1.8p52), 0x1.8p52);
+}
+
+__device__ __forceinline__ double ceil_small(double d) {
+  const double r = rint_small(d);
+  return r < d ? __dadd_rn(r, 1.0) : r;
+}
+
 __device__ __forceinline__ double quotient_z(double s, const DevConsts& dc) {
   const double d = __dsub_rn(__dmul_rn(s, dc.inv_p), 0.5);
-  const double r = rint(d);
-  if (fabs(__dsub_rn(d, r)) > 0x1p-40 * (fabs(d) + 1.0)) return ceil(d);
+  const double r = rint_small(d);
+  if (fabs(__dsub_rn(d, r)) > 0x1p-40 * (fabs(d) + 1.0)) return ceil_small(d);
   return ceil(__dsub_rn(__ddiv_rn(s, dc.p_hi), 0.5));
+}
+
+// residue byte q of a word whose bytes are e + 128 (word ^ 0x80808080) -> (double)e
+// exactly: the bit pattern 0x43300000:(e + 128) is 2^52 + e + 128 (no I2F)
+__device__ __forceinline__ double byte_to_f64(uint32_t wx, int q) {
+  return __dsub_rn(__hiloint2double(0x43300000, int(__byte_perm(wx, 0, 0x4440 + q))),
+                   4503599627370624.0 /* 2^52 + 128 */);
 }
 
 // symmetric_mod_wide (crt.py:154-184), double-double path
@@ -171,16 +183,17 @@ __global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t*
       const int l = l0 + b;
       if (l >= dc.n) break;
       const double cl = dc.coeff_lo[l];
+      const uint32_t xr = wr[b] ^ 0x80808080u, xi = wi[b] ^ 0x80808080u;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int32_t er = int32_t(int8_t(wr[b] >> (8 * q)));
-        const int32_t ei = int32_t(int8_t(wi[b] >> (8 * q)));
+        const double er = byte_to_f64(xr, q);
+        const double ei = REAL ? 0.0 : byte_to_f64(xi, q);
         if constexpr (!LIMBS) {
-          s1r[q] = __dadd_rn(s1r[q], __dmul_rn(dc.coeff_hi[l], double(er)));
-          s1i[q] = __dadd_rn(s1i[q], __dmul_rn(dc.coeff_hi[l], double(ei)));
+          s1r[q] = __dadd_rn(s1r[q], __dmul_rn(dc.coeff_hi[l], er));
+          s1i[q] = __dadd_rn(s1i[q], __dmul_rn(dc.coeff_hi[l], ei));
         }
-        s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, double(er)));
-        if (!REAL) s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, double(ei)));
+        s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, er));
+        if (!REAL) s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, ei));
       }
     }
   }

@@ -105,21 +105,28 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
 // ---------------------------------------------------------------------------
 // Residue kernel.  CTA tile = 16 operand rows x 128 K (one packed K block);
 // thread = 8 consecutive K of one row (16 real values).  Each value is
-// decomposed once into 3 registers; per modulus a value then costs 6 (narrow)
-// or ~15 (wide) integer ops.  Output goes through a 6 KiB smem stage so every
-// global store is a coalesced 16-byte write of a contiguous 2 KiB run of the
-// packed plane.
+// decomposed once into 16-bit limbs; per modulus a value then costs two (or
+// three) dp2a and one magic-number reduction.  A rows store straight to the
+// packed plane; B columns go through a 6 KiB smem stage so every global store
+// is a coalesced 16-byte write of a contiguous 2 KiB run of the packed plane.
+//
+// Stored representative.  SYM = true writes the reference's symmetric residue
+// (crt.py:136-151; the crtg_residues parity hook and the real path, whose
+// int32 overflow check depends on it).  SYM = false (the complex pipeline)
+// writes (a' + 128 mod p) - 128 in [-128, p - 129]: congruent to a', so every
+// modular product and e-plane is unchanged, |value| <= 128 keeps the Karatsuba
+// and split sums within the epilogue's 2^30 bias for k <= 2^16, and the byte is
+// t ^ 0x80 -- one LOP per four values instead of four subtractions.
 // ---------------------------------------------------------------------------
 constexpr int kResRows = 16;
 
-// Value representations, read straight from the IEEE bits:
-//  narrow (|a'| < 2^53): v = 2^53 + a' (< 2^54) as w0 = v >> 32 (22 bits),
-//      w1 = low word; u = dp2a(w1 halves, (1, 2^16 mod p)) + k + w0*(2^32 mod p)
-//      (< 2^31): 2 instructions
-//  wide (some |a'| >= 2^53 in the thread): v = 2^90 + a' (< 2^91) as three words
-//      = six 16-bit limbs; u = sum limb_i*(2^(16i) mod p) + kw (< 2^27) as three
-//      dp2a (16-bit x 8-bit pair dot products): 3 instructions
-// Both give u == a' + floor(p/2) (mod p); one magic reduction -> t in [0,p).
+// Value representations (one truncating conversion per value):
+//  medium (|a'| < 2^63, every warp at N <= 14 and most at N <= 20):
+//      v = a' + 2^63 as (lo, hi) words = four 16-bit limbs;
+//      u = dp2a.hi(hi, c, dp2a.lo(lo, c, k63)) with c = bytes (1, 2^16, 2^32, 2^48 mod p)
+//  wide (some |a'| >= 2^63 in the warp): v = 2^90 + a' as three words = six limbs,
+//      one more dp2a against (2^64, 2^80 mod p)
+// Both give u == a' + off (mod p), u < 2^27; one magic reduction -> t in [0,p).
 struct Val3 {
   uint32_t w0, w1, w2;
 };
@@ -137,14 +144,6 @@ __device__ __forceinline__ void int_parts(double q, uint64_t& M, int& s) {
     M = sig;
     s = e2 - 52;
   }
-}
-
-__device__ __forceinline__ Val3 split_narrow(double q) {
-  uint64_t M;
-  int s;
-  int_parts(q, M, s);
-  const uint64_t v = (q < 0.0) ? (uint64_t(1) << 53) - M : (uint64_t(1) << 53) + M;
-  return {uint32_t(v >> 32), uint32_t(v), 0u};
 }
 
 __device__ __forceinline__ Val3 split_wide(double q) {
@@ -178,10 +177,11 @@ __device__ __forceinline__ uint32_t dp2a_hi(uint32_t a, uint32_t b, uint32_t c) 
   return d;
 }
 
+// u mod p for u < 2^31: q = umulhi(u, magic) >> shift (powers of two: magic =
+// 2^(32 - log2 p), shift 0), t = u - q p -- three instructions, no branch
 __device__ __forceinline__ uint32_t mod_small(uint32_t u, const ResConst& c) {
-  if (c.shift < 0) return u & 0xFFu;
   const uint32_t q = __umulhi(u, c.magic) >> c.shift;
-  return mad_lo(q, c.neg_p, u);  // u - q*p
+  return mad_lo(q, c.neg_p, u);
 }
 
 template <bool WIDE>
@@ -192,22 +192,27 @@ __device__ __forceinline__ uint32_t res_t(const Val3& v, const ResConst& c) {
     u = dp2a_hi(v.w1, c.dw0123, u);
     u = dp2a_lo(v.w2, c.dw45, u);
   } else {
-    u = mad_lo(v.w0, c.c32, dp2a_lo(v.w1, c.dn, c.k));
+    u = dp2a_hi(v.w1, c.dw0123, dp2a_lo(v.w0, c.dw0123, c.k63));
   }
-  return mod_small(u, c);  // t = (a' + h) mod p
+  return mod_small(u, c);  // t = (a' + off) mod p
 }
 
-// 4 values t_i in [0,p) -> packed int8 (t_i - h)
-__device__ __forceinline__ uint32_t pack_sym(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
-                                             uint32_t h) {
-  const uint32_t lo = __byte_perm(a - h, b - h, 0x0040);
-  const uint32_t hi = __byte_perm(c - h, d - h, 0x0040);
-  return __byte_perm(lo, hi, 0x5410);
+// 4 values t_i in [0,p) -> packed int8 (t_i - off)
+template <bool SYM>
+__device__ __forceinline__ uint32_t pack_t(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
+                                           uint32_t off) {
+  if (SYM) {
+    const uint32_t lo = __byte_perm(a - off, b - off, 0x0040);
+    const uint32_t hi = __byte_perm(c - off, d - off, 0x0040);
+    return __byte_perm(lo, hi, 0x5410);
+  }
+  // off = 128: (t - 128) mod 256 == t ^ 0x80 for t < 256
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410) ^ 0x80808080u;
 }
 
 // planes of one modulus: [re, im, re+im] (Karatsuba), or [U, V] = [re + j im,
 // re - j im] for a split modulus (c.split; w[2] is then not written)
-template <bool WIDE>
+template <bool WIDE, bool SYM>
 __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&im)[8],
                                               const ResConst& c, uint32_t (&w)[3][2]) {
 #pragma unroll
@@ -222,26 +227,72 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
       uint32_t tu[4], tv[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        // (re + j im) + h = (tr - h) + j (ti - h) + h  (mod p); likewise with p - j
+        // (re + j im) + off = (tr - off) + j (ti - off) + off  (mod p); likewise with p - j
         tu[j] = mod_small(mad_lo(ti[j], c.gj, tr[j] + c.gku), c);
         tv[j] = mod_small(mad_lo(ti[j], c.gjn, tr[j] + c.gkv), c);
       }
-      w[0][half] = pack_sym(tu[0], tu[1], tu[2], tu[3], c.h);
-      w[1][half] = pack_sym(tv[0], tv[1], tv[2], tv[3], c.h);
+      w[0][half] = pack_t<SYM>(tu[0], tu[1], tu[2], tu[3], c.off);
+      w[1][half] = pack_t<SYM>(tv[0], tv[1], tv[2], tv[3], c.off);
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        // (re + im) + h = (tr - h) + (ti - h) + h  (mod p)
-        ts[j] = mod_small(tr[j] + ti[j] + c.sum_k, c);
-      w[0][half] = pack_sym(tr[0], tr[1], tr[2], tr[3], c.h);
-      w[1][half] = pack_sym(ti[0], ti[1], ti[2], ti[3], c.h);
-      w[2][half] = pack_sym(ts[0], ts[1], ts[2], ts[3], c.h);
+      for (int j = 0; j < 4; ++j) {
+        // (re + im) + off = (tr - off) + (ti - off) + off  (mod p); x < 3p, so two
+        // conditional subtractions on the ALU pipe (umin(x, x - p) wraps below p)
+        // instead of a magic reduction on the busier FMA-heavy pipe
+        const uint32_t x = tr[j] + ti[j] + c.sum_k;
+        const uint32_t y = min(x, x + c.neg_p);
+        ts[j] = min(y, y + c.neg_p);
+      }
+      w[0][half] = pack_t<SYM>(tr[0], tr[1], tr[2], tr[3], c.off);
+      w[1][half] = pack_t<SYM>(ti[0], ti[1], ti[2], ti[3], c.off);
+      w[2][half] = pack_t<SYM>(ts[0], ts[1], ts[2], ts[3], c.off);
     }
   }
 }
 
-template <typename T, int OPERAND, bool REAL>
-__global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, int64_t ldx, int rows,
+// the per-modulus loop of one tile (complex operands)
+template <int OPERAND, bool WIDE, bool SYM>
+__device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&vi)[8],
+                                             const DevConsts& dc, const ResConst* rcs,
+                                             int8_t* __restrict__ out, int64_t plane_bytes,
+                                             int64_t goff, int soff, int cq, int cs,
+                                             uint8_t (*stage)[kResRows * 128]) {
+  for (int l = 0; l < dc.n; ++l) {
+    const ResConst c = rcs[l];
+    uint32_t w[3][2];
+    residue_words<WIDE, SYM>(vr, vi, c, w);
+    if (OPERAND == 0) {
+      // A rows: the 16 lanes of a row cover its whole 128-byte line of the plane,
+      // so a warp store is already two full lines -- no staging needed
+      int8_t* base = out + int64_t(3 * l) * plane_bytes + goff + soff;
+      *reinterpret_cast<uint2*>(base) = make_uint2(w[0][0], w[0][1]);
+      *reinterpret_cast<uint2*>(base + plane_bytes) = make_uint2(w[1][0], w[1][1]);
+      if (!c.split)
+        *reinterpret_cast<uint2*>(base + 2 * plane_bytes) = make_uint2(w[2][0], w[2][1]);
+    } else {
+      *reinterpret_cast<uint2*>(&stage[0][soff]) = make_uint2(w[0][0], w[0][1]);
+      *reinterpret_cast<uint2*>(&stage[1][soff]) = make_uint2(w[1][0], w[1][1]);
+      if (!c.split) *reinterpret_cast<uint2*>(&stage[2][soff]) = make_uint2(w[2][0], w[2][1]);
+      __syncthreads();
+      int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
+      reinterpret_cast<uint4*>(base + cq * plane_bytes)[cs] =
+          reinterpret_cast<const uint4*>(stage[cq])[cs];
+      if (cq == 0 && !c.split)
+        reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
+            reinterpret_cast<const uint4*>(stage[2])[cs];
+      __syncthreads();
+    }
+  }
+}
+
+template <bool WIDE>
+__device__ __forceinline__ uint32_t pack_real(const Val3 (&v)[8], int i0, const ResConst& c) {
+  return pack_t<true>(res_t<WIDE>(v[i0], c), res_t<WIDE>(v[i0 + 1], c), res_t<WIDE>(v[i0 + 2], c),
+                      res_t<WIDE>(v[i0 + 3], c), c.off);
+}
+
+template <typename T, int OPERAND, bool REAL, bool SYM>
+__global__ void __launch_bounds__(256, 4) k_residues(const T* __restrict__ X, int64_t ldx, int rows,
                                                   int kdim, int64_t col0,
                                                   const int32_t* __restrict__ exps,
                                                   const __grid_constant__ DevConsts dc,
@@ -250,6 +301,8 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
                                                   unsigned long long* __restrict__ overflow,
                                                   int n_kb, int n_rt, int row_base) {
   __shared__ __align__(16) uint8_t stage[3][kResRows * 128];
+  // representative of the stored residues: the symmetric (rc) or the 128-offset (rx) tables
+  const ResConst* rcs = SYM ? dc.rc : dc.rx;
   // grid-stride over (K block, 16-row tile): a full grid when launched alone, one
   // CTA per SM when it runs beside the persistent GEMM (side stream)
   for (int tile = blockIdx.x; tile < n_kb * n_rt; tile += gridDim.x) {
@@ -276,7 +329,7 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
   // q = x * 2^e exactly (quantize, scaling.py:277-293); a' = trunc(q)
   double qr[8], qi[8];
   int bad = 0;
-  bool wide = false, huge = false;
+  bool huge = false;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int h = h0 + t;
@@ -290,31 +343,19 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
     qi[t] = __dmul_rn(im, scale);
     if (!(fabs(qr[t]) < 0x1p90)) { bad = 1; qr[t] = 0.0; }
     if (!(fabs(qi[t]) < 0x1p90)) { bad = 1; qi[t] = 0.0; }
-    const double mq = fmax(fabs(qr[t]), fabs(qi[t]));
-    wide |= mq >= 0x1p53;  // (q >= 2^53 is an integer, so this is |trunc q| >= 2^53)
-    huge |= mq >= 0x1p63;
+    huge |= fmax(fabs(qr[t]), fabs(qi[t])) >= 0x1p63;
   }
   // warp-uniform representation (the wide form is valid for every value): a
   // warp that mixed both would execute both per-modulus paths
-  wide = __any_sync(0xffffffffu, wide);
   huge = __any_sync(0xffffffffu, huge);
   Val3 vr[8], vi[8];
   if (!huge) {
-    // |a'| < 2^63: one truncating conversion gives a' as int64; then
-    //   narrow: v = 2^53 + a' -> (v >> 32, low word)
-    //   wide:   2^90 + a' (96-bit) = (lo(a'), hi(a'), 2^26 + sign(a'))
+    // |a'| < 2^63: one truncating conversion gives a' as int64; a' + 2^63 flips the sign bit
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const long long ar = __double2ll_rz(qr[t]), ai = __double2ll_rz(qi[t]);
-      if (wide) {
-        vr[t] = {uint32_t(ar), uint32_t(uint64_t(ar) >> 32), (1u << 26) + uint32_t(ar >> 63)};
-        vi[t] = {uint32_t(ai), uint32_t(uint64_t(ai) >> 32), (1u << 26) + uint32_t(ai >> 63)};
-      } else {
-        const uint64_t wr = uint64_t(ar) + (uint64_t(1) << 53);
-        const uint64_t wi = uint64_t(ai) + (uint64_t(1) << 53);
-        vr[t] = {uint32_t(wr >> 32), uint32_t(wr), 0u};
-        vi[t] = {uint32_t(wi >> 32), uint32_t(wi), 0u};
-      }
+      vr[t] = {uint32_t(ar), uint32_t(uint64_t(ar) >> 32) ^ 0x80000000u, 0u};
+      vi[t] = {uint32_t(ai), uint32_t(uint64_t(ai) >> 32) ^ 0x80000000u, 0u};
     }
   } else {
 #pragma unroll
@@ -334,21 +375,17 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
   const int cq = threadIdx.x >> 7;       // copy-out: plane handled by this half
   const int cs = threadIdx.x & 127;      // 16-byte slot within the 2 KiB run
 
-  for (int l = 0; l < dc.n; ++l) {
-    const ResConst c = dc.rc[l];
-    if constexpr (REAL) {
-      // one plane per modulus (emulate_gemm_real: no imaginary part / Karatsuba sum)
-      uint32_t w0 = 0, w1 = 0;
-      if (wide) {
-        w0 = pack_sym(res_t<true>(vr[0], c), res_t<true>(vr[1], c), res_t<true>(vr[2], c),
-                      res_t<true>(vr[3], c), c.h);
-        w1 = pack_sym(res_t<true>(vr[4], c), res_t<true>(vr[5], c), res_t<true>(vr[6], c),
-                      res_t<true>(vr[7], c), c.h);
+  if constexpr (REAL) {
+    // one plane per modulus (emulate_gemm_real: no imaginary part / Karatsuba sum)
+    for (int l = 0; l < dc.n; ++l) {
+      const ResConst c = dc.rc[l];
+      uint32_t w0, w1;
+      if (huge) {
+        w0 = pack_real<true>(vr, 0, c);
+        w1 = pack_real<true>(vr, 4, c);
       } else {
-        w0 = pack_sym(res_t<false>(vr[0], c), res_t<false>(vr[1], c), res_t<false>(vr[2], c),
-                      res_t<false>(vr[3], c), c.h);
-        w1 = pack_sym(res_t<false>(vr[4], c), res_t<false>(vr[5], c), res_t<false>(vr[6], c),
-                      res_t<false>(vr[7], c), c.h);
+        w0 = pack_real<false>(vr, 0, c);
+        w1 = pack_real<false>(vr, 4, c);
       }
       if (OPERAND == 0) {
         *reinterpret_cast<uint2*>(out + int64_t(l) * plane_bytes + goff + soff) = make_uint2(w0, w1);
@@ -360,39 +397,11 @@ __global__ void __launch_bounds__(256, 3) k_residues(const T* __restrict__ X, in
               reinterpret_cast<const uint4*>(stage[0])[cs];
         __syncthreads();
       }
-    } else if (OPERAND == 0) {
-      // A rows: the 16 lanes of a row cover its whole 128-byte line of the plane,
-      // so a warp store is already two full lines — no staging needed
-      uint32_t w[3][2];
-      if (wide)
-        residue_words<true>(vr, vi, c, w);
-      else
-        residue_words<false>(vr, vi, c, w);
-      int8_t* base = out + int64_t(3 * l) * plane_bytes + goff + soff;
-#pragma unroll
-      for (int pl = 0; pl < 2; ++pl)
-        *reinterpret_cast<uint2*>(base + pl * plane_bytes) = make_uint2(w[pl][0], w[pl][1]);
-      if (!c.split)
-        *reinterpret_cast<uint2*>(base + 2 * plane_bytes) = make_uint2(w[2][0], w[2][1]);
-    } else {
-      uint32_t w[3][2];
-      if (wide)
-        residue_words<true>(vr, vi, c, w);
-      else
-        residue_words<false>(vr, vi, c, w);
-#pragma unroll
-      for (int pl = 0; pl < 2; ++pl)
-        *reinterpret_cast<uint2*>(&stage[pl][soff]) = make_uint2(w[pl][0], w[pl][1]);
-      if (!c.split) *reinterpret_cast<uint2*>(&stage[2][soff]) = make_uint2(w[2][0], w[2][1]);
-      __syncthreads();
-      int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
-      reinterpret_cast<uint4*>(base + cq * plane_bytes)[cs] =
-          reinterpret_cast<const uint4*>(stage[cq])[cs];
-      if (cq == 0 && !c.split)
-        reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
-            reinterpret_cast<const uint4*>(stage[2])[cs];
-      __syncthreads();
     }
+  } else if (huge) {
+    store_moduli<OPERAND, true, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+  } else {
+    store_moduli<OPERAND, false, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   }
   }  // tile loop
 }
@@ -436,9 +445,17 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
     const int n_kb = int((kdim + 127) / 128), n_rt = int((extent + kResRows - 1) / kResRows);
     const int64_t tiles = int64_t(n_kb) * n_rt;
     const unsigned grid = unsigned(max_ctas > 0 && max_ctas < tiles ? max_ctas : tiles);
-    k_residues<T, OP, REAL><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows), int(kdim),
-                                          col0, exps, dc, out, plane_bytes, rb_count, overflow,
-                                          n_kb, n_rt, int(row_base));
+    // symmetric residues for the real path and the parity hook (dc.sym), the
+    // 128-offset representative in the complex pipeline
+    if (REAL || dc.sym)
+      k_residues<T, OP, REAL, true><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),
+                                                        int(kdim), col0, exps, dc, out, plane_bytes,
+                                                        rb_count, overflow, n_kb, n_rt, int(row_base));
+    else
+      k_residues<T, OP, false, false><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),
+                                                          int(kdim), col0, exps, dc, out, plane_bytes,
+                                                          rb_count, overflow, n_kb, n_rt,
+                                                          int(row_base));
   } else {
   // cover every padded row of the plane so the GEMM reads zeros there
   dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kTileRows));

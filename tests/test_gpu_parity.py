@@ -133,14 +133,53 @@ def test_split_moduli_equal_karatsuba_form(crt, tmp_path):
 def test_complex_gemm_mod_full_range_k_cap(crt):
     # extreme residues at the complex k cap: int32 D-E would overflow without
     # reducing D, E, F first (reference kernel.py:46-50)
+    p = 256
     k = 2 ** 16
     ar = np.full((2, k), -128, np.int8)
     ai = np.full((2, k), 127, np.int8)
     br = np.full((k, 256), -128, np.int8)
     bi = np.full((k, 256), -128, np.int8)
-    er, ei = crt.complex_gemm_mod(ar, ai, br, bi, 256)
-    xr, xi = orc.karatsuba_mod(ar, ai, br, bi, 256)
+    er, ei = crt.complex_gemm_mod(ar, ai, br, bi, p)
+    xr, xi = orc.karatsuba_mod(ar, ai, br, bi, p)
     assert np.array_equal(er, xr) and np.array_equal(ei, xi)
+
+
+@pytest.mark.parametrize("p,j", [(241, 64), (173, 80)])
+def test_complex_gemm_mod_split_extreme_k_cap(crt, p, j):
+    # split modulus: U = V = -128 everywhere (re = -128 mod p, im = 0) so both
+    # products reach k * 128^2 = 2^30 at the k cap
+    assert (j * j + 1) % p == 0
+    k = 2 ** 16
+    v = np.int8(p - 128)
+    ar = np.full((3, k), v, np.int8)
+    ai = np.zeros((3, k), np.int8)
+    br = np.full((k, 260), v, np.int8)
+    bi = np.zeros((k, 260), np.int8)
+    bi[5, :] = 3  # break the symmetry a little
+    er, ei = crt.complex_gemm_mod(ar, ai, br, bi, p)
+    xr, xi = orc.karatsuba_mod(ar, ai, br, bi, p)
+    assert np.array_equal(er, xr) and np.array_equal(ei, xi)
+
+
+@pytest.mark.parametrize("N", [15, 20])
+def test_offset_residues_extreme_k_cap(crt, N):
+    """The pipeline stores residues as ((a' + 128) mod p) - 128, so a' = -128 gives
+    -128 in EVERY modulus plane.  With injected exponents 0 and k = 2^16 every
+    Karatsuba / split product reaches k * 128^2 = 2^30.  (The CRT is accurate
+    relative to P, not exact for such a small product, so the check is against
+    the oracle on the same exponents.)"""
+    from paper_2512_08321_b200 import dist
+    k, m, n = 2 ** 16, 2, 3
+    a = np.full((m, k), complex(-128, -128))
+    b = np.full((k, n), complex(-128, -127))
+    b[7, 1] = complex(-128, 5)
+    mu, nu = np.zeros(m, np.int32), np.zeros(n, np.int32)
+    dev = torch.device("cuda")
+    cfg = crt.EmuConfig(precision="double", domain="complex", mode="fast", num_moduli=N)
+    out = dist.tile_with_exponents(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev),
+                                   torch.from_numpy(mu).to(dev), torch.from_numpy(nu).to(dev), cfg)
+    want = orc.emulate_complex_exps(a, b, mu, nu, N, "double")
+    assert out.cpu().numpy().tobytes() == want.tobytes()
 
 
 # ------------------------------------------------------------------ K1: scaling
