@@ -124,6 +124,16 @@ bool pair_enabled() {
   return on;
 }
 
+// Wide 256 x 256 Karatsuba tiles (default); CRTG_GEMM=one selects the
+// 128 x 256 double-buffered kernel
+bool wide_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CRTG_GEMM");
+    return !(v && (std::string(v) == "one" || std::string(v) == "pair"));
+  }();
+  return on;
+}
+
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v && *v ? std::atoi(v) : dflt;
@@ -137,6 +147,8 @@ int run_gemm(int mode, const GemmArgs& g0, cudaStream_t s) {
   g.group_m = group_m;
   if (pair_enabled() && mode != EPI_BOUND && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
     return launch_gemm_pair(mode, g, sm_count(), s);
+  if (wide_enabled() && mode == EPI_KARATSUBA && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
+    return launch_gemm_wide(g, sm_count(), s);
   return launch_gemm(mode, g, sm_count(), s);
 }
 
@@ -856,6 +868,8 @@ int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A, const int
   g.raw = raw;
   g.raw_ld = n_pad;
   g.raw_plane = m * n_pad;
+  g.unsigned_ops = env_int("CRTG_RAW_UNSIGNED", 0);  // experiment knobs (power vs data)
+  g.repeat_mma = env_int("CRTG_RAW_REPEAT", 0);
   CRTG_TRY(run_gemm(EPI_RAW, g, s), "i8 gemm");
   CRTG_TRY(cudaMemcpy2DAsync(C, n * 4, raw, n_pad * 4, n * 4, m, cudaMemcpyDeviceToDevice, s),
            "copy out");

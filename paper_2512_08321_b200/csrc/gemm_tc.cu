@@ -127,7 +127,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = idesc_i8(128, 256);
+    // unsigned operands (bits 7 / 10 clear): residues stored as t in [0, p)
+    const uint32_t idesc = g.unsigned_ops ? idesc_i8(128, 256) & ~((1u << 7) | (1u << 10))
+                                          : idesc_i8(128, 256);
     uint32_t stage = 0, phase = 0, gslot = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm, tn;
@@ -160,6 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
           for (int kk = 0; kk < 4; ++kk) {
             // advance 32 bytes of K inside the 128-byte swizzle atom
             mma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk | sg.accumulate) != 0);
+            if (MODE == EPI_RAW && g.repeat_mma) {
+              // power experiment: a second MMA on operands already in smem --
+              // 1: same A and B, 2: same A / next B slice, 3: next A and B slices
+              const int ka = g.repeat_mma == 3 ? (kk + 1) & 3 : kk;
+              const int kbb = g.repeat_mma >= 2 ? (kk + 1) & 3 : kk;
+              mma_i8(d, ad + 2 * ka, bd + 2 * kbb, idesc, 1);
+            }
           }
           mma_commit(smem_u32(&empty_bar[stage]));  // frees the smem slot when MMAs finish
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -241,7 +250,171 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
   }
 }
 
+// ---------------------------------------------------------------------------
+// Wide-tile Karatsuba / split kernel: 256 x 256 output tile per CTA.
+//
+// The 128 x 256 kernel above pulls 48 KiB from L2 per 128 x 256 x 128 MACs.
+// Measured on B200 (tools/power_data.py, profiles/r01_gemm_reuse_experiment.json):
+// with operands already in shared memory a second MMA costs far less than one
+// whose operands crossed the L2 -> SM network, i.e. the power-capped GEMM pays
+// for L2 -> SMEM bytes, not for MACs alone.  Two M = 128 MMAs that share one
+// 256-column B tile (rows 0-127 -> TMEM columns [0,256), rows 128-255 ->
+// [256,512)) cut that traffic to 64 KiB per 256 x 256 x 128 MACs (-33%), with
+// no peer-SM traffic (the CTA-pair kernel moves the same third over DSMEM).
+// The price: the accumulators fill all 512 TMEM columns, so each segment's
+// epilogue (TMEM -> registers -> bytes, ~2% of a segment) is not overlapped.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr uint32_t kWStageA = 32768;  // 256 rows x 128 B (two packed blocks)
+constexpr uint32_t kWStageB = 32768;  // 256 rows x 128 B
+constexpr uint32_t kWStageBytes = kWStageA + kWStageB;
+constexpr int kWStages = 3;
+constexpr int kWGroupM = 8;  // 256-row tiles per column sweep
+
+__device__ __forceinline__ void decode_tile_w(int t, const GemmArgs& g, int& l, int& tm2,
+                                              int& tn) {
+  const int mt2 = g.mt >> 1;
+  const int per = mt2 * g.nt;
+  l = t / per;
+  const int r = t - l * per;
+  const int G = g.group_m > 0 ? g.group_m : kWGroupM;
+  const int grp = r / (G * g.nt);
+  const int first = grp * G;
+  const int gm = min(G, mt2 - first);
+  const int in = r - grp * G * g.nt;
+  tm2 = first + in % gm + (g.mt0 >> 1);
+  tn = in / gm;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1) k_gemm_w(const __grid_constant__ GemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[kWStages];
+  __shared__ __align__(8) uint64_t empty_bar[kWStages];
+  __shared__ __align__(8) uint64_t tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWStages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    mbar_init(smem_u32(&tfull_bar), 1);
+    mbar_init(smem_u32(&tempty_bar), kEpiThreads);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(&tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const int total = g.nl * (g.mt >> 1) * g.nt;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer: A rows [256 tm2, +256) and B rows [256 tn, +256) ----------------
+    uint32_t stage = 0, phase = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int l, tm2, tn;
+      decode_tile_w(t, g, l, tm2, tn);
+      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
+      for (int s = 0; s < nseg; ++s) {
+        const int8_t* a = g.a + (int64_t)(l * g.planes_per_l + s) * g.a_plane;
+        const int8_t* b = g.b + (int64_t)(l * g.planes_per_l + s) * g.b_plane;
+        for (int kb = 0; kb < g.kb; ++kb) {
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+          const uint32_t fb = smem_u32(&full_bar[stage]);
+          const uint32_t sa = smem_base + stage * kWStageBytes;
+          mbar_expect_tx(fb, kWStageBytes);
+          bulk_g2s(sa, a + ((int64_t)kb * g.a_rb + 2 * tm2) * kBlockBytes, kWStageA, fb);
+          bulk_g2s(sa + kWStageA, b + ((int64_t)kb * g.b_rb + 2 * tn) * kBlockBytes, kWStageB, fb);
+          if (++stage == kWStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer: two M=128 MMAs per K step share the B tile ----------------
+    const uint32_t idesc = idesc_i8(128, 256);
+    uint32_t stage = 0, phase = 0, gslot = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int l, tm2, tn;
+      decode_tile_w(t, g, l, tm2, tn);
+      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
+      for (int s = 0; s < nseg; ++s) {
+        mbar_wait(smem_u32(&tempty_bar), (gslot & 1) ^ 1);  // epilogue drained both halves
+        tc_fence_after();
+        for (int kb = 0; kb < g.kb; ++kb) {
+          mbar_wait(smem_u32(&full_bar[stage]), phase);
+          tc_fence_after();
+          const uint32_t sa = smem_base + stage * kWStageBytes;
+          const uint64_t a0 = smem_desc_sw128(sa);
+          const uint64_t a1 = smem_desc_sw128(sa + kWStageA / 2);
+          const uint64_t bd = smem_desc_sw128(sa + kWStageA);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t acc = (kb | kk) != 0;
+            mma_i8(tmem, a0 + 2 * kk, bd + 2 * kk, idesc, acc);
+            mma_i8(tmem + 256, a1 + 2 * kk, bd + 2 * kk, idesc, acc);
+          }
+          mma_commit(smem_u32(&empty_bar[stage]));
+          if (++stage == kWStages) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(smem_u32(&tfull_bar));
+        ++gslot;
+      }
+    }
+  } else if (warp >= 4) {
+    // ------- epilogue: 8 warps, lane quarter warp % 4, row half (warp - 4) / 4, 256 columns -------
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const uint32_t lane_addr = tmem + (uint32_t(32 * q) << 16) + uint32_t(256 * half);
+    uint32_t gslot = 0;
+    uint32_t st[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) st[i] = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int l, tm2, tn;
+      decode_tile_w(t, g, l, tm2, tn);
+      const int row = tm2 * 256 + 128 * half + 32 * q + lane;
+      const bool row_ok = row < g.m;
+      const int col_base = tn * 256;
+      const ModConst mc = g.mc[l];
+      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
+      for (int s = 0; s < nseg; ++s) {
+        mbar_wait(smem_u32(&tfull_bar), gslot & 1);
+        tc_fence_after();
+        epilogue_phase<EPI_KARATSUBA, 8>(g, lane_addr, s, l, row, row_ok, col_base, mc, st);
+        tc_fence_before();
+        mbar_arrive(smem_u32(&tempty_bar));
+        ++gslot;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<kTmemCols>(tmem);
+  }
+}
+
 size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + 1024; }
+
+int launch_gemm_wide(const GemmArgs& g, int num_sms, cudaStream_t stream) {
+  const int total = g.nl * (g.mt >> 1) * g.nt;
+  if (total <= 0) return 0;
+  const int grid = total < num_sms ? total : num_sms;
+  const size_t smem = size_t(kWStages) * kWStageBytes + 1024;
+  const cudaError_t err =
+      cudaFuncSetAttribute(k_gemm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (err != cudaSuccess) return int(err);
+  k_gemm_w<<<grid, kThreads, smem, stream>>>(g);
+  return launched(1);
+}
 
 int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {
   const int total = g.nl * g.mt * g.nt;
