@@ -290,12 +290,16 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     flops_step = 8.0 * a.m * a.n * a.k * world
     value = flops_step / (ms_step * 1e-3) / 1e12
 
-    # roofline of the dominant kernel (K3 tcgen05 GEMM): algorithmic INT8 ops per
-    # launch = 6 * N * m * n_block * k (3 GEMMs x 2 ops/MAC x N moduli)
+    # roofline of the dominant kernel (K3 tcgen05 GEMM): INT8 ops the tensor
+    # cores execute per launch = 2 * m * n_block * k * sum_l products_l, with 3
+    # products per modulus (Karatsuba) or 2 for a modulus with a square root of
+    # -1 (split form); the reference's perf model counts 6 * N * mnk
     bf16, bf16_sus, hbm, src = peaks()
     launches_gemm = max(1, stage_n["gemm"])
     gemm_ms = stage_ms["gemm"] / launches_gemm
-    ops_launch = 6.0 * a.moduli * a.m * a.n * a.k * a.steps / launches_gemm
+    prods = sum(crt.moduli.products_per_modulus(crt.select_moduli(a.moduli)))
+    ops_launch = 2.0 * prods * a.m * a.n * a.k * a.steps / launches_gemm
+    ops_model = 6.0 * a.moduli * a.m * a.n * a.k * a.steps / launches_gemm
     achieved = ops_launch / (gemm_ms * 1e-3) / 1e12
     # K3 runs inside a long, power-capped step -> the SUSTAINED figure is the
     # denominator (B200 dense INT8 rate = 2 x dense BF16)
@@ -304,13 +308,18 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     if traffic and [traffic.get(k) for k in ("m", "n", "k", "N", "n_block", "mode")] != \
             [a.m, a.n, a.k, a.moduli, a.n_block, a.mode]:
         traffic = None  # the committed capture is for another configuration
-    roof = {"bound": "tensor", "kernel": "k_gemm_i8<EPI_KARATSUBA>", "achieved": achieved,
+    roof = {"bound": "tensor", "kernel": "k_gemm_w (256x256 Karatsuba/split tiles)",
+            "achieved": achieved,
             "peak": peak_int8, "unit": "TOPS", "frac": achieved / peak_int8,
             "peak_note": f"INT8 dense = 2 x {src} SUSTAINED bf16 ({bf16_sus} TF/s, "
                          f"MEASURED_PEAKS.json; kernel timed inside a long step); burst 2 x {bf16}; "
                          "spec 4500",
             "frac_of_burst": achieved / (2.0 * bf16), "frac_of_spec": achieved / 4500.0,
             "ops_per_launch": ops_launch, "ms_per_launch": gemm_ms,
+            "int8_products_per_step": prods,
+            "ops_note": f"executed INT8 ops: {prods} products of m x n_block x k per launch "
+                        f"(3N = {3 * a.moduli} Karatsuba, minus one per split modulus); the "
+                        f"reference model's 6*N*mnk = {ops_model:.4g} per launch",
             "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
             "traffic_note": traffic.get("config") if traffic else None}
     stages = {k: v / a.steps for k, v in stage_ms.items()}

@@ -147,8 +147,11 @@ int run_gemm(int mode, const GemmArgs& g0, cudaStream_t s) {
   g.group_m = group_m;
   if (pair_enabled() && mode != EPI_BOUND && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
     return launch_gemm_pair(mode, g, sm_count(), s);
-  if (wide_enabled() && mode == EPI_KARATSUBA && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
+  static const bool mc = env_int("CRTG_MC", 0) != 0;
+  if (wide_enabled() && mode == EPI_KARATSUBA && (g.mt % 2) == 0 && (g.mt0 % 2) == 0) {
+    if (mc && (g.nt % 2) == 0) return launch_gemm_wide_mc(g, sm_count(), s);
     return launch_gemm_wide(g, sm_count(), s);
+  }
   return launch_gemm(mode, g, sm_count(), s);
 }
 

@@ -77,6 +77,21 @@ def select_moduli(num_moduli: int) -> ModulusSet:
     return ModulusSet.from_moduli(chosen)
 
 
+def has_sqrt_minus_one(p: int) -> bool:
+    """True when some j has j^2 == -1 (mod p): Z[i]/p splits and the library
+    forms a complex product mod p from two INT8 products instead of three
+    (the e-planes are identical either way)."""
+    return p % 2 == 1 and any((j * j + 1) % p == 0 for j in range(1, p))
+
+
+def products_per_modulus(ms: "ModulusSet") -> list:
+    """INT8 products the GPU runs per modulus in the complex pipeline: 2 for a
+    split modulus, 3 (Karatsuba) otherwise; CRTG_SPLIT=0 forces 3."""
+    import os
+    split_on = os.environ.get("CRTG_SPLIT", "1") != "0"
+    return [2 if split_on and has_sqrt_minus_one(int(p)) else 3 for p in ms.moduli]
+
+
 def _f32_down(y: float) -> np.float32:
     r = np.float32(y)
     return np.nextafter(r, np.float32(-np.inf)) if float(r) > y else r
