@@ -1108,59 +1108,51 @@ cudaStream_t copy_stream(int which) {
 }
 }  // namespace
 
-// host-entry chunking: A in row chunks (multiples of 128 rows), B in column
-// blocks, so the first GEMM starts once one chunk of each has arrived
+// host-entry pieces: A in row chunks, B in column blocks (multiples of 256)
 struct HostChunks {
   int64_t rows;  // rows per A chunk
-  int64_t cols;  // columns per B block (= plan nb)
+  int64_t cols;  // columns per B block
 };
 
-// Staircase streaming: A in row chunks and B in column blocks of about 1/8 of
-// the matrix each, transferred interleaved (A0 B0 A1 B1 ...).  After the first
-// pair lands, every new piece releases a whole row or column of output tiles,
-// so the GPU runs back to back while the rest of the inputs stream in; the last
-// piece leaves only 1/8 of a row of tiles to compute after the final transfer.
+// Staircase streaming: A in row chunks and B in column blocks of about 1/16 of
+// the matrix each, transferred interleaved (A0 B0 A1 B1 ...).  Every piece that
+// lands releases a whole strip of output tiles (A_t: rows of chunk t x blocks
+// 0..t-1; B_t: chunks 0..t x block t), computed as ONE GEMM launch over the
+// strip.  With f of both operands resident only f^2 of the product can run, so
+// the wall time is bounded below by max_f [f T_x + (1 - f^2) T_c]; finer pieces
+// approach that bound (8 -> 16 pieces: ~5 ms at 16384^3, tools/e2e_profile.py).
 HostChunks host_chunks(const Plan& P) {
-  HostChunks h;
-  h.rows = P.m >= 4096 ? round_up((P.m + 7) / 8, 256) : P.m;
-  h.cols = P.nb;
-  return h;
+  auto piece = [](int64_t x) {
+    return x >= 4096 ? round_up((x + 15) / 16, 256) : round_up(x, 256);
+  };
+  return HostChunks{piece(P.m), piece(P.n)};
 }
 
+// one plan over the whole product: B's packed planes and the e-planes span all n
 Plan host_plan(int mode, int64_t m, int64_t n, int64_t k, int N, int64_t n_block) {
-  int64_t nb = n_block < 1 ? n : n_block;
-  if (n >= 4096) nb = std::min(nb, std::max<int64_t>(512, round_up((n + 7) / 8, 256)));
-  return make_plan(mode, m, n, k, N, nb);
+  (void)n_block;  // the strips bound the working set; results are bitwise invariant
+  return make_plan(mode, m, n, k, N, round_up(std::max<int64_t>(n, 1), 256));
 }
 
 namespace {
 int load_tree(const Plan& P, void* ws, cudaStream_t s, PwTree& tree);  // below
 }  // namespace
 
-// bytes of the packed B residues of every column block (all stay resident)
-size_t host_bpack_bytes(const Plan& P) {
-  const int64_t nblk = (P.n + P.nb - 1) / P.nb;
-  return size_t(nblk) * size_t(3 * P.N) * size_t(P.nb_pad) * size_t(P.k_pad);
-}
-
 extern "C" size_t crtg_host_workspace_size(int precision, int mode, int64_t m, int64_t n,
                                            int64_t k, int num_moduli, int64_t n_block) {
   const Plan P = host_plan(mode, m, n, k, num_moduli, n_block);
-  const HostChunks hc = host_chunks(P);
   const size_t esz = (precision & CRTG_IN_C64) ? 8 : 16;
   const size_t csz = (precision & CRTG_SINGLE) ? 8 : 16;
   auto r = [](size_t x) { return (x + 255) & ~size_t(255); };
-  return P.total + r(size_t(m) * k * esz) + r(size_t(k) * n * esz) +
-         2 * r(size_t(hc.rows) * P.nb * csz) + r(host_bpack_bytes(P));
+  return P.total + r(size_t(m) * k * esz) + r(size_t(k) * n * esz) + r(size_t(m) * n * csz);
 }
 
-// End-to-end entry on HOST buffers (pinned for full overlap).  Transfers are
-// ordered A_0, B_0, A_1 .. A_last, B_1 .. B_last on a copy-engine stream; the
-// GEMM of tile (A chunk i, B block j) starts as soon as both are resident and
-// each finished C tile goes back on a second copy stream while the next tile
-// computes.  Fast mode computes the statistics per chunk/block (they are row /
-// column local); accurate mode needs every bound maximum first and so waits for
-// all inputs before its exponents.
+// End-to-end entry on HOST buffers (pinned for full overlap).  Transfers run
+// A_0, B_0, A_1, B_1, ... on a copy-engine stream; each landed piece gets its
+// statistics (fast mode) and residues, then the strip of output tiles it
+// completes runs as one GEMM + CRT, and the strip of C goes back on a second
+// copy stream while the next strip computes.  Accurate mode needs every bound
+// maximum first and so waits for all inputs before its exponents.
 extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_t n, int64_t k,
                                       const void* A, int64_t lda, const void* B, int64_t ldb,
                                       void* C, int64_t ldc, const crtg_consts* K, int64_t n_block,
@@ -1180,12 +1172,12 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   cudaStream_t h2d = copy_stream(0), d2h = copy_stream(1);
   const bool in32 = (precision & CRTG_IN_C64) != 0;
   const bool single = (precision & CRTG_SINGLE) != 0;
+  const int elem = in32 ? E_C64 : E_C128;
   const size_t esz = in32 ? 8 : 16, csz = single ? 8 : 16;
   auto r = [](size_t x) { return (x + 255) & ~size_t(255); };
   char* dA = static_cast<char*>(ws) + P.total;
   char* dB = dA + r(size_t(m) * k * esz);
-  char* dC = dB + r(size_t(k) * n * esz);
-  const size_t cbuf = r(size_t(hc.rows) * P.nb * csz);
+  char* dC = dB + r(size_t(k) * n * esz);  // m x n, row-major (ld n)
   unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
                                 : at<unsigned long long>(ws, P.diag);
   const DevConsts dc = make_dev(*K);
@@ -1198,8 +1190,8 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   CRTG_TRY(cudaStreamWaitEvent(d2h, ev0, 0), "wait");
 
   const int64_t nrc = (m + hc.rows - 1) / hc.rows;
-  const int64_t nblk = (n + P.nb - 1) / P.nb;
-  std::vector<cudaEvent_t> evA(nrc), evB(nblk);
+  const int64_t ncb = (n + hc.cols - 1) / hc.cols;
+  std::vector<cudaEvent_t> evA(nrc), evB(ncb);
   auto copy_a = [&](int64_t i) -> int {
     const int64_t i0 = i * hc.rows, h = std::min(hc.rows, m - i0);
     CRTG_TRY(cudaMemcpy2DAsync(dA + size_t(i0) * k * esz, k * esz,
@@ -1210,7 +1202,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     return int(cudaEventRecord(evA[i], h2d));
   };
   auto copy_b = [&](int64_t j) -> int {
-    const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0);
+    const int64_t j0 = j * hc.cols, w = std::min(hc.cols, n - j0);
     CRTG_TRY(cudaMemcpy2DAsync(dB + j0 * esz, n * esz, static_cast<const char*>(B) + j0 * esz,
                                ldb * esz, w * esz, k, cudaMemcpyHostToDevice, h2d),
              "H2D B");
@@ -1218,17 +1210,10 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     return int(cudaEventRecord(evB[j], h2d));
   };
   // transfer order: A0 B0 A1 B1 ... (the longer list's tail last)
-  for (int64_t t = 0; t < std::max(nrc, nblk); ++t) {
+  const int64_t npieces = std::max(nrc, ncb);
+  for (int64_t t = 0; t < npieces; ++t) {
     if (t < nrc) CRTG_TRY(copy_a(t), "record");
-    if (t < nblk) CRTG_TRY(copy_b(t), "record");
-  }
-  // tile order: as pieces land (fast mode); accurate mode has all inputs first
-  std::vector<std::pair<int64_t, int64_t>> order;
-  for (int64_t t = 0; t < std::max(nrc, nblk); ++t) {
-    if (t < nrc)
-      for (int64_t j = 0; j < std::min(t, nblk); ++j) order.push_back({t, j});
-    if (t < nblk)
-      for (int64_t i = 0; i <= std::min(t, nrc - 1); ++i) order.push_back({i, t});
+    if (t < ncb) CRTG_TRY(copy_b(t), "record");
   }
 
   int32_t* mu = at<int32_t>(ws, P.mu);
@@ -1236,101 +1221,113 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   PwTree tree{};
   if (mode == CRTG_ACCURATE) {
     CRTG_TRY(cudaStreamWaitEvent(s, evA[nrc - 1], 0), "wait");
-    CRTG_TRY(cudaStreamWaitEvent(s, evB[nblk - 1], 0), "wait");
+    CRTG_TRY(cudaStreamWaitEvent(s, evB[ncb - 1], 0), "wait");
     if (int e = run_scaling(P, precision, mode, dA, k, dB, n, dc, ws, dg, s, s)) return e;
   } else {
     if (int e = load_tree(P, ws, s, tree)) return e;
   }
-  const int64_t a_plane = P.m_pad * P.k_pad;
-  const int64_t bblk = int64_t(3 * N) * P.nb_pad * P.k_pad;  // packed bytes per B block
+  const int64_t a_plane = P.m_pad * P.k_pad, b_plane = P.n_pad * P.k_pad;
   int8_t* apack = at<int8_t>(ws, P.a_pack);
-  int8_t* bpack = reinterpret_cast<int8_t*>(dC + 2 * cbuf);
-  std::vector<char> a_done(nrc, 0), b_done(nblk, 0);
-  std::vector<cudaEvent_t> evD;
-  int64_t tile = 0;
-  for (const auto& ij : order) {
-    const int64_t i = ij.first, j = ij.second;
+  int8_t* bpack = at<int8_t>(ws, P.b_pack);
+  int8_t* ere = at<int8_t>(ws, P.e_re);
+  int8_t* eim = at<int8_t>(ws, P.e_im);
+
+  auto piece_a = [&](int64_t i) -> int {  // A chunk i: statistics (fast) and residues
     const int64_t i0 = i * hc.rows, h = std::min(hc.rows, m - i0);
-    const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
-    const bool last_rows = i == nrc - 1;
-    int8_t* bpj = bpack + j * bblk;
-    if (!a_done[i]) {  // A chunk i: statistics (fast) and residues, once
-      a_done[i] = 1;
-      CRTG_TRY(cudaStreamWaitEvent(s, evA[i], 0), "wait");
-      const char* Ai = dA + size_t(i0) * k * esz;
-      if (mode == CRTG_FAST) {
-        StageTimer timer(CRTG_STAGE_SCALING, s);
-        CRTG_TRY(launch_row_stats(in32 ? E_C64 : E_C128, true, Ai, k, h, k, tree, dc.p_fast,
-                                  dc.delta, mu + i0, at<double>(ws, P.rowabs) + i0, dg, s),
-                 "row stats");
-      }
-      StageTimer timer(CRTG_STAGE_RESIDUE_A, s);
-      CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 0, PACK_RESIDUE, Ai, k, h, k, 0, mu + i0, dc,
-                           apack, a_plane, P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s, 0, i0,
-                           last_rows ? P.m_pad - i0 : h),
-               "residues A");
+    CRTG_TRY(cudaStreamWaitEvent(s, evA[i], 0), "wait");
+    const char* Ai = dA + size_t(i0) * k * esz;
+    if (mode == CRTG_FAST) {
+      StageTimer timer(CRTG_STAGE_SCALING, s);
+      CRTG_TRY(launch_row_stats(elem, true, Ai, k, h, k, tree, dc.p_fast, dc.delta, mu + i0,
+                                at<double>(ws, P.rowabs) + i0, dg, s),
+               "row stats");
     }
-    if (!b_done[j]) {  // B block j: statistics (fast) and residues, once
-      b_done[j] = 1;
-      CRTG_TRY(cudaStreamWaitEvent(s, evB[j], 0), "wait");
-      if (mode == CRTG_FAST) {
-        StageTimer timer(CRTG_STAGE_SCALING, s);
-        const char* Bj = dB + j0 * esz;
-        double* cabs = at<double>(ws, P.colabs) + j0;
-        CRTG_TRY(launch_col_fast(in32 ? E_C64 : E_C128, Bj, n, k, w, cabs,
-                                 at<double>(ws, P.colsq) + 2 * j0, dc.p_fast, dc.delta, nu + j0,
-                                 dg, s),
-                 "col stats");
-      }
-      StageTimer timer(CRTG_STAGE_RESIDUE_B, s);
-      CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 1, PACK_RESIDUE, dB, n, w, k, j0, nu + j0, dc,
-                           bpj, w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s),
-               "residues B");
+    StageTimer timer(CRTG_STAGE_RESIDUE_A, s);
+    CRTG_TRY(launch_pack(elem, 0, PACK_RESIDUE, Ai, k, h, k, 0, mu + i0, dc, apack, a_plane,
+                         P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s, 0, i0,
+                         i == nrc - 1 ? P.m_pad - i0 : h),
+             "residues A");
+    return CRTG_OK;
+  };
+  auto piece_b = [&](int64_t j) -> int {  // B block j: statistics (fast) and residues
+    const int64_t j0 = j * hc.cols, w = std::min(hc.cols, n - j0);
+    CRTG_TRY(cudaStreamWaitEvent(s, evB[j], 0), "wait");
+    if (mode == CRTG_FAST) {
+      StageTimer timer(CRTG_STAGE_SCALING, s);
+      CRTG_TRY(launch_col_fast(elem, dB + j0 * esz, n, k, w, at<double>(ws, P.colabs) + j0,
+                               at<double>(ws, P.colsq) + 2 * j0, dc.p_fast, dc.delta, nu + j0,
+                               dg, s),
+               "col stats");
     }
+    StageTimer timer(CRTG_STAGE_RESIDUE_B, s);
+    CRTG_TRY(launch_pack(elem, 1, PACK_RESIDUE, dB, n, w, k, j0, nu + j0, dc, bpack, b_plane,
+                         P.n_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, s, 0, j0,
+                         j == ncb - 1 ? P.n_pad - j0 : w),
+             "residues B");
+    return CRTG_OK;
+  };
+  // output strip rows [r0, r1) x columns [c0, c1): one GEMM launch, one CRT, one D2H
+  auto strip = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
     GemmArgs g{};
     g.a = apack;
-    g.b = bpj;
+    g.b = bpack;
     g.a_plane = a_plane;
-    g.b_plane = w_pad * P.k_pad;
+    g.b_plane = b_plane;
     g.a_rb = int(P.m_pad / 128);
-    g.b_rb = int(w_pad / 128);
-    g.mt0 = int(i0 / 128);
-    g.mt = int((last_rows ? P.m_pad - i0 : h) / 128);
-    g.nt = int(w_pad / 256);
+    g.b_rb = int(P.n_pad / 128);
+    g.mt0 = int(r0 / 128);
+    g.mt = int((std::min(round_up(r1, 256), P.m_pad) - r0) / 128);
+    g.nt0 = int(c0 / 256);
+    g.nt = int((std::min(round_up(c1, 256), P.n_pad) - c0) / 256);
     g.kb = int(P.k_pad / 128);
     g.nl = N;
     g.planes_per_l = 3;
     g.nphase = 3;
-    g.m = int(i0 + h);
-    g.n = int(w);
-    g.e_re = at<int8_t>(ws, P.e_re);
-    g.e_im = at<int8_t>(ws, P.e_im);
-    g.e_ld = P.nb_pad;
-    g.e_plane = m * P.nb_pad;
+    g.m = int(r1);
+    g.n = int(c1);
+    g.e_re = ere;
+    g.e_im = eim;
+    g.e_ld = P.n_pad;
+    g.e_plane = m * P.n_pad;
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
     {
       StageTimer timer(CRTG_STAGE_GEMM, s);
       CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
     }
-    if (tile >= 2) CRTG_TRY(cudaStreamWaitEvent(s, evD[tile - 2], 0), "wait");
-    char* cblk = dC + (tile & 1) * cbuf;
+    char* cst = dC + (size_t(r0) * n + c0) * csz;
     {
       StageTimer timer(CRTG_STAGE_CRT, s);
-      CRTG_TRY(launch_crt(single, false, h, w, g.e_re + i0 * g.e_ld, g.e_im + i0 * g.e_ld,
-                          g.e_plane, g.e_ld, mu + i0, nu + j0, dc, cblk, w, s),
+      CRTG_TRY(launch_crt(single, false, r1 - r0, c1 - c0, ere + r0 * P.n_pad + c0,
+                          eim + r0 * P.n_pad + c0, g.e_plane, g.e_ld, mu + r0, nu + c0, dc, cst, n,
+                          s),
                "crt");
     }
     cudaEvent_t evC = E.get();
     CRTG_TRY(cudaEventRecord(evC, s), "record");
     CRTG_TRY(cudaStreamWaitEvent(d2h, evC, 0), "wait");
-    CRTG_TRY(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(i0) * ldc + j0) * csz, ldc * csz,
-                               cblk, w * csz, w * csz, h, cudaMemcpyDeviceToHost, d2h),
+    CRTG_TRY(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(r0) * ldc + c0) * csz, ldc * csz,
+                               cst, n * csz, (c1 - c0) * csz, r1 - r0, cudaMemcpyDeviceToHost, d2h),
              "D2H C");
-    evD.push_back(E.get());
-    CRTG_TRY(cudaEventRecord(evD.back(), d2h), "record");
-    ++tile;
+    return CRTG_OK;
+  };
+  for (int64_t t = 0; t < npieces; ++t) {
+    if (t < nrc) {  // A_t: rows of chunk t x every block already resident
+      CRTG_TRY(piece_a(t), "piece A");
+      const int64_t jb = std::min(t, ncb);
+      if (jb > 0)
+        CRTG_TRY(strip(t * hc.rows, std::min((t + 1) * hc.rows, m), 0, std::min(jb * hc.cols, n)),
+                 "strip");
+    }
+    if (t < ncb) {  // B_t: every resident chunk x block t
+      CRTG_TRY(piece_b(t), "piece B");
+      const int64_t ib = std::min(t + 1, nrc);
+      CRTG_TRY(strip(0, std::min(ib * hc.rows, m), t * hc.cols, std::min((t + 1) * hc.cols, n)),
+               "strip");
+    }
   }
-  CRTG_TRY(cudaStreamWaitEvent(s, evD.back(), 0), "wait");
+  cudaEvent_t evD = E.get();
+  CRTG_TRY(cudaEventRecord(evD, d2h), "record");
+  CRTG_TRY(cudaStreamWaitEvent(s, evD, 0), "wait");
   if (sync_check) return check_diag(dg, s);
   return CRTG_OK;
 }

@@ -55,7 +55,7 @@ __device__ __forceinline__ void decode_pair(int t, const GemmArgs& g, int& l, in
   const int gm = min(kPGroupM, mt2 - first);
   const int in = r - grp * kPGroupM * g.nt;
   tm2 = first + in % gm + (g.mt0 >> 1);
-  tn = in / gm;
+  tn = in / gm + g.nt0;
 }
 
 }  // namespace

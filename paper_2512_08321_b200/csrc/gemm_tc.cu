@@ -65,7 +65,7 @@ __device__ __forceinline__ void decode_tile(int t, const GemmArgs& g, int& l, in
   const int gm = min(G, g.mt - first);
   const int in = r - grp * G * g.nt;
   tm = first + in % gm + g.mt0;
-  tn = in / gm;
+  tn = in / gm + g.nt0;
 }
 
 }  // namespace
@@ -283,7 +283,7 @@ __device__ __forceinline__ void decode_tile_w(int t, const GemmArgs& g, int& l, 
   const int gm = min(G, mt2 - first);
   const int in = r - grp * G * g.nt;
   tm2 = first + in % gm + (g.mt0 >> 1);
-  tn = in / gm;
+  tn = in / gm + g.nt0;
 }
 }  // namespace
 
@@ -440,6 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   // pair tiles: (l, tm2, column pair); CTA rank r takes column tile 2 * pair + r
   GemmArgs gp = g;
   gp.nt = g.nt >> 1;
+  gp.nt0 = 0;
   const int total = g.nl * (g.mt >> 1) * gp.nt;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
@@ -448,7 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int t = cid; t < total; t += ncl) {
       int l, tm2, tp;
       decode_tile_w(t, gp, l, tm2, tp);
-      const int tn = 2 * tp + int(rank);
+      const int tn = 2 * tp + int(rank) + g.nt0;
       const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const int8_t* a = g.a + (int64_t)(l * g.planes_per_l + s) * g.a_plane;
@@ -510,7 +511,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       decode_tile_w(t, gp, l, tm2, tp);
       const int row = tm2 * 256 + 128 * half + 32 * q + lane;
       const bool row_ok = row < g.m;
-      const int col_base = (2 * tp + int(rank)) * 256;
+      const int col_base = (2 * tp + int(rank) + g.nt0) * 256;
       const ModConst mc = g.mc[l];
       const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
       for (int s = 0; s < nseg; ++s) {

@@ -17,6 +17,7 @@ struct GemmArgs {
   int a_rb, b_rb;    // 128-row blocks per plane
   int mt, nt, kb;    // 128-row tiles, 256-col tiles, 128-byte K blocks
   int mt0;           // first 128-row tile of this launch (row-chunked launches)
+  int nt0;           // first 256-column tile of this launch (column strips)
   int nl;            // moduli handled by this launch
   int planes_per_l;  // planes per modulus (3 = re, im, re+im)
   int nphase;        // segments per tile for KARATSUBA (3) / RAW (1..3)

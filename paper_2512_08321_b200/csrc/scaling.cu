@@ -382,28 +382,56 @@ __global__ void __launch_bounds__(128) k_col_stats(const T* __restrict__ B, int6
 
 #pragma unroll
   for (int st = 0; st < kColS - 1; ++st) issue(st);
+  // warp 0 runs the 32 order-dependent sum chains (numpy's sequential axis-0
+  // order) and nothing else, so each row costs it one load, one DMUL and the
+  // DADD on the chain; warps 1-3 take the order-free statistics (absmax,
+  // smallest nonzero, finiteness) of the same stage rows in parallel
+  __shared__ double red_mx[3][32], red_mn[3][32];
+  __shared__ int red_bad[3][32];
   double sum = 0.0, mx = 0.0, mn = INFINITY;
   int bad = 0;
   const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   for (int st = 0; st < nst; ++st) {
     issue(st + kColS - 1);
     cp_async_wait<kColS - 1>();
     __syncthreads();
-    if (threadIdx.x < 32) {
-      const T* seg = reinterpret_cast<const T*>(ring + (st % kColS) * (kColR * kSeg));
-      const int nr = min(kColR, k - st * kColR);
-      for (int r = 0; r < nr; ++r) {
+    const T* seg = reinterpret_cast<const T*>(ring + (st % kColS) * (kColR * kSeg));
+    const int nr = min(kColR, k - st * kColR);
+    if (warp == 0) {
+      if (nr == kColR) {
+#pragma unroll 16
+        for (int r = 0; r < kColR; ++r) {
+          const double x = double(seg[r * 32 + lane]);
+          sum = __dadd_rn(sum, __dmul_rn(x, x));
+        }
+      } else {
+        for (int r = 0; r < nr; ++r) {
+          const double x = double(seg[r * 32 + lane]);
+          sum = __dadd_rn(sum, __dmul_rn(x, x));
+        }
+      }
+    } else {
+      for (int r = warp - 1; r < nr; r += 3) {
         const double x = double(seg[r * 32 + lane]);
         const double ax = fabs(x);
         bad |= !isfinite(x);
         mx = fmax(mx, ax);
-        if (ax != 0.0) mn = fmin(mn, ax);
-        sum = __dadd_rn(sum, __dmul_rn(x, x));
+        mn = fmin(mn, ax != 0.0 ? ax : INFINITY);
       }
     }
     __syncthreads();
   }
-  if (threadIdx.x >= 32) return;
+  if (warp > 0) {
+    red_mx[warp - 1][lane] = mx;
+    red_mn[warp - 1][lane] = mn;
+    red_bad[warp - 1][lane] = bad;
+  }
+  __syncthreads();
+  if (warp > 0) return;
+  mx = fmax(fmax(red_mx[0][lane], red_mx[1][lane]), red_mx[2][lane]);
+  mn = fmin(fmin(red_mn[0][lane], red_mn[1][lane]), red_mn[2][lane]);
+  bad = red_bad[0][lane] | red_bad[1][lane] | red_bad[2][lane];
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicAdd(diag + CRTG_DIAG_NONFINITE_B, 1ull);
   double other = 0.0;
   if (!REAL) {  // lanes (2c, 2c+1) = (re, im) of column c
