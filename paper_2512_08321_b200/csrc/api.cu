@@ -1122,8 +1122,9 @@ struct HostChunks {
 // the wall time is bounded below by max_f [f T_x + (1 - f^2) T_c]; finer pieces
 // approach that bound (8 -> 16 pieces: ~5 ms at 16384^3, tools/e2e_profile.py).
 HostChunks host_chunks(const Plan& P) {
+  static const int npieces = std::max(1, env_int("CRTG_HOST_PIECES", 16));
   auto piece = [](int64_t x) {
-    return x >= 4096 ? round_up((x + 15) / 16, 256) : round_up(x, 256);
+    return x >= 4096 ? round_up((x + npieces - 1) / npieces, 256) : round_up(x, 256);
   };
   return HostChunks{piece(P.m), piece(P.n)};
 }

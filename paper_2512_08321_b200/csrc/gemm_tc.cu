@@ -161,8 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             // advance 32 bytes of K inside the 128-byte swizzle atom
-            mma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk | sg.accumulate) != 0);
-            if (MODE == EPI_RAW && g.repeat_mma) {
+            if (MODE != EPI_RAW || g.repeat_mma >= 0)
+              mma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk | sg.accumulate) != 0);
+            if (MODE == EPI_RAW && g.repeat_mma > 0) {
               // power experiment: a second MMA on operands already in smem --
               // 1: same A and B, 2: same A / next B slice, 3: next A and B slices
               const int ka = g.repeat_mma == 3 ? (kk + 1) & 3 : kk;

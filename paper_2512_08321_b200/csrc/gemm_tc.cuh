@@ -32,7 +32,7 @@ struct GemmArgs {
   unsigned long long* overflow;  // REAL: int32 accumulator overflow (kernel.py:33-34)
   int group_m;       // raster: row tiles per column sweep (0 -> 16)
   int unsigned_ops;  // u8 x u8 products (accumulator read as u32)
-  int repeat_mma;    // RAW power experiment: every MMA issued twice
+  int repeat_mma;    // RAW experiments: >0 every MMA issued twice, -1 no MMA (load-only)
   ModConst mc[CRTG_MAX_MODULI];
 };
 

@@ -141,7 +141,7 @@ def repeat():
     from paper_2512_08321_b200.emulate import _gemm_i8_raw
     n = 16384
     dev = torch.device("cuda")
-    k = 16384 if os.environ.get("CRTG_RAW_REPEAT", "0") != "0" else 32768
+    k = 32768 if os.environ.get("CRTG_RAW_REPEAT", "0") in ("0", "-1") else 16384
     a = torch.randint(-128, 128, (n, k), dtype=torch.int8, device=dev)
     b = torch.randint(-128, 128, (k, n), dtype=torch.int8, device=dev)
     r = run_fn(f"s8 full, k={k}, repeat={os.environ.get('CRTG_RAW_REPEAT', '0')}",
