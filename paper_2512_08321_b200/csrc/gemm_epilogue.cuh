@@ -52,13 +52,17 @@ __device__ __forceinline__ void karatsuba_phase(const GemmArgs& g, uint32_t tadd
   if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
   if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
   const uint32_t bias = uint32_t(mc.bias), bias_h = mc.bias_h, h = mc.h;
-  uint32_t v[2][32];
+  // 8 chunks per thread: chunk c+1's TMEM load is in flight while chunk c is
+  // reduced; 4 chunks (16 epilogue warps, register-limited): one buffer
+  constexpr int NB = NCH >= 8 ? 2 : 1;
+  uint32_t v[NB][32];
   tmem_ld32(taddr, v[0]);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
+    if (NB == 1 && c > 0) tmem_ld32(taddr + c * 32, v[0]);
     tmem_wait_ld();  // chunk c has landed (the only load in flight)
-    if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
-    const uint32_t (&cv)[32] = v[c & 1];
+    if (NB == 2 && c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) % NB]);
+    const uint32_t (&cv)[32] = v[c % NB];
     uint32_t out[8];
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
@@ -108,13 +112,15 @@ __device__ __forceinline__ void split_phase(const GemmArgs& g, uint32_t taddr, i
   int8_t* dim = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
   const uint32_t bias = uint32_t(mc.bias), h = mc.h, p = uint32_t(mc.p);
   const uint32_t inv2 = mc.inv2, inv2j = mc.inv2j;
-  uint32_t v[2][32];
+  constexpr int NB = NCH >= 8 ? 2 : 1;
+  uint32_t v[NB][32];
   tmem_ld32(taddr, v[0]);
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
+    if (NB == 1 && c > 0) tmem_ld32(taddr + c * 32, v[0]);
     tmem_wait_ld();
-    if (c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) & 1]);
-    const uint32_t (&cv)[32] = v[c & 1];
+    if (NB == 2 && c + 1 < NCH) tmem_ld32(taddr + (c + 1) * 32, v[(c + 1) % NB]);
+    const uint32_t (&cv)[32] = v[c % NB];
     uint32_t ore[8], oim[8];
 #pragma unroll
     for (int w = 0; w < 8; ++w) {

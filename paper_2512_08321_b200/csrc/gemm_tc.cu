@@ -21,6 +21,7 @@
 //   EPI_BOUND: cross = AI*BR + AR*BI (buffer 0) and diff = AD*BD (buffer 1);
 //     bound = max(cross+diff, cross); row / column maxima by atomicMax.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm_tc.cuh"
@@ -288,7 +289,10 @@ __device__ __forceinline__ void decode_tile_w(int t, const GemmArgs& g, int& l, 
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1) k_gemm_w(const __grid_constant__ GemmArgs g) {
+// EW epilogue warps: 8 (lane quarter x row half, 256 columns each) or 16 (also
+// x column half, 128 columns each: the non-overlapped drain takes half as long)
+template <int EW>
+__global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_constant__ GemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kWStages];
   __shared__ __align__(8) uint64_t empty_bar[kWStages];
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_w(const __grid_constant__ 
       mbar_init(smem_u32(&empty_bar[s]), 1);
     }
     mbar_init(smem_u32(&tfull_bar), 1);
-    mbar_init(smem_u32(&tempty_bar), kEpiThreads);
+    mbar_init(smem_u32(&tempty_bar), 32 * EW);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(&tmem_slot));
@@ -368,26 +372,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_w(const __grid_constant__ 
       }
     }
   } else if (warp >= 4) {
-    // ------- epilogue: 8 warps, lane quarter warp % 4, row half (warp - 4) / 4, 256 columns -------
+    // ------- epilogue: lane quarter warp % 4, row half, (EW = 16) column half -------
+    constexpr int NCH = EW == 16 ? 4 : 8;  // 32-column chunks per thread
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
-    const uint32_t lane_addr = tmem + (uint32_t(32 * q) << 16) + uint32_t(256 * half);
+    const int idx = (warp - 4) >> 2;
+    const int half = EW == 16 ? idx >> 1 : idx;
+    const int colh = EW == 16 ? idx & 1 : 0;
+    const uint32_t lane_addr =
+        tmem + (uint32_t(32 * q) << 16) + uint32_t(256 * half) + uint32_t(32 * NCH * colh);
     uint32_t gslot = 0;
-    uint32_t st[64];
+    uint32_t st[NCH * 8];
 #pragma unroll
-    for (int i = 0; i < 64; ++i) st[i] = 0;
+    for (int i = 0; i < NCH * 8; ++i) st[i] = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm2, tn;
       decode_tile_w(t, g, l, tm2, tn);
       const int row = tm2 * 256 + 128 * half + 32 * q + lane;
       const bool row_ok = row < g.m;
-      const int col_base = tn * 256;
+      const int col_base = tn * 256 + 32 * NCH * colh;
       const ModConst mc = g.mc[l];
       const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
       for (int s = 0; s < nseg; ++s) {
         mbar_wait(smem_u32(&tfull_bar), gslot & 1);
         tc_fence_after();
-        epilogue_phase<EPI_KARATSUBA, 8>(g, lane_addr, s, l, row, row_ok, col_base, mc, st);
+        epilogue_phase<EPI_KARATSUBA, NCH>(g, lane_addr, s, l, row, row_ok, col_base, mc, st);
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty_bar));
         ++gslot;
@@ -553,10 +561,22 @@ int launch_gemm_wide(const GemmArgs& g, int num_sms, cudaStream_t stream) {
   if (total <= 0) return 0;
   const int grid = total < num_sms ? total : num_sms;
   const size_t smem = size_t(kWStages) * kWStageBytes + 1024;
-  const cudaError_t err =
-      cudaFuncSetAttribute(k_gemm_w, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (err != cudaSuccess) return int(err);
-  k_gemm_w<<<grid, kThreads, smem, stream>>>(g);
+  // CRTG_EPI_WARPS=16 halves the non-overlapped drain but measured 10% slower
+  // (96-register cap -> spills, more issue energy under the power cap)
+  static const int ew = [] {
+    const char* v = std::getenv("CRTG_EPI_WARPS");
+    return v && std::atoi(v) == 16 ? 16 : 8;
+  }();
+  cudaError_t err;
+  if (ew == 16) {
+    err = cudaFuncSetAttribute(k_gemm_w<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (err != cudaSuccess) return int(err);
+    k_gemm_w<16><<<grid, 128 + 32 * 16, smem, stream>>>(g);
+  } else {
+    err = cudaFuncSetAttribute(k_gemm_w<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (err != cudaSuccess) return int(err);
+    k_gemm_w<8><<<grid, 128 + 32 * 8, smem, stream>>>(g);
+  }
   return launched(1);
 }
 

@@ -112,3 +112,42 @@ class TestModuli:
         assert int(k.p_hi) + int(k.p_lo) == ms.product or abs(
             (int(k.p_hi) + int(k.p_lo)) - ms.product) < 2 ** 60
         assert np.float32(k.p_fast) == crt.ScalingConstants.from_product(ms.product).p_fast
+
+
+class TestSplitModuli:
+    """Moduli with a square root of -1 take the 2-product (split) form on the GPU."""
+
+    def test_sqrt_minus_one(self):
+        from paper_2512_08321_b200.moduli import has_sqrt_minus_one
+        # primes 1 mod 4 split, primes 3 mod 4 and even moduli do not
+        assert [p for p in (241, 233, 229, 197, 193, 181, 173) if has_sqrt_minus_one(p)] == \
+            [241, 233, 229, 197, 193, 181, 173]
+        assert not any(has_sqrt_minus_one(p) for p in (256, 255, 253, 251, 247, 239, 227, 223,
+                                                       217, 211, 199, 191, 179))
+        # composite with every factor 1 mod 4 (5 * 13 = 65, 5 * 17 = 85)
+        assert has_sqrt_minus_one(65) and has_sqrt_minus_one(85)
+        assert not has_sqrt_minus_one(3 * 5)
+
+    def test_identity_on_residues(self):
+        # e_R = (X + Y)/2, e_I = (X - Y)/(2j) with X = U U', Y = V V'  (mod p)
+        rng = np.random.default_rng(3)
+        for p in (241, 173, 197):
+            j = next(x for x in range(1, p) if (x * x + 1) % p == 0)
+            ar, ai, br, bi = (rng.integers(-(p // 2), p // 2 + 1, 50) for _ in range(4))
+            u, v = (ar + j * ai) % p, (ar - j * ai) % p
+            u2, v2 = (br + j * bi) % p, (br - j * bi) % p
+            X, Y = int(np.sum(u * u2)), int(np.sum(v * v2))
+            inv2, inv2j = pow(2, -1, p), pow(2 * j, -1, p)
+            er = int(np.sum(ar * br - ai * bi))
+            ei = int(np.sum(ar * bi + ai * br))
+            assert (X + Y) * inv2 % p == er % p
+            assert (X - Y) * inv2j % p == ei % p
+
+    def test_products_per_modulus(self, monkeypatch):
+        from paper_2512_08321_b200.moduli import products_per_modulus
+        ms = crt.select_moduli(15)
+        monkeypatch.setenv("CRTG_SPLIT", "1")
+        assert sum(products_per_modulus(ms)) == 41
+        assert sum(products_per_modulus(crt.select_moduli(20))) == 53
+        monkeypatch.setenv("CRTG_SPLIT", "0")
+        assert sum(products_per_modulus(ms)) == 45
