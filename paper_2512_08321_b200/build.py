@@ -57,6 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     def compile_one(src):
         obj = os.path.join(BUILD, src.replace(".cu", ".o"))
         flags = list(COMMON)
+        # A/B experiments only: extra -D definitions (e.g. CRTG_NVCC_DEFS="CRTG_EPI_DB=1")
+        flags += ["-D" + d for d in os.environ.get("CRTG_NVCC_DEFS", "").split()]
         if src in EXACT:
             flags.append("-fmad=false")
         cmd = [cc, *ARCH, *flags, "-c", os.path.join(CSRC, src), "-o", obj]

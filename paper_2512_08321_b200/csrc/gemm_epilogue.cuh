@@ -13,6 +13,13 @@
 #include "common.cuh"
 #include "gemm_tc.cuh"
 
+// CRTG_EPI_DB=1 double-buffers the TMEM loads of 8-chunk epilogues (chunk c+1
+// in flight while chunk c is reduced); the default single buffer keeps the
+// 256-column wide-tile epilogue within 168 registers without spills
+#ifndef CRTG_EPI_DB
+#define CRTG_EPI_DB 0
+#endif
+
 namespace crtg {
 
 __device__ __forceinline__ uint32_t ep_pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
@@ -54,7 +61,7 @@ __device__ __forceinline__ void karatsuba_phase(const GemmArgs& g, uint32_t tadd
   const uint32_t bias = uint32_t(mc.bias), bias_h = mc.bias_h, h = mc.h;
   // 8 chunks per thread: chunk c+1's TMEM load is in flight while chunk c is
   // reduced; 4 chunks (16 epilogue warps, register-limited): one buffer
-  constexpr int NB = NCH >= 8 ? 2 : 1;
+  constexpr int NB = NCH >= 8 && CRTG_EPI_DB ? 2 : 1;
   uint32_t v[NB][32];
   tmem_ld32(taddr, v[0]);
 #pragma unroll
@@ -112,7 +119,7 @@ __device__ __forceinline__ void split_phase(const GemmArgs& g, uint32_t taddr, i
   int8_t* dim = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
   const uint32_t bias = uint32_t(mc.bias), h = mc.h, p = uint32_t(mc.p);
   const uint32_t inv2 = mc.inv2, inv2j = mc.inv2j;
-  constexpr int NB = NCH >= 8 ? 2 : 1;
+  constexpr int NB = NCH >= 8 && CRTG_EPI_DB ? 2 : 1;
   uint32_t v[NB][32];
   tmem_ld32(taddr, v[0]);
 #pragma unroll
