@@ -1322,8 +1322,17 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     if (t < ncb) {  // B_t: every resident chunk x block t
       CRTG_TRY(piece_b(t), "piece B");
       const int64_t ib = std::min(t + 1, nrc);
-      CRTG_TRY(strip(0, std::min(ib * hc.rows, m), t * hc.cols, std::min((t + 1) * hc.cols, n)),
-               "strip");
+      const int64_t c0 = t * hc.cols, c1 = std::min((t + 1) * hc.cols, n);
+      if (t == npieces - 1 && ib >= 8) {
+        // the last strip in four row parts: the D2H of each part overlaps the
+        // next part's GEMM, so only a quarter of the final copy-back is exposed
+        const int64_t per = (ib + 3) / 4;
+        for (int64_t i = 0; i < ib; i += per)
+          CRTG_TRY(strip(i * hc.rows, std::min(std::min(i + per, ib) * hc.rows, m), c0, c1),
+                   "strip");
+      } else {
+        CRTG_TRY(strip(0, std::min(ib * hc.rows, m), c0, c1), "strip");
+      }
     }
   }
   cudaEvent_t evD = E.get();
