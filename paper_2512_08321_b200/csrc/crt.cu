@@ -12,6 +12,11 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+// CTAs per SM the CRT kernel is compiled for (3: 80 registers, no spills)
+#ifndef CRTG_CRT_MINB
+#define CRTG_CRT_MINB 3
+#endif
+
 namespace crtg {
 
 namespace {
@@ -115,7 +120,7 @@ __device__ __forceinline__ uint32_t load_word(const int8_t* p, bool aligned, int
 }
 
 template <bool SINGLE, bool LIMBS, bool REAL>
-__global__ void __launch_bounds__(256) k_crt(int64_t m, int64_t n, const int8_t* __restrict__ e_re,
+__global__ void __launch_bounds__(256, CRTG_CRT_MINB) k_crt(int64_t m, int64_t n, const int8_t* __restrict__ e_re,
                                              const int8_t* __restrict__ e_im, int64_t e_plane,
                                              int64_t e_ld, const int32_t* __restrict__ mu,
                                              const int32_t* __restrict__ nu,
