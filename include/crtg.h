@@ -116,11 +116,13 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k,
 
 /*
  * The same product on HOST buffers (pinned for full overlap): A, B, C are host
- * pointers; B's column blocks are copied in (copy engine) while the GPU works on
- * the blocks already resident and finished C blocks are copied back while the
- * next block computes.  `ws` is a DEVICE workspace of
- * crtg_host_workspace_size(...) bytes.  On return (stream-ordered) C is complete
- * once `stream` is synchronized.
+ * pointers.  A's row chunks and B's column blocks (~1/16 of each) are copied in
+ * interleaved on a copy engine; each landed piece releases a strip of output
+ * tiles that is computed (one GEMM + CRT launch) while later pieces are still
+ * in flight, and finished strips of C are copied back on a second copy engine.
+ * `n_block` is accepted (results are bitwise invariant) but the pieces bound the
+ * working set.  `ws` is a DEVICE workspace of crtg_host_workspace_size(...)
+ * bytes.  On return (stream-ordered) C is complete once `stream` is synchronized.
  */
 size_t crtg_host_workspace_size(int precision, int mode, int64_t m, int64_t n, int64_t k,
                                 int num_moduli, int64_t n_block);
