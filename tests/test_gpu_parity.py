@@ -399,3 +399,23 @@ def test_host_streaming_equals_device_path(crt, mode, shape):
     if mode == "fast":
         want = orc.emulate_complex(a[-37:], b[:, -41:], 13, "fast")
         assert host[-37:, -41:].tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("prec,N", [("single", 8), ("double", 20)])
+def test_host_streaming_single_and_wide_moduli(crt, prec, N):
+    """Host-streaming entry with complex64 inputs (single precision) and with
+    N = 20 (7 split moduli, wide residue limbs at phi = 4), 16-piece staircase
+    with ragged last pieces: bitwise the device path."""
+    m, n, k = 4100, 4352, 700
+    rng = np.random.default_rng(N)
+    dt = np.complex64 if prec == "single" else np.complex128
+    a = (rng.standard_normal((m, k)) * np.exp(4 * rng.standard_normal((m, k)))
+         + 1j * rng.standard_normal((m, k))).astype(dt)
+    b = (rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))).astype(dt)
+    cfg = crt.EmuConfig(precision=prec, domain="complex", mode="fast", num_moduli=N)
+    host = crt.emulate_gemm_complex(a, b, cfg)
+    dev = crt.emulate_gemm_complex(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), cfg)
+    assert host.dtype == dev.cpu().numpy().dtype
+    assert host.tobytes() == dev.cpu().numpy().tobytes()
+    want = orc.emulate_complex(a[:33], b[:, -29:], N, "fast", prec)
+    assert host[:33, -29:].tobytes() == want.tobytes()
