@@ -1190,6 +1190,22 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   CRTG_TRY(cudaStreamWaitEvent(h2d, ev0, 0), "wait");
   CRTG_TRY(cudaStreamWaitEvent(d2h, ev0, 0), "wait");
 
+  // CRTG_HOST_TRACE=1: print a timeline (ms after the call starts) of every
+  // piece landing and every strip's GEMM start / end (diagnostics only)
+  static const bool trace = env_int("CRTG_HOST_TRACE", 0) != 0;
+  std::vector<std::pair<std::string, cudaEvent_t>> marks;
+  cudaEvent_t t0ev = nullptr;
+  auto mark = [&](const std::string& what, cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    marks.push_back({what, e});
+  };
+  if (trace) {
+    cudaEventCreate(&t0ev);
+    cudaEventRecord(t0ev, s);
+  }
   const int64_t nrc = (m + hc.rows - 1) / hc.rows;
   const int64_t ncb = (n + hc.cols - 1) / hc.cols;
   std::vector<cudaEvent_t> evA(nrc), evB(ncb);
@@ -1200,6 +1216,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
                                k * esz, h, cudaMemcpyHostToDevice, h2d),
              "H2D A");
     evA[i] = E.get();
+    mark("A" + std::to_string(i) + " landed", h2d);
     return int(cudaEventRecord(evA[i], h2d));
   };
   auto copy_b = [&](int64_t j) -> int {
@@ -1208,6 +1225,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
                                ldb * esz, w * esz, k, cudaMemcpyHostToDevice, h2d),
              "H2D B");
     evB[j] = E.get();
+    mark("B" + std::to_string(j) + " landed", h2d);
     return int(cudaEventRecord(evB[j], h2d));
   };
   // transfer order: A0 B0 A1 B1 ... (the longer list's tail last)
@@ -1268,7 +1286,33 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     return CRTG_OK;
   };
   // output strip rows [r0, r1) x columns [c0, c1): one GEMM launch, one CRT, one D2H
+  // PCIe is full duplex but not free: with C copied back while inputs stream in,
+  // H2D drops from 55.6 to ~46 GB/s (tools/pcie_2d.py duplex).  The input
+  // transfer is the critical path, so the copy-back of finished strips waits
+  // until a fraction CRTG_D2H_GATE (default 0.6) of the input pieces has
+  // landed; the backlog then drains beside the last pieces and the final strips.
+  static const double d2h_gate = [] {
+    const char* v = std::getenv("CRTG_D2H_GATE");
+    return v && *v ? std::atof(v) : 0.6;
+  }();
+  {
+    const int64_t total_pieces = nrc + ncb;
+    const int64_t gp = std::min<int64_t>(total_pieces - 1,
+                                         int64_t(d2h_gate * double(total_pieces)));
+    if (gp > 0) {
+      // the gp-th piece in transfer order (A0 B0 A1 B1 ...)
+      int64_t cnt = 0;
+      cudaEvent_t gate = nullptr;
+      for (int64_t t = 0; t < npieces && !gate; ++t) {
+        if (t < nrc && cnt++ == gp) gate = evA[t];
+        if (!gate && t < ncb && cnt++ == gp) gate = evB[t];
+      }
+      if (gate) CRTG_TRY(cudaStreamWaitEvent(d2h, gate, 0), "wait");
+    }
+  }
   auto strip = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
+    mark("strip " + std::to_string(r0) + ":" + std::to_string(r1) + " x " + std::to_string(c0) +
+             ":" + std::to_string(c1) + " start", s);
     GemmArgs g{};
     g.a = apack;
     g.b = bpack;
@@ -1305,6 +1349,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     }
     cudaEvent_t evC = E.get();
     CRTG_TRY(cudaEventRecord(evC, s), "record");
+    mark("  strip end", s);
     CRTG_TRY(cudaStreamWaitEvent(d2h, evC, 0), "wait");
     CRTG_TRY(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(r0) * ldc + c0) * csz, ldc * csz,
                                cst, n * csz, (c1 - c0) * csz, r1 - r0, cudaMemcpyDeviceToHost, d2h),
@@ -1338,6 +1383,17 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   cudaEvent_t evD = E.get();
   CRTG_TRY(cudaEventRecord(evD, d2h), "record");
   CRTG_TRY(cudaStreamWaitEvent(s, evD, 0), "wait");
+  if (trace) {
+    mark("done", s);
+    cudaStreamSynchronize(s);
+    std::vector<std::pair<float, std::string>> tl;
+    for (auto& mk : marks) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, t0ev, mk.second) == cudaSuccess) tl.push_back({ms, mk.first});
+    }
+    std::sort(tl.begin(), tl.end());
+    for (auto& x : tl) std::fprintf(stderr, "[crtg trace] %8.2f ms  %s\n", x.first, x.second.c_str());
+  }
   if (sync_check) return check_diag(dg, s);
   return CRTG_OK;
 }

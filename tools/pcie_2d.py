@@ -28,5 +28,40 @@ def main():
     print(json.dumps({"h2d_GBps_2d": out}))
 
 
+
+
+def duplex():
+    """H2D alone, D2H alone, and both at once on two streams (4 GiB each)."""
+    n = 1 << 28  # complex128 elements = 4 GiB
+    h1 = torch.empty(n, dtype=torch.complex128).pin_memory()
+    h2 = torch.empty(n, dtype=torch.complex128).pin_memory()
+    d1 = torch.empty(n, dtype=torch.complex128, device="cuda")
+    d2 = torch.empty(n, dtype=torch.complex128, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    out = {}
+    for name, ops in (("h2d", [(s1, d1, h1)]), ("d2h", [(s2, h2, d2)]),
+                      ("both", [(s1, d1, h1), (s2, h2, d2)])):
+        for _ in range(2):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            evs = []
+            for st, dst, src in ops:
+                st.wait_event(e0)
+                with torch.cuda.stream(st):
+                    dst.copy_(src, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(st)
+                    evs.append(ev)
+            for ev in evs:
+                torch.cuda.current_stream().wait_event(ev)
+            e1.record()
+            torch.cuda.synchronize()
+        out[name] = round(len(ops) * n * 16 / (e0.elapsed_time(e1) * 1e-3) / 1e9, 1)
+    print(json.dumps({"duplex_GBps_total": out}))
+
+
 if __name__ == "__main__":
-    main()
+    import sys
+    duplex() if "duplex" in sys.argv else main()
