@@ -310,7 +310,8 @@ def run_ours(a, rank: int, world: int, local_rank: int):
         traffic = None  # the committed capture is for another configuration
     roof = {"bound": "tensor", "kernel": "k_gemm_w (256x256 Karatsuba/split tiles)",
             "achieved": achieved,
-            "peak": peak_int8, "unit": "TOPS", "frac": achieved / peak_int8,
+            "peak": peak_int8, "unit": "TFLOP/s", "op_kind": "INT8 tensor ops (one MAC = 2 ops), TOPS",
+            "frac": achieved / peak_int8,
             "peak_note": f"INT8 dense = 2 x {src} SUSTAINED bf16 ({bf16_sus} TF/s, "
                          f"MEASURED_PEAKS.json; kernel timed inside a long step); burst 2 x {bf16}; "
                          "spec 4500",
