@@ -301,9 +301,12 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     ops_launch = 2.0 * prods * a.m * a.n * a.k * a.steps / launches_gemm
     ops_model = 6.0 * a.moduli * a.m * a.n * a.k * a.steps / launches_gemm
     achieved = ops_launch / (gemm_ms * 1e-3) / 1e12
-    # K3 runs inside a long, power-capped step -> the SUSTAINED figure is the
-    # denominator (B200 dense INT8 rate = 2 x dense BF16)
-    peak_int8 = 2.0 * bf16_sus
+    # B200 dense INT8 rate = 2 x dense BF16.  K3 runs inside a long, power-capped
+    # step, but an INT8 MAC costs less energy than a bf16 one, so the capped
+    # INT8 GEMM runs ABOVE 2 x the capped (sustained) bf16 rate (frac > 1);
+    # the denominator is therefore 2 x the BURST bf16 figure, with the
+    # sustained-based and spec ratios reported beside it
+    peak_int8 = 2.0 * bf16
     traffic = profile_traffic()
     if traffic and [traffic.get(k) for k in ("m", "n", "k", "N", "n_block", "mode")] != \
             [a.m, a.n, a.k, a.moduli, a.n_block, a.mode]:
@@ -312,10 +315,9 @@ def run_ours(a, rank: int, world: int, local_rank: int):
             "achieved": achieved,
             "peak": peak_int8, "unit": "TFLOP/s", "op_kind": "INT8 tensor ops (one MAC = 2 ops), TOPS",
             "frac": achieved / peak_int8,
-            "peak_note": f"INT8 dense = 2 x {src} SUSTAINED bf16 ({bf16_sus} TF/s, "
-                         f"MEASURED_PEAKS.json; kernel timed inside a long step); burst 2 x {bf16}; "
-                         "spec 4500",
-            "frac_of_burst": achieved / (2.0 * bf16), "frac_of_spec": achieved / 4500.0,
+            "peak_note": f"INT8 dense = 2 x {src} BURST bf16 ({bf16} TF/s, MEASURED_PEAKS.json); "
+                         f"sustained 2 x {bf16_sus}; spec 4500",
+            "frac_of_sustained": achieved / (2.0 * bf16_sus), "frac_of_spec": achieved / 4500.0,
             "ops_per_launch": ops_launch, "ms_per_launch": gemm_ms,
             "int8_products_per_step": prods,
             "ops_note": f"executed INT8 ops: {prods} products of m x n_block x k per launch "
