@@ -291,6 +291,7 @@ ResConst make_res(int p, uint32_t off) {
     return t;
   };
   const uint64_t o = off % P;
+  rc.k31 = uint32_t((o + P - pow2_mod(31)) % P);
   rc.k63 = uint32_t((o + P - pow2_mod(63)) % P);
   rc.kw = uint32_t((o + P - pow2_mod(90)) % P);
   rc.sum_k = uint32_t((P - o) % P);

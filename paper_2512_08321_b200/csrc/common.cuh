@@ -69,8 +69,8 @@ struct ModConst {
 
 // Residue-kernel constants for one modulus and one stored representative
 // (off = floor(p/2): the symmetric residue t - off; off = 128: t ^ 0x80).
-// A value a' is read as 16-bit limbs of v = a' + 2^63 (four limbs) or 2^90 + a'
-// (six); u = sum_i limb_i * (2^(16 i) mod p) + k is congruent to a' + off and
+// A value a' is read as 16-bit limbs of v = a' + 2^31 (two limbs), a' + 2^63
+// (four) or 2^90 + a' (six); u = sum_i limb_i * (2^(16 i) mod p) + k is congruent to a' + off and
 // below 2^27, so one magic reduction gives t = (a' + off) mod p.
 struct ResConst {
   uint32_t magic;   // ceil(2^(32+shift) / p), or 2^(32 - log2 p) with shift 0 for p = 2^s
@@ -80,6 +80,7 @@ struct ResConst {
   // dp2a byte tables (each 2^(16 i) mod p < 256 fits a byte):
   //  dw0123 = bytes (c0, c16, c32, c48), dw45 = (c64, c80)
   uint32_t dw0123, dw45;
+  uint32_t k31;     // (off - 2^31) mod p
   uint32_t k63;     // (off - 2^63) mod p
   uint32_t kw;      // (off - 2^90) mod p
   uint32_t sum_k;   // (-off) mod p: t_s = (t_re + t_im + sum_k) mod p

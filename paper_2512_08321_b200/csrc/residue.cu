@@ -184,15 +184,19 @@ __device__ __forceinline__ uint32_t mod_small(uint32_t u, const ResConst& c) {
   return mad_lo(q, c.neg_p, u);
 }
 
-template <bool WIDE>
+// FORM 1: |a'| < 2^31, v = a' + 2^31 (one word, one dp2a); 2: |a'| < 2^63, four
+// limbs (two dp2a); 3: six limbs of 2^90 + a' (three dp2a)
+template <int FORM>
 __device__ __forceinline__ uint32_t res_t(const Val3& v, const ResConst& c) {
   uint32_t u;
-  if (WIDE) {
+  if (FORM == 3) {
     u = dp2a_lo(v.w0, c.dw0123, c.kw);
     u = dp2a_hi(v.w1, c.dw0123, u);
     u = dp2a_lo(v.w2, c.dw45, u);
-  } else {
+  } else if (FORM == 2) {
     u = dp2a_hi(v.w1, c.dw0123, dp2a_lo(v.w0, c.dw0123, c.k63));
+  } else {
+    u = dp2a_lo(v.w0, c.dw0123, c.k31);
   }
   return mod_small(u, c);  // t = (a' + off) mod p
 }
@@ -212,7 +216,7 @@ __device__ __forceinline__ uint32_t pack_t(uint32_t a, uint32_t b, uint32_t c, u
 
 // planes of one modulus: [re, im, re+im] (Karatsuba), or [U, V] = [re + j im,
 // re - j im] for a split modulus (c.split; w[2] is then not written)
-template <bool WIDE, bool SYM>
+template <int FORM, bool SYM>
 __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&im)[8],
                                               const ResConst& c, uint32_t (&w)[3][2]) {
 #pragma unroll
@@ -220,8 +224,8 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
     uint32_t tr[4], ti[4], ts[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      tr[j] = res_t<WIDE>(re[4 * half + j], c);
-      ti[j] = res_t<WIDE>(im[4 * half + j], c);
+      tr[j] = res_t<FORM>(re[4 * half + j], c);
+      ti[j] = res_t<FORM>(im[4 * half + j], c);
     }
     if (c.split) {
       uint32_t tu[4], tv[4];
@@ -251,7 +255,7 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
 }
 
 // the per-modulus loop of one tile (complex operands)
-template <int OPERAND, bool WIDE, bool SYM>
+template <int OPERAND, int FORM, bool SYM>
 __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&vi)[8],
                                              const DevConsts& dc, const ResConst* rcs,
                                              int8_t* __restrict__ out, int64_t plane_bytes,
@@ -260,7 +264,7 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
   for (int l = 0; l < dc.n; ++l) {
     const ResConst c = rcs[l];
     uint32_t w[3][2];
-    residue_words<WIDE, SYM>(vr, vi, c, w);
+    residue_words<FORM, SYM>(vr, vi, c, w);
     if (OPERAND == 0) {
       // A rows: the 16 lanes of a row cover its whole 128-byte line of the plane,
       // so a warp store is already two full lines -- no staging needed
@@ -285,10 +289,10 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
   }
 }
 
-template <bool WIDE>
+template <int FORM>
 __device__ __forceinline__ uint32_t pack_real(const Val3 (&v)[8], int i0, const ResConst& c) {
-  return pack_t<true>(res_t<WIDE>(v[i0], c), res_t<WIDE>(v[i0 + 1], c), res_t<WIDE>(v[i0 + 2], c),
-                      res_t<WIDE>(v[i0 + 3], c), c.off);
+  return pack_t<true>(res_t<FORM>(v[i0], c), res_t<FORM>(v[i0 + 1], c), res_t<FORM>(v[i0 + 2], c),
+                      res_t<FORM>(v[i0 + 3], c), c.off);
 }
 
 template <typename T, int OPERAND, bool REAL, bool SYM>
@@ -329,7 +333,7 @@ __global__ void __launch_bounds__(256, 4) k_residues(const T* __restrict__ X, in
   // q = x * 2^e exactly (quantize, scaling.py:277-293); a' = trunc(q)
   double qr[8], qi[8];
   int bad = 0;
-  bool huge = false;
+  bool huge = false, medium = false;
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int h = h0 + t;
@@ -343,13 +347,23 @@ __global__ void __launch_bounds__(256, 4) k_residues(const T* __restrict__ X, in
     qi[t] = __dmul_rn(im, scale);
     if (!(fabs(qr[t]) < 0x1p90)) { bad = 1; qr[t] = 0.0; }
     if (!(fabs(qi[t]) < 0x1p90)) { bad = 1; qi[t] = 0.0; }
-    huge |= fmax(fabs(qr[t]), fabs(qi[t])) >= 0x1p63;
+    const double mq = fmax(fabs(qr[t]), fabs(qi[t]));
+    huge |= mq >= 0x1p63;
+    medium |= mq >= 0x1p31;
   }
-  // warp-uniform representation (the wide form is valid for every value): a
-  // warp that mixed both would execute both per-modulus paths
+  // warp-uniform representation (a wider form is valid for every value): a
+  // warp that mixed forms would execute several per-modulus paths
   huge = __any_sync(0xffffffffu, huge);
+  medium = __any_sync(0xffffffffu, medium);
   Val3 vr[8], vi[8];
-  if (!huge) {
+  if (!medium) {
+    // |a'| < 2^31 (single precision at N <= 8): a' + 2^31 in one word
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      vr[t] = {uint32_t(__double2int_rz(qr[t])) ^ 0x80000000u, 0u, 0u};
+      vi[t] = {uint32_t(__double2int_rz(qi[t])) ^ 0x80000000u, 0u, 0u};
+    }
+  } else if (!huge) {
     // |a'| < 2^63: one truncating conversion gives a' as int64; a' + 2^63 flips the sign bit
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -381,11 +395,14 @@ __global__ void __launch_bounds__(256, 4) k_residues(const T* __restrict__ X, in
       const ResConst c = dc.rc[l];
       uint32_t w0, w1;
       if (huge) {
-        w0 = pack_real<true>(vr, 0, c);
-        w1 = pack_real<true>(vr, 4, c);
+        w0 = pack_real<3>(vr, 0, c);
+        w1 = pack_real<3>(vr, 4, c);
+      } else if (medium) {
+        w0 = pack_real<2>(vr, 0, c);
+        w1 = pack_real<2>(vr, 4, c);
       } else {
-        w0 = pack_real<false>(vr, 0, c);
-        w1 = pack_real<false>(vr, 4, c);
+        w0 = pack_real<1>(vr, 0, c);
+        w1 = pack_real<1>(vr, 4, c);
       }
       if (OPERAND == 0) {
         *reinterpret_cast<uint2*>(out + int64_t(l) * plane_bytes + goff + soff) = make_uint2(w0, w1);
@@ -399,9 +416,11 @@ __global__ void __launch_bounds__(256, 4) k_residues(const T* __restrict__ X, in
       }
     }
   } else if (huge) {
-    store_moduli<OPERAND, true, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    store_moduli<OPERAND, 3, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+  } else if (medium) {
+    store_moduli<OPERAND, 2, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   } else {
-    store_moduli<OPERAND, false, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    store_moduli<OPERAND, 1, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   }
   }  // tile loop
 }
