@@ -270,7 +270,10 @@ namespace {
 constexpr uint32_t kWStageA = 32768;  // 256 rows x 128 B (two packed blocks)
 constexpr uint32_t kWStageB = 32768;  // 256 rows x 128 B
 constexpr uint32_t kWStageBytes = kWStageA + kWStageB;
-constexpr int kWStages = 3;
+#ifndef CRTG_W_STAGES
+#define CRTG_W_STAGES 3
+#endif
+constexpr int kWStages = CRTG_W_STAGES;
 constexpr int kWGroupM = 8;  // 256-row tiles per column sweep
 
 __device__ __forceinline__ void decode_tile_w(int t, const GemmArgs& g, int& l, int& tm2,
