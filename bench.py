@@ -423,9 +423,10 @@ def run_ours(a, rank: int, world: int, local_rank: int):
         barrier()
         dt = max_over_ranks((time.perf_counter() - t0) / reps)
         result["e2e"] = {"value": flops_step / dt / 1e12, "unit": UNIT,
-                         "h2d_bytes_per_step": int(hA.numel() * hA.element_size()
-                                                   + hB.numel() * hB.element_size()),
-                         "d2h_bytes_per_step": int(hC.numel() * hC.element_size()),
+                         # whole job: every rank streams its own operands / tile
+                         "h2d_bytes_per_step": world * int(hA.numel() * hA.element_size()
+                                                           + hB.numel() * hB.element_size()),
+                         "d2h_bytes_per_step": world * int(hC.numel() * hC.element_size()),
                          "ms_per_step": dt * 1e3,
                          "api": "paper_2512_08321_b200.emulate_gemm_complex(pinned host tensors)"
                                 " -> crtg_gemm_complex_host (A row chunks / B column blocks streamed in a staircase, C tiles back, on the copy engines)"}
