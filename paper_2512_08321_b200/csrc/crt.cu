@@ -16,6 +16,10 @@
 #ifndef CRTG_CRT_MINB
 #define CRTG_CRT_MINB 3
 #endif
+// moduli whose residue words are loaded ahead of the arithmetic (even)
+#ifndef CRTG_CRT_BATCH
+#define CRTG_CRT_BATCH 6
+#endif
 
 namespace crtg {
 
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(256, CRTG_CRT_MINB) k_crt(int64_t m, int64_t n
   // (latency-bound otherwise); S2 terms are still added in ascending l, and the
   // exact integer S1 limbs take two moduli per dp2a (16-bit limb pair x the
   // residue bytes of both moduli)
-  constexpr int kB = 6;
+  constexpr int kB = CRTG_CRT_BATCH;
   for (int l0 = 0; l0 < dc.n; l0 += kB) {
     uint32_t wr[kB], wi[kB];
 #pragma unroll
