@@ -148,9 +148,10 @@ int run_gemm(int mode, const GemmArgs& g0, cudaStream_t s) {
   if (pair_enabled() && mode != EPI_BOUND && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
     return launch_gemm_pair(mode, g, sm_count(), s);
   static const bool mc = env_int("CRTG_MC", 0) != 0;
-  if (wide_enabled() && mode == EPI_KARATSUBA && (g.mt % 2) == 0 && (g.mt0 % 2) == 0) {
-    if (mc && (g.nt % 2) == 0) return launch_gemm_wide_mc(g, sm_count(), s);
-    return launch_gemm_wide(g, sm_count(), s);
+  if (wide_enabled() && (mode == EPI_KARATSUBA || mode == EPI_REAL) && (g.mt % 2) == 0 &&
+      (g.mt0 % 2) == 0) {
+    if (mc && mode == EPI_KARATSUBA && (g.nt % 2) == 0) return launch_gemm_wide_mc(g, sm_count(), s);
+    return launch_gemm_wide(mode, g, sm_count(), s);
   }
   return launch_gemm(mode, g, sm_count(), s);
 }
@@ -1590,7 +1591,7 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
     {
       StageTimer timer(CRTG_STAGE_GEMM, s);
-      CRTG_TRY(launch_gemm(EPI_REAL, g, sm_count(), s), "real gemm");
+      CRTG_TRY(run_gemm(EPI_REAL, g, s), "real gemm");
     }
     {
       StageTimer timer(CRTG_STAGE_CRT, s);

@@ -294,7 +294,7 @@ __device__ __forceinline__ void decode_tile_w(int t, const GemmArgs& g, int& l, 
 
 // EW epilogue warps: 8 (lane quarter x row half, 256 columns each) or 16 (also
 // x column half, 128 columns each: the non-overlapped drain takes half as long)
-template <int EW>
+template <int MODE, int EW>
 __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_constant__ GemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[kWStages];
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm2, tn;
       decode_tile_w(t, g, l, tm2, tn);
-      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
+      const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const int8_t* a = g.a + (int64_t)(l * g.planes_per_l + s) * g.a_plane;
         const int8_t* b = g.b + (int64_t)(l * g.planes_per_l + s) * g.b_plane;
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm2, tn;
       decode_tile_w(t, g, l, tm2, tn);
-      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
+      const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         mbar_wait(smem_u32(&tempty_bar), (gslot & 1) ^ 1);  // epilogue drained both halves
         tc_fence_after();
@@ -394,11 +394,11 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
       const bool row_ok = row < g.m;
       const int col_base = tn * 256 + 32 * NCH * colh;
       const ModConst mc = g.mc[l];
-      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
+      const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         mbar_wait(smem_u32(&tfull_bar), gslot & 1);
         tc_fence_after();
-        epilogue_phase<EPI_KARATSUBA, NCH>(g, lane_addr, s, l, row, row_ok, col_base, mc, st);
+        epilogue_phase<MODE, NCH>(g, lane_addr, s, l, row, row_ok, col_base, mc, st);
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty_bar));
         ++gslot;
@@ -559,7 +559,24 @@ int launch_gemm_wide_mc(const GemmArgs& g, int num_sms, cudaStream_t stream) {
 
 size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + 1024; }
 
-int launch_gemm_wide(const GemmArgs& g, int num_sms, cudaStream_t stream) {
+template <int MODE>
+int launch_wide_mode(const GemmArgs& g, int grid, size_t smem, int ew, cudaStream_t stream) {
+  cudaError_t err;
+  if (ew == 16) {
+    err = cudaFuncSetAttribute(k_gemm_w<MODE, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+    if (err != cudaSuccess) return int(err);
+    k_gemm_w<MODE, 16><<<grid, 128 + 32 * 16, smem, stream>>>(g);
+  } else {
+    err = cudaFuncSetAttribute(k_gemm_w<MODE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(smem));
+    if (err != cudaSuccess) return int(err);
+    k_gemm_w<MODE, 8><<<grid, 128 + 32 * 8, smem, stream>>>(g);
+  }
+  return launched(1);
+}
+
+int launch_gemm_wide(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {
   const int total = g.nl * (g.mt >> 1) * g.nt;
   if (total <= 0) return 0;
   const int grid = total < num_sms ? total : num_sms;
@@ -570,17 +587,8 @@ int launch_gemm_wide(const GemmArgs& g, int num_sms, cudaStream_t stream) {
     const char* v = std::getenv("CRTG_EPI_WARPS");
     return v && std::atoi(v) == 16 ? 16 : 8;
   }();
-  cudaError_t err;
-  if (ew == 16) {
-    err = cudaFuncSetAttribute(k_gemm_w<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (err != cudaSuccess) return int(err);
-    k_gemm_w<16><<<grid, 128 + 32 * 16, smem, stream>>>(g);
-  } else {
-    err = cudaFuncSetAttribute(k_gemm_w<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (err != cudaSuccess) return int(err);
-    k_gemm_w<8><<<grid, 128 + 32 * 8, smem, stream>>>(g);
-  }
-  return launched(1);
+  return mode == EPI_REAL ? launch_wide_mode<EPI_REAL>(g, grid, smem, ew, stream)
+                          : launch_wide_mode<EPI_KARATSUBA>(g, grid, smem, ew, stream);
 }
 
 int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {

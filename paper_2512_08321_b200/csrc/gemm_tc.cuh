@@ -39,9 +39,9 @@ struct GemmArgs {
 size_t gemm_smem_bytes();
 // returns a cudaError_t value (0 = success)
 int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream);
-// wide-tile Karatsuba / split variant (256 x 256 per CTA, gemm_tc.cu); g.mt and
+// wide-tile KARATSUBA (split) / REAL variant (256 x 256 per CTA, gemm_tc.cu); g.mt and
 // g.mt0 must be even
-int launch_gemm_wide(const GemmArgs& g, int num_sms, cudaStream_t stream);
+int launch_gemm_wide(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream);
 // wide tiles in 2-CTA clusters along N sharing A by multicast; g.nt even
 int launch_gemm_wide_mc(const GemmArgs& g, int num_sms, cudaStream_t stream);
 // CTA-pair variant (cta_group::2, 256x256 tiles; KARATSUBA and RAW); g.mt and
