@@ -43,6 +43,8 @@ import numpy as np  # noqa: E402
 METRIC = ("emulated ZGEMM TFLOPS (8mnk/t) at m=n=k=16384 per GPU, fast mode, 15 moduli "
           "(max rel. error <= cuBLAS native)")
 UNIT = "TFLOPS"
+METRIC_STRONG = ("emulated ZGEMM TFLOPS (8mnk/t) of one m=n=k=32768 product sharded by output "
+                 "tiles (cfg5), scatter + compute + gather per step")
 
 
 def parse():
@@ -63,9 +65,15 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-accuracy", action="store_true",
                     help="skip the live max-relative-error check (GPU double-double reference)")
+    ap.add_argument("--strong", action="store_true",
+                    help="cfg5 strong scaling: ONE product of --shape (default 32768^3) sharded "
+                         "by output tiles over the ranks; rank 0 holds A and B, scatters the "
+                         "row / column blocks and gathers C over NCCL inside the timed step")
     ap.add_argument("--cpu-sample", type=int, default=128,
                     help="rows/cols of the CPU sample block (k kept full)")
     a = ap.parse_args()
+    if a.strong and a.shape == [16384, 16384, 16384]:
+        a.shape = [32768, 32768, 32768]
     a.m, a.n, a.k = a.shape
     return a
 
@@ -440,6 +448,116 @@ def run_ours(a, rank: int, world: int, local_rank: int):
         dist.destroy_process_group()
 
 
+def run_strong(a, rank: int, world: int, local_rank: int):
+    """cfg5: one (m x k) @ (k x n) product sharded by output tiles over `world`
+    ranks (paper_2512_08321_b200.dist).  The timed step is what a caller of the
+    sharded product pays with operands resident on rank 0: scatter of A's row
+    blocks and B's column blocks (NCCL send/recv over NVLink), each rank's tile,
+    gather of C to rank 0.  Tile compute alone is reported beside it."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_08321_b200 as crt
+    from paper_2512_08321_b200 import _native as nat
+    from paper_2512_08321_b200 import dist as cdist
+
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local_rank % max(ndev, 1))
+    torch.cuda.set_device(dev)
+    if world > 1:
+        backend = os.environ.get("CRTG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    grid = cdist.TileGrid.for_world(world)
+    cdt = torch.complex128 if a.precision == "double" else torch.complex64
+    cfg = crt.EmuConfig(precision=a.precision, domain="complex", mode=a.mode,
+                        num_moduli=a.moduli, n_block=a.n_block)
+    A = B = None
+    if rank == 0:
+        A = synth(torch, a.m, a.k, a.phi, 1000, cdt, dev)
+        B = synth(torch, a.k, a.n, a.phi, 2000, cdt, dev)
+    emu = cdist.ShardedEmulator(cfg, grid, rank) if world > 1 else None
+    tile_ms = []
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        if world == 1:
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            crt.run_complex(A, B, cfg, None, dev, sync_check=False)
+            t1.record()
+            tile_ms.append((t0, t1))
+            return
+        a_loc, b_loc = cdist.scatter_operands(A, B, grid, rank, a.m, a.n, a.k, cdt, dev)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        c_loc = emu.tile(a_loc, b_loc, sync_check=False)
+        t1.record()
+        tile_ms.append((t0, t1))
+        cdist.gather_tiles(c_loc, grid, rank, a.m, a.n)
+
+    for _ in range(a.warmup):
+        step()
+    barrier()
+    tile_ms.clear()
+    nat.profile_enable(True)
+    nat.profile_read()
+    launches0 = nat.launch_count()
+    sampler = ClockSampler(dev.index)
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record()
+    for _ in range(a.steps):
+        step()
+    e1.record()
+    barrier()
+    clocks = sampler.stop()
+    launches = nat.launch_count() - launches0
+    nat.profile_enable(False)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        on_dev = dist.get_backend() == "nccl"
+        t = torch.tensor([x], dtype=torch.float64, device=dev if on_dev else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms_step = max_over_ranks(e0.elapsed_time(e1)) / a.steps
+    ms_tile = max_over_ranks(sum(x.elapsed_time(y) for x, y in tile_ms)) / a.steps
+    flops = 8.0 * a.m * a.n * a.k
+    result = {"metric": METRIC_STRONG, "value": flops / (ms_step * 1e-3) / 1e12, "unit": UNIT,
+              "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
+              "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+              "dtype": "int8 tensor / f64" if a.precision == "double" else "int8 tensor / f32",
+              "data": "synthetic (u-0.5)*exp(z*phi), drawn on device (rank 0)",
+              "config": {"workload": f"zgemm_{a.m}x{a.n}x{a.k}_{a.mode}_N{a.moduli}_sharded"
+                                     if a.precision == "double" else
+                                     f"cgemm_{a.m}x{a.n}x{a.k}_{a.mode}_N{a.moduli}_sharded",
+                         "m": a.m, "n": a.n, "k": a.k, "num_moduli": a.moduli, "mode": a.mode,
+                         "grid": f"{grid.R}x{grid.C}", "parallelism": f"output-tile x{world}",
+                         "l2": "operands far larger than the 126 MB L2; no flush"},
+              "tile_compute_ms": ms_tile,
+              "tile_compute_tflops": flops / (ms_tile * 1e-3) / 1e12,
+              "comm_ms": ms_step - ms_tile,
+              "gpu_launches": int(launches), "clocks": clocks}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -447,6 +565,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if a.impl == "reference":
         run_reference(a, rank)
+        return
+    if a.strong:
+        run_strong(a, rank, world, local_rank)
         return
     run_ours(a, rank, world, local_rank)
 

@@ -107,6 +107,25 @@ def reduce_bound_maxima(row_max: torch.Tensor, col_max: torch.Tensor,
         dist.all_reduce(col_max, op=dist.ReduceOp.MAX, group=groups.col_group)
 
 
+def _staged() -> bool:
+    """gloo moves CPU tensors only: device tensors are staged through the host
+    (CPU tests / several ranks sharing one GPU); NCCL sends device memory."""
+    return dist.get_backend() == "gloo"
+
+
+def _send(t: torch.Tensor, dst: int) -> None:
+    dist.send(t.cpu() if (_staged() and t.is_cuda) else t, dst)
+
+
+def _recv(t: torch.Tensor, src: int) -> None:
+    if _staged() and t.is_cuda:
+        buf = torch.empty(t.shape, dtype=t.dtype)
+        dist.recv(buf, src)
+        t.copy_(buf)
+    else:
+        dist.recv(t, src)
+
+
 def scatter_operands(a, b, grid: TileGrid, rank: int, m: int, n: int, k: int,
                      dtype, device, root: int = 0):
     """Root sends A[I_r,:] and B[:,J_c] to every rank; returns the local blocks
@@ -122,13 +141,13 @@ def scatter_operands(a, b, grid: TileGrid, rank: int, m: int, n: int, k: int,
             if dst == root:
                 a_loc, b_loc = ablk, bblk
             else:
-                dist.send(ablk, dst)
-                dist.send(bblk, dst)
+                _send(ablk, dst)
+                _send(bblk, dst)
         return a_loc, b_loc
     a_loc = torch.empty((i1 - i0, k), dtype=dtype, device=device)
     b_loc = torch.empty((k, j1 - j0), dtype=dtype, device=device)
-    dist.recv(a_loc, root)
-    dist.recv(b_loc, root)
+    _recv(a_loc, root)
+    _recv(b_loc, root)
     return a_loc, b_loc
 
 
@@ -136,7 +155,7 @@ def gather_tiles(c_loc: torch.Tensor, grid: TileGrid, rank: int, m: int, n: int,
                  root: int = 0):
     """Every rank sends its C tile to root; root returns the assembled C."""
     if rank != root:
-        dist.send(c_loc.contiguous(), root)
+        _send(c_loc.contiguous(), root)
         return None
     out = torch.empty((m, n), dtype=c_loc.dtype, device=c_loc.device)
     for src in range(grid.world):
@@ -146,7 +165,7 @@ def gather_tiles(c_loc: torch.Tensor, grid: TileGrid, rank: int, m: int, n: int,
             out[i0:i1, j0:j1] = c_loc
         else:
             buf = torch.empty((i1 - i0, j1 - j0), dtype=c_loc.dtype, device=c_loc.device)
-            dist.recv(buf, src)
+            _recv(buf, src)
             out[i0:i1, j0:j1] = buf
     return out
 
