@@ -479,6 +479,8 @@ def run_strong(a, rank: int, world: int, local_rank: int):
         A = synth(torch, a.m, a.k, a.phi, 1000, cdt, dev)
         B = synth(torch, a.k, a.n, a.phi, 2000, cdt, dev)
     emu = cdist.ShardedEmulator(cfg, grid, rank) if world > 1 else None
+    groups = emu.groups if (emu and emu.groups) else (
+        cdist.TileGroups(grid, rank) if world > 2 else None)
     tile_ms = []
 
     def barrier():
@@ -495,7 +497,8 @@ def run_strong(a, rank: int, world: int, local_rank: int):
             t1.record()
             tile_ms.append((t0, t1))
             return
-        a_loc, b_loc = cdist.scatter_operands(A, B, grid, rank, a.m, a.n, a.k, cdt, dev)
+        a_loc, b_loc = cdist.scatter_operands(A, B, grid, rank, a.m, a.n, a.k, cdt, dev,
+                                              groups=groups)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()

@@ -127,28 +127,79 @@ def _recv(t: torch.Tensor, src: int) -> None:
 
 
 def scatter_operands(a, b, grid: TileGrid, rank: int, m: int, n: int, k: int,
-                     dtype, device, root: int = 0):
-    """Root sends A[I_r,:] and B[:,J_c] to every rank; returns the local blocks
-    (contiguous, on `device`)."""
+                     dtype, device, root: int = 0, groups: "TileGroups | None" = None):
+    """Root distributes A[I_r,:] and B[:,J_c]; returns the local blocks (contiguous,
+    on `device`).
+
+    With `groups` (R x C > 2 ranks): two levels, so the root sends each block
+    ONCE — A's row-block r goes to the row leader (r, 0) and B's column-block c
+    to the column leader (0, c), which broadcast it over their grid row / column
+    (NVSwitch: every rank has full bandwidth to every peer, so the broadcasts of
+    different groups run side by side).  Root egress ~ |A| + |B| instead of
+    R*C*(|A|/R + |B|/C).  Without groups: one point-to-point send per rank."""
     i0, i1 = grid.rows(m, rank)
     j0, j1 = grid.cols(n, rank)
-    if rank == root:
-        for dst in range(grid.world):
-            di0, di1 = grid.rows(m, dst)
-            dj0, dj1 = grid.cols(n, dst)
-            ablk = a[di0:di1].contiguous().to(device)
-            bblk = b[:, dj0:dj1].contiguous().to(device)
-            if dst == root:
-                a_loc, b_loc = ablk, bblk
-            else:
-                _send(ablk, dst)
-                _send(bblk, dst)
+    r_me, c_me = grid.coords(rank)
+    if groups is None or grid.world <= 2:
+        if rank == root:
+            for dst in range(grid.world):
+                di0, di1 = grid.rows(m, dst)
+                dj0, dj1 = grid.cols(n, dst)
+                ablk = a[di0:di1].contiguous().to(device)
+                bblk = b[:, dj0:dj1].contiguous().to(device)
+                if dst == root:
+                    a_loc, b_loc = ablk, bblk
+                else:
+                    _send(ablk, dst)
+                    _send(bblk, dst)
+            return a_loc, b_loc
+        a_loc = torch.empty((i1 - i0, k), dtype=dtype, device=device)
+        b_loc = torch.empty((k, j1 - j0), dtype=dtype, device=device)
+        _recv(a_loc, root)
+        _recv(b_loc, root)
         return a_loc, b_loc
-    a_loc = torch.empty((i1 - i0, k), dtype=dtype, device=device)
-    b_loc = torch.empty((k, j1 - j0), dtype=dtype, device=device)
-    _recv(a_loc, root)
-    _recv(b_loc, root)
+    a_lead = grid.row_members(r_me)[0]   # (r, 0)
+    b_lead = grid.col_members(c_me)[0]   # (0, c)
+    a_loc = b_loc = None
+    # level 1: root -> leaders (one block each)
+    if rank == root:
+        for r in range(grid.R):
+            di0, di1 = grid.rows(m, grid.row_members(r)[0])
+            blk = a[di0:di1].contiguous().to(device)
+            if grid.row_members(r)[0] == root:
+                a_loc = blk
+            else:
+                _send(blk, grid.row_members(r)[0])
+        for c in range(grid.C):
+            dj0, dj1 = grid.cols(n, grid.col_members(c)[0])
+            blk = b[:, dj0:dj1].contiguous().to(device)
+            if grid.col_members(c)[0] == root:
+                b_loc = blk
+            else:
+                _send(blk, grid.col_members(c)[0])
+    if a_loc is None:
+        a_loc = torch.empty((i1 - i0, k), dtype=dtype, device=device)
+        if rank == a_lead:
+            _recv(a_loc, root)
+    if b_loc is None:
+        b_loc = torch.empty((k, j1 - j0), dtype=dtype, device=device)
+        if rank == b_lead:
+            _recv(b_loc, root)
+    # level 2: leaders broadcast over their grid row / column
+    if grid.C > 1:
+        _bcast(a_loc, a_lead, groups.row_group)
+    if grid.R > 1:
+        _bcast(b_loc, b_lead, groups.col_group)
     return a_loc, b_loc
+
+
+def _bcast(t: torch.Tensor, src: int, group) -> None:
+    if _staged() and t.is_cuda:
+        buf = t.cpu()
+        dist.broadcast(buf, src, group=group)
+        t.copy_(buf)
+    else:
+        dist.broadcast(t, src, group=group)
 
 
 def gather_tiles(c_loc: torch.Tensor, grid: TileGrid, rank: int, m: int, n: int,

@@ -94,19 +94,29 @@ def test_accurate_bound_exchange_gloo(R, C):
     _run(_accurate_exchange, 2, R, C)
 
 
-def _scatter_gather(rank, world):
+def _scatter_gather(rank, world, two_level):
     grid = TileGrid.for_world(world)
+    groups = TileGroups(grid, rank) if two_level else None
     m, n, k = 9, 14, 11
     rng = np.random.default_rng(3)
     a = b = None
     if rank == 0:
         a = torch.from_numpy(rng.integers(-9, 9, (m, k)) + 1j * rng.integers(-9, 9, (m, k)))
         b = torch.from_numpy(rng.integers(-9, 9, (k, n)) + 1j * rng.integers(-9, 9, (k, n)))
-    a_loc, b_loc = scatter_operands(a, b, grid, rank, m, n, k, torch.complex128, "cpu")
+    a_loc, b_loc = scatter_operands(a, b, grid, rank, m, n, k, torch.complex128, "cpu",
+                                    groups=groups)
+    i0, i1 = grid.rows(m, rank)
+    j0, j1 = grid.cols(n, rank)
+    assert a_loc.shape == (i1 - i0, k) and b_loc.shape == (k, j1 - j0)
     c = gather_tiles(a_loc @ b_loc, grid, rank, m, n)
     if rank == 0:
         assert torch.equal(c, a @ b)
 
 
 def test_scatter_gather_gloo():
-    _run(_scatter_gather, 2)
+    _run(_scatter_gather, 2, False)
+
+
+def test_scatter_two_level_gloo():
+    # 2 x 2 grid: root -> row / column leaders -> broadcasts over grid rows / columns
+    _run(_scatter_gather, 4, True)
