@@ -274,19 +274,23 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
       if (!c.split)
         *reinterpret_cast<uint2*>(base + 2 * plane_bytes) = make_uint2(w[2][0], w[2][1]);
     } else {
-      *reinterpret_cast<uint2*>(&stage[0][soff]) = make_uint2(w[0][0], w[0][1]);
-      *reinterpret_cast<uint2*>(&stage[1][soff]) = make_uint2(w[1][0], w[1][1]);
-      if (!c.split) *reinterpret_cast<uint2*>(&stage[2][soff]) = make_uint2(w[2][0], w[2][1]);
+      // double-buffered stage: modulus l uses buffer l & 1, so one barrier per
+      // modulus suffices (a thread writing buffer b again for l + 2 has passed
+      // the barrier of l + 1, which every thread reaches only after copying l out)
+      uint8_t (*sb)[kResRows * 128] = stage + 3 * (l & 1);
+      *reinterpret_cast<uint2*>(&sb[0][soff]) = make_uint2(w[0][0], w[0][1]);
+      *reinterpret_cast<uint2*>(&sb[1][soff]) = make_uint2(w[1][0], w[1][1]);
+      if (!c.split) *reinterpret_cast<uint2*>(&sb[2][soff]) = make_uint2(w[2][0], w[2][1]);
       __syncthreads();
       int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
       reinterpret_cast<uint4*>(base + cq * plane_bytes)[cs] =
-          reinterpret_cast<const uint4*>(stage[cq])[cs];
+          reinterpret_cast<const uint4*>(sb[cq])[cs];
       if (cq == 0 && !c.split)
         reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
-            reinterpret_cast<const uint4*>(stage[2])[cs];
-      __syncthreads();
+            reinterpret_cast<const uint4*>(sb[2])[cs];
     }
   }
+  if (OPERAND != 0) __syncthreads();  // the next tile reuses the buffers
 }
 
 template <int FORM>
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(256, 4) k_residues(const T* __restrict__ X, in
                                                   int64_t rb_count,
                                                   unsigned long long* __restrict__ overflow,
                                                   int n_kb, int n_rt, int row_base) {
-  __shared__ __align__(16) uint8_t stage[3][kResRows * 128];
+  __shared__ __align__(16) uint8_t stage[6][kResRows * 128];  // 2 x (3 planes)
   // representative of the stored residues: the symmetric (rc) or the 128-offset (rx) tables
   const ResConst* rcs = SYM ? dc.rc : dc.rx;
   // grid-stride over (K block, 16-row tile): a full grid when launched alone, one

@@ -334,8 +334,13 @@ __global__ void __launch_bounds__(128) k_col_sumsq(const T* __restrict__ B, int6
 // the per-column chains are inherently sequential, so with few columns (n =
 // 4096 at k = 65536) a register-only loop cannot cover the DRAM latency.
 // ---------------------------------------------------------------------------
-constexpr int kColR = 64;  // rows per stage
-constexpr int kColS = 4;   // stages
+// rows per stage x stages of the cp.async ring (64 x 4 = 64 KiB per CTA for
+// complex128: 3 CTAs per SM; CRTG_COL_R=32 halves it)
+#ifndef CRTG_COL_R
+#define CRTG_COL_R 64
+#endif
+constexpr int kColR = CRTG_COL_R;  // rows per stage
+constexpr int kColS = 4;           // stages
 constexpr int32_t kNuPending = INT32_MIN;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
