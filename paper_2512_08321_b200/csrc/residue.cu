@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
 // t ^ 0x80 -- one LOP per four values instead of four subtractions.
 // ---------------------------------------------------------------------------
 constexpr int kResRows = 16;
+#ifndef CRTG_RES_UNROLL
+#define CRTG_RES_UNROLL 1
+#endif
 
 // Value representations (one truncating conversion per value):
 //  medium (|a'| < 2^63, every warp at N <= 14 and most at N <= 20):
@@ -264,7 +267,15 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
                                              int8_t* __restrict__ out, int64_t plane_bytes,
                                              int64_t goff, int soff, int cq, int cs,
                                              uint8_t (*stage)[kResRows * 128]) {
+  // unrolled over the modulus index: each modulus's constants become immediate
+  // constant-bank operands instead of per-iteration LDC loads
+#if CRTG_RES_UNROLL
+#pragma unroll
+  for (int l = 0; l < CRTG_MAX_MODULI; ++l) {
+    if (l >= dc.n) break;
+#else
   for (int l = 0; l < dc.n; ++l) {
+#endif
     const ResConst c = rcs[l];
     uint32_t w[3][2];
     residue_words<FORM, SYM>(vr, vi, c, w);
