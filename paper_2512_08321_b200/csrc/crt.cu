@@ -17,6 +17,9 @@
 #define CRTG_CRT_MINB 3
 #endif
 // moduli whose residue words are loaded ahead of the arithmetic (even)
+#ifndef CRTG_CRT_UNROLL
+#define CRTG_CRT_UNROLL 0
+#endif
 #ifndef CRTG_CRT_BATCH
 #define CRTG_CRT_BATCH 6
 #endif
@@ -152,7 +155,15 @@ __global__ void __launch_bounds__(256, CRTG_CRT_MINB) k_crt(int64_t m, int64_t n
   // exact integer S1 limbs take two moduli per dp2a (16-bit limb pair x the
   // residue bytes of both moduli)
   constexpr int kB = CRTG_CRT_BATCH;
+#if CRTG_CRT_UNROLL
+  // unrolled over the moduli: coeff_lo / limb constants become immediate
+  // constant-bank operands instead of per-modulus LDC loads
+#pragma unroll
+  for (int l0 = 0; l0 < CRTG_MAX_MODULI; l0 += kB) {
+    if (l0 >= dc.n) break;
+#else
   for (int l0 = 0; l0 < dc.n; l0 += kB) {
+#endif
     uint32_t wr[kB], wi[kB];
 #pragma unroll
     for (int b = 0; b < kB; ++b) {
