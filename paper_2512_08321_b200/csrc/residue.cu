@@ -519,7 +519,7 @@ __device__ __forceinline__ void words_from_t(const uint32_t (&tr)[8], const uint
 }
 
 template <typename T, int OPERAND>
-__global__ void __launch_bounds__(256, 4) k_residues_tc(const T* __restrict__ X, int64_t ldx,
+__global__ void __launch_bounds__(256, 3) k_residues_tc(const T* __restrict__ X, int64_t ldx,
                                                      int rows, int kdim, int64_t col0,
                                                      const int32_t* __restrict__ exps,
                                                      const __grid_constant__ DevConsts dc,
@@ -645,40 +645,45 @@ __global__ void __launch_bounds__(256, 4) k_residues_tc(const T* __restrict__ X,
           make_uint4(uint32_t(v2), uint32_t(v2 >> 32), uint32_t(v3), uint32_t(v3 >> 32));
     }
     fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
-    for (int pass = 0; pass < npass; ++pass) {
-      tc_fence_before();
-      __syncthreads();  // VA written / previous pass's TMEM reads done
-      if (threadIdx.x == 0) {
-        tc_fence_after();
-        const uint64_t bd = smem_desc_noswz(smem_u32(cb + pass * 512), 128, 256);
+    tc_fence_before();
+    __syncthreads();  // VA written
+    auto issue = [&](int pass) {
+      tc_fence_after();
+      const uint64_t bd = smem_desc_noswz(smem_u32(cb + pass * 512), 128, 256);
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          const uint64_t ad = smem_desc_noswz(smem_u32(va + b * kTcBlock), 128, 256);
-          mma_i8(tmem + 64 * (b >> 2) + 16 * (b & 3), ad, bd, idesc, 0);
-        }
-        mma_commit(smem_u32(&mma_bar));
+      for (int b = 0; b < 8; ++b) {
+        const uint64_t ad = smem_desc_noswz(smem_u32(va + b * kTcBlock), 128, 256);
+        mma_i8(tmem + 64 * (b >> 2) + 16 * (b & 3), ad, bd, idesc, 0);
       }
+      mma_commit(smem_u32(&mma_bar));
+    };
+    if (threadIdx.x == 0) issue(0);
+    const uint32_t ta = tmem + (uint32_t(32 * quarter) << 16) + 64 * grp;
+    for (int pass = 0; pass < npass; ++pass) {
       mbar_wait(smem_u32(&mma_bar), mma_phase);
       mma_phase ^= 1;
       tc_fence_after();
-      const uint32_t ta = tmem + (uint32_t(32 * quarter) << 16) + 64 * grp;
-#pragma unroll 1
+      // all of this pass's u into registers, then the next pass's MMAs overwrite
+      // TMEM while the reductions run (software pipeline over the passes)
+      uint32_t u[4][16];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) tmem_ld16(ta + 16 * j, u[j]);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncthreads();  // every thread holds its u
+      if (threadIdx.x == 0 && pass + 1 < npass) issue(pass + 1);
+#pragma unroll
       for (int ml = 0; ml < 4; ++ml) {
         const int l = 4 * pass + ml;
         if (l >= dc.n) break;
-        // u of this modulus for the 16 values: 4 columns in each of the 4 blocks
-        uint32_t u[4][4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) tmem_ld4(ta + 16 * j + 4 * ml, u[j]);
-        tmem_wait_ld();
         const ResConst c = rcs[l];
         uint32_t tr[8], ti[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          tr[2 * j] = mod_small(u[j][0] + c.k63, c);
-          ti[2 * j] = mod_small(u[j][1] + c.k63, c);
-          tr[2 * j + 1] = mod_small(u[j][2] + c.k63, c);
-          ti[2 * j + 1] = mod_small(u[j][3] + c.k63, c);
+          tr[2 * j] = mod_small(u[j][4 * ml] + c.k63, c);
+          ti[2 * j] = mod_small(u[j][4 * ml + 1] + c.k63, c);
+          tr[2 * j + 1] = mod_small(u[j][4 * ml + 2] + c.k63, c);
+          ti[2 * j + 1] = mod_small(u[j][4 * ml + 3] + c.k63, c);
         }
         uint32_t w[3][2];
         words_from_t(tr, ti, c, w);
@@ -723,10 +728,10 @@ __global__ void k_unpack_i8(const int8_t* __restrict__ packed, int64_t rows, int
 }
 
 // CRTG_TC_RESIDUES=1 selects the tensor-core limb sums (k_residues_tc) for the
-// complex pipeline.  Bit-identical but measured slower on B200 (A 6.0 -> 7.6 ms,
-// B 6.3 -> 7.9 ms at 16384^3 N=15): the per-pass barrier + MMA round trip + TMEM
-// reads serialise each CTA, and 128 TMEM columns per CTA (4 CTAs per SM) leave
-// no room to double-buffer passes.  Off by default.
+// complex pipeline.  Bit-identical but measured slower on B200 (pipelined: A
+// 5.6 -> 6.8 ms, B 6.1 -> 7.2 ms at 16384^3 N=15): VA staging, the per-pass
+// barriers and the TMEM reads cost more than the two dp2a they replace.  Off by
+// default.
 bool tc_residues_enabled() {
   static const bool on = [] {
     const char* v = std::getenv("CRTG_TC_RESIDUES");
@@ -754,14 +759,14 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
                                                         int(kdim), col0, exps, dc, out, plane_bytes,
                                                         rb_count, overflow, n_kb, n_rt, int(row_base));
     } else if (tc_residues_enabled()) {
-      // persistent: 4 CTAs per SM (128 TMEM columns each), grid-stride over tiles
+      // persistent: 3 CTAs per SM (128 TMEM columns each), grid-stride over tiles
       static int nsm = [] {
         int d = 0, v = 148;
         cudaGetDevice(&d);
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
         return v;
       }();
-      const unsigned tgrid = unsigned(std::min<int64_t>(tiles, int64_t(4) * nsm));
+      const unsigned tgrid = unsigned(std::min<int64_t>(tiles, int64_t(3) * nsm));
       const unsigned g2 = max_ctas > 0 ? std::min(tgrid, unsigned(max_ctas)) : tgrid;
       const size_t smem = kTcVA + kTcCB + 6 * kResRows * 128;
       cudaFuncSetAttribute(k_residues_tc<T, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
