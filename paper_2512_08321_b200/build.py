@@ -61,6 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         flags += ["-D" + d for d in os.environ.get("CRTG_NVCC_DEFS", "").split()]
         if src in EXACT:
             flags.append("-fmad=false")
+        if src == "api.cu":
+            flags += ["-Xcompiler", "-fopenmp"]  # host-side staging copies
         cmd = [cc, *ARCH, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
@@ -72,7 +74,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = OUT + ".tmp"
-    cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs]
+    cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-o", tmp, *objs]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")

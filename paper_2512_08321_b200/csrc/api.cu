@@ -1141,6 +1141,83 @@ namespace {
 int load_tree(const Plan& P, void* ws, cudaStream_t s, PwTree& tree);  // below
 }  // namespace
 
+namespace {
+// true when p is page-locked host memory (cudaHostAlloc / cudaHostRegister)
+bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Pageable host operands: pieces are gathered by host threads (OpenMP) into a
+// ring of pinned staging slots and copied from there on the copy engine, so a
+// plain numpy caller gets full-rate PCIe without page-locking its arrays (which
+// costs ~0.33 s per 4 GiB plus the unlock).  The CPU runs at most kSlots pieces
+// ahead of the copy engine.
+struct HostStager {
+  static constexpr int kSlots = 3;
+  char* slot[kSlots] = {};
+  cudaEvent_t done[kSlots] = {};
+  bool pending[kSlots] = {};
+  size_t bytes = 0;
+  int next = 0;
+  int ensure(size_t need) {
+    if (need <= bytes) return 0;
+    for (int i = 0; i < kSlots; ++i) {
+      if (pending[i]) cudaEventSynchronize(done[i]);
+      pending[i] = false;
+      if (slot[i]) cudaFreeHost(slot[i]);
+      slot[i] = nullptr;
+    }
+    bytes = 0;
+    for (int i = 0; i < kSlots; ++i) {
+      if (int e = int(cudaHostAlloc(reinterpret_cast<void**>(&slot[i]), need, cudaHostAllocPortable)))
+        return e;
+      if (!done[i])
+        if (int e = int(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming))) return e;
+    }
+    bytes = need;
+    return 0;
+  }
+  // next free slot (waits for the copy that last read it)
+  char* acquire(int& s) {
+    s = next;
+    next = (next + 1) % kSlots;
+    if (pending[s]) cudaEventSynchronize(done[s]);
+    pending[s] = false;
+    return slot[s];
+  }
+  int release(int s, cudaStream_t st) {
+    pending[s] = true;
+    return int(cudaEventRecord(done[s], st));
+  }
+};
+
+HostStager& host_stager() {
+  static thread_local HostStager st;
+  return st;
+}
+
+// dst (contiguous rows of row_bytes) <- rows of src at src_pitch, host threads
+void gather_rows(char* dst, const char* src, int64_t rows, size_t row_bytes, size_t src_pitch) {
+  const int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(rows, 64));
+#pragma omp parallel for num_threads(16) schedule(static)
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t r0 = rows * b / nblk, r1 = rows * (b + 1) / nblk;
+    if (src_pitch == row_bytes) {
+      std::memcpy(dst + size_t(r0) * row_bytes, src + size_t(r0) * src_pitch,
+                  size_t(r1 - r0) * row_bytes);
+    } else {
+      for (int64_t r = r0; r < r1; ++r)
+        std::memcpy(dst + size_t(r) * row_bytes, src + size_t(r) * src_pitch, row_bytes);
+    }
+  }
+}
+}  // namespace
+
 extern "C" size_t crtg_host_workspace_size(int precision, int mode, int64_t m, int64_t n,
                                            int64_t k, int num_moduli, int64_t n_block) {
   const Plan P = host_plan(mode, m, n, k, num_moduli, n_block);
@@ -1211,30 +1288,63 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   const int64_t nrc = (m + hc.rows - 1) / hc.rows;
   const int64_t ncb = (n + hc.cols - 1) / hc.cols;
   std::vector<cudaEvent_t> evA(nrc), evB(ncb);
+  // pageable operands go through pinned staging slots (HostStager)
+  const bool stage_a = !host_pinned(A), stage_b = !host_pinned(B);
+  HostStager& stager = host_stager();
+  if (stage_a || stage_b) {
+    const size_t need = std::max(size_t(hc.rows) * k * esz, size_t(hc.cols) * k * esz);
+    CRTG_TRY(stager.ensure(need), "pinned staging");
+  }
   auto copy_a = [&](int64_t i) -> int {
     const int64_t i0 = i * hc.rows, h = std::min(hc.rows, m - i0);
-    CRTG_TRY(cudaMemcpy2DAsync(dA + size_t(i0) * k * esz, k * esz,
-                               static_cast<const char*>(A) + size_t(i0) * lda * esz, lda * esz,
-                               k * esz, h, cudaMemcpyHostToDevice, h2d),
-             "H2D A");
+    const char* src = static_cast<const char*>(A) + size_t(i0) * lda * esz;
+    if (stage_a) {
+      int sl = 0;
+      char* buf = stager.acquire(sl);
+      gather_rows(buf, src, h, size_t(k) * esz, size_t(lda) * esz);
+      CRTG_TRY(cudaMemcpyAsync(dA + size_t(i0) * k * esz, buf, size_t(h) * k * esz,
+                               cudaMemcpyHostToDevice, h2d),
+               "H2D A");
+      CRTG_TRY(stager.release(sl, h2d), "record");
+    } else {
+      CRTG_TRY(cudaMemcpy2DAsync(dA + size_t(i0) * k * esz, k * esz, src, lda * esz, k * esz, h,
+                                 cudaMemcpyHostToDevice, h2d),
+               "H2D A");
+    }
     evA[i] = E.get();
     mark("A" + std::to_string(i) + " landed", h2d);
     return int(cudaEventRecord(evA[i], h2d));
   };
   auto copy_b = [&](int64_t j) -> int {
     const int64_t j0 = j * hc.cols, w = std::min(hc.cols, n - j0);
-    CRTG_TRY(cudaMemcpy2DAsync(dB + j0 * esz, n * esz, static_cast<const char*>(B) + j0 * esz,
-                               ldb * esz, w * esz, k, cudaMemcpyHostToDevice, h2d),
-             "H2D B");
+    const char* src = static_cast<const char*>(B) + j0 * esz;
+    if (stage_b) {
+      int sl = 0;
+      char* buf = stager.acquire(sl);
+      gather_rows(buf, src, k, size_t(w) * esz, size_t(ldb) * esz);
+      CRTG_TRY(cudaMemcpy2DAsync(dB + j0 * esz, n * esz, buf, w * esz, w * esz, k,
+                                 cudaMemcpyHostToDevice, h2d),
+               "H2D B");
+      CRTG_TRY(stager.release(sl, h2d), "record");
+    } else {
+      CRTG_TRY(cudaMemcpy2DAsync(dB + j0 * esz, n * esz, src, ldb * esz, w * esz, k,
+                                 cudaMemcpyHostToDevice, h2d),
+               "H2D B");
+    }
     evB[j] = E.get();
     mark("B" + std::to_string(j) + " landed", h2d);
     return int(cudaEventRecord(evB[j], h2d));
   };
-  // transfer order: A0 B0 A1 B1 ... (the longer list's tail last)
+  // transfer order: A0 B0 A1 B1 ... (the longer list's tail last).  Fast mode
+  // enqueues each copy right before the strip it releases (a staged copy blocks
+  // the CPU until a slot is free, and the strips must already be queued behind
+  // the copies); accurate mode needs every piece before its exponents.
   const int64_t npieces = std::max(nrc, ncb);
-  for (int64_t t = 0; t < npieces; ++t) {
-    if (t < nrc) CRTG_TRY(copy_a(t), "record");
-    if (t < ncb) CRTG_TRY(copy_b(t), "record");
+  if (mode == CRTG_ACCURATE) {
+    for (int64_t t = 0; t < npieces; ++t) {
+      if (t < nrc) CRTG_TRY(copy_a(t), "record");
+      if (t < ncb) CRTG_TRY(copy_b(t), "record");
+    }
   }
 
   int32_t* mu = at<int32_t>(ws, P.mu);
@@ -1290,28 +1400,41 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   // output strip rows [r0, r1) x columns [c0, c1): one GEMM launch, one CRT, one D2H
   // PCIe is full duplex but not free: with C copied back while inputs stream in,
   // H2D drops from 55.6 to ~46 GB/s (tools/pcie_2d.py duplex).  The input
-  // transfer is the critical path, so the copy-back of finished strips waits
-  // until a fraction CRTG_D2H_GATE (default 0.6) of the input pieces has
-  // landed; the backlog then drains beside the last pieces and the final strips.
+  // transfer is the critical path, so the copy-back of finished strips is held
+  // back until a fraction CRTG_D2H_GATE (default 0.6) of the input pieces has
+  // been queued (the d2h stream then also waits for that piece to land); the
+  // backlog drains beside the last pieces and the final strips.
   static const double d2h_gate = [] {
     const char* v = std::getenv("CRTG_D2H_GATE");
     return v && *v ? std::atof(v) : 0.6;
   }();
-  {
-    const int64_t total_pieces = nrc + ncb;
-    const int64_t gp = std::min<int64_t>(total_pieces - 1,
-                                         int64_t(d2h_gate * double(total_pieces)));
-    if (gp > 0) {
-      // the gp-th piece in transfer order (A0 B0 A1 B1 ...)
-      int64_t cnt = 0;
-      cudaEvent_t gate = nullptr;
-      for (int64_t t = 0; t < npieces && !gate; ++t) {
-        if (t < nrc && cnt++ == gp) gate = evA[t];
-        if (!gate && t < ncb && cnt++ == gp) gate = evB[t];
-      }
-      if (gate) CRTG_TRY(cudaStreamWaitEvent(d2h, gate, 0), "wait");
+  const int64_t total_pieces = nrc + ncb;
+  const int64_t gate_piece =
+      std::min<int64_t>(total_pieces - 1, int64_t(d2h_gate * double(total_pieces)));
+  int64_t pieces_queued = 0;
+  bool gate_open = gate_piece <= 0;
+  struct PendingD2H {
+    int64_t r0, r1, c0, c1;
+    cudaEvent_t ready;
+  };
+  std::vector<PendingD2H> pending_d2h;
+  auto enqueue_d2h = [&](const PendingD2H& x) -> int {
+    CRTG_TRY(cudaStreamWaitEvent(d2h, x.ready, 0), "wait");
+    return int(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(x.r0) * ldc + x.c0) * csz,
+                                 ldc * csz, dC + (size_t(x.r0) * n + x.c0) * csz, n * csz,
+                                 (x.c1 - x.c0) * csz, x.r1 - x.r0, cudaMemcpyDeviceToHost, d2h));
+  };
+  // called after every queued input piece (ev = its landing event)
+  auto piece_queued = [&](cudaEvent_t ev) -> int {
+    ++pieces_queued;
+    if (!gate_open && pieces_queued > gate_piece) {
+      gate_open = true;
+      CRTG_TRY(cudaStreamWaitEvent(d2h, ev, 0), "wait");
+      for (const auto& x : pending_d2h) CRTG_TRY(enqueue_d2h(x), "D2H C");
+      pending_d2h.clear();
     }
-  }
+    return CRTG_OK;
+  };
   auto strip = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1) -> int {
     mark("strip " + std::to_string(r0) + ":" + std::to_string(r1) + " x " + std::to_string(c0) +
              ":" + std::to_string(c1) + " start", s);
@@ -1352,14 +1475,19 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     cudaEvent_t evC = E.get();
     CRTG_TRY(cudaEventRecord(evC, s), "record");
     mark("  strip end", s);
-    CRTG_TRY(cudaStreamWaitEvent(d2h, evC, 0), "wait");
-    CRTG_TRY(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(r0) * ldc + c0) * csz, ldc * csz,
-                               cst, n * csz, (c1 - c0) * csz, r1 - r0, cudaMemcpyDeviceToHost, d2h),
-             "D2H C");
+    (void)cst;
+    const PendingD2H x{r0, r1, c0, c1, evC};
+    if (gate_open) {
+      CRTG_TRY(enqueue_d2h(x), "D2H C");
+    } else {
+      pending_d2h.push_back(x);
+    }
     return CRTG_OK;
   };
   for (int64_t t = 0; t < npieces; ++t) {
     if (t < nrc) {  // A_t: rows of chunk t x every block already resident
+      if (mode == CRTG_FAST) CRTG_TRY(copy_a(t), "record");
+      CRTG_TRY(piece_queued(evA[t]), "gate");
       CRTG_TRY(piece_a(t), "piece A");
       const int64_t jb = std::min(t, ncb);
       if (jb > 0)
@@ -1367,6 +1495,8 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
                  "strip");
     }
     if (t < ncb) {  // B_t: every resident chunk x block t
+      if (mode == CRTG_FAST) CRTG_TRY(copy_b(t), "record");
+      CRTG_TRY(piece_queued(evB[t]), "gate");
       CRTG_TRY(piece_b(t), "piece B");
       const int64_t ib = std::min(t + 1, nrc);
       const int64_t c0 = t * hc.cols, c1 = std::min((t + 1) * hc.cols, n);
@@ -1382,6 +1512,8 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
       }
     }
   }
+  for (const auto& x : pending_d2h) CRTG_TRY(enqueue_d2h(x), "D2H C");
+  pending_d2h.clear();
   cudaEvent_t evD = E.get();
   CRTG_TRY(cudaEventRecord(evD, d2h), "record");
   CRTG_TRY(cudaStreamWaitEvent(s, evD, 0), "wait");

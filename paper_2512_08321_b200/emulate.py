@@ -19,6 +19,7 @@ Lower-level GPU parity hooks mirror the reference's stage functions:
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -129,17 +130,19 @@ _REGISTER_MIN_BYTES = 32 << 20
 
 
 class _HostPins:
-    """Page-locks large numpy operands IN PLACE (cudaHostRegister) for the
-    duration of a host-path call.  Copying a 4 GiB array into a fresh pinned
-    buffer (`Tensor.pin_memory`) takes ~2.7 s on the B200 boxes; registering the
-    caller's pages takes ~0.33 s, and the copy engines then stream at full PCIe
-    rate (50 GB/s vs 11 GB/s from pageable memory)."""
+    """Pageable numpy operands are staged by the library itself (host threads
+    gather each piece into a ring of pinned slots that the copy engine streams
+    from, crtg_gemm_complex_host), so by default nothing is page-locked here.
+    CRTG_HOST_REGISTER=1 instead page-locks the caller's arrays IN PLACE
+    (cudaHostRegister, ~0.33 s per 4 GiB plus the unlock) for the call."""
+
+    REGISTER = os.environ.get("CRTG_HOST_REGISTER", "0") == "1"
 
     def __init__(self):
         self.ptrs = []
 
     def pin(self, arr: np.ndarray):
-        if arr.nbytes < _REGISTER_MIN_BYTES:
+        if not self.REGISTER or arr.nbytes < _REGISTER_MIN_BYTES:
             return torch.from_numpy(arr)
         cr = torch.cuda.cudart()
         err = cr.cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
