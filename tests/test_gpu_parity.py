@@ -419,3 +419,20 @@ def test_host_streaming_single_and_wide_moduli(crt, prec, N):
     assert host.tobytes() == dev.cpu().numpy().tobytes()
     want = orc.emulate_complex(a[:33], b[:, -29:], N, "fast", prec)
     assert host[:33, -29:].tobytes() == want.tobytes()
+
+
+def test_host_pinned_and_staged_paths_agree(crt):
+    """The host entry streams pinned (page-locked) operands directly and
+    pageable ones through its pinned staging ring: both are bitwise the device
+    path (ragged pieces, 16-piece staircase)."""
+    m, n, k = 4300, 4200, 500
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((m, k)) + 1j * rng.standard_normal((m, k))
+    b = rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))
+    cfg = crt.EmuConfig(domain="complex", mode="fast", num_moduli=14)
+    staged = crt.emulate_gemm_complex(a, b, cfg)                       # numpy: staged
+    ta = torch.from_numpy(a).pin_memory()
+    tb = torch.from_numpy(b).pin_memory()
+    pinned = crt.emulate_gemm_complex(ta, tb, cfg)                     # pinned: direct
+    dev = crt.emulate_gemm_complex(ta.cuda(), tb.cuda(), cfg)
+    assert staged.tobytes() == pinned.numpy().tobytes() == dev.cpu().numpy().tobytes()
