@@ -1201,6 +1201,22 @@ HostStager& host_stager() {
   return st;
 }
 
+HostStager& host_out_stager() {
+  static thread_local HostStager st;
+  return st;
+}
+
+// rows of src (row_bytes each, contiguous) -> dst at dst_pitch, host threads
+void scatter_rows(char* dst, const char* src, int64_t rows, size_t row_bytes, size_t dst_pitch) {
+  const int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(rows, 64));
+#pragma omp parallel for num_threads(16) schedule(static)
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int64_t r0 = rows * b / nblk, r1 = rows * (b + 1) / nblk;
+    for (int64_t r = r0; r < r1; ++r)
+      std::memcpy(dst + size_t(r) * dst_pitch, src + size_t(r) * row_bytes, row_bytes);
+  }
+}
+
 // dst (contiguous rows of row_bytes) <- rows of src at src_pitch, host threads
 void gather_rows(char* dst, const char* src, int64_t rows, size_t row_bytes, size_t src_pitch) {
   const int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(rows, 64));
@@ -1418,15 +1434,69 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     cudaEvent_t ready;
   };
   std::vector<PendingD2H> pending_d2h;
+  // pageable C: strips come back through a second ring of pinned slots and host
+  // threads scatter them into C (serviced between pieces and drained at the end)
+  const bool stage_c = !host_pinned(C);
+  HostStager& ostager = host_out_stager();
+  struct OutCopy {
+    int slot;
+    int64_t r0, r1, c0, c1;
+  };
+  std::vector<OutCopy> out_q;  // FIFO of staged strips not yet in C
+  if (stage_c) {
+    const size_t need = std::max(size_t(hc.rows) * n, size_t(m) * hc.cols) * csz;
+    CRTG_TRY(ostager.ensure(need), "pinned staging");
+  }
+  auto finish_out = [&](const OutCopy& o) {  // slot's copy has landed (waited by the caller)
+    scatter_rows(static_cast<char*>(C) + (size_t(o.r0) * ldc + o.c0) * csz, ostager.slot[o.slot],
+                 o.r1 - o.r0, size_t(o.c1 - o.c0) * csz, size_t(ldc) * csz);
+  };
+  auto service_out = [&](bool drain) -> int {
+    while (!out_q.empty()) {
+      const OutCopy& o = out_q.front();
+      if (!drain) {
+        const cudaError_t q = cudaEventQuery(ostager.done[o.slot]);
+        if (q == cudaErrorNotReady) break;
+        CRTG_TRY(int(q), "event");
+      } else {
+        CRTG_TRY(cudaEventSynchronize(ostager.done[o.slot]), "sync");
+      }
+      finish_out(o);
+      ostager.pending[o.slot] = false;
+      out_q.erase(out_q.begin());
+    }
+    return CRTG_OK;
+  };
   auto enqueue_d2h = [&](const PendingD2H& x) -> int {
     CRTG_TRY(cudaStreamWaitEvent(d2h, x.ready, 0), "wait");
-    return int(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(x.r0) * ldc + x.c0) * csz,
-                                 ldc * csz, dC + (size_t(x.r0) * n + x.c0) * csz, n * csz,
-                                 (x.c1 - x.c0) * csz, x.r1 - x.r0, cudaMemcpyDeviceToHost, d2h));
+    if (!stage_c)
+      return int(cudaMemcpy2DAsync(static_cast<char*>(C) + (size_t(x.r0) * ldc + x.c0) * csz,
+                                   ldc * csz, dC + (size_t(x.r0) * n + x.c0) * csz, n * csz,
+                                   (x.c1 - x.c0) * csz, x.r1 - x.r0, cudaMemcpyDeviceToHost, d2h));
+    // the next slot must be empty: it is held by the oldest staged strip (slots
+    // are used round-robin), so finish that one
+    const int sl = ostager.next;
+    if (ostager.pending[sl] && !out_q.empty()) {
+      const OutCopy o = out_q.front();
+      CRTG_TRY(cudaEventSynchronize(ostager.done[o.slot]), "sync");
+      finish_out(o);
+      ostager.pending[o.slot] = false;
+      out_q.erase(out_q.begin());
+    }
+    int got = 0;
+    char* buf = ostager.acquire(got);
+    CRTG_TRY(cudaMemcpy2DAsync(buf, (x.c1 - x.c0) * csz, dC + (size_t(x.r0) * n + x.c0) * csz,
+                               n * csz, (x.c1 - x.c0) * csz, x.r1 - x.r0, cudaMemcpyDeviceToHost,
+                               d2h),
+             "D2H C");
+    CRTG_TRY(ostager.release(got, d2h), "record");
+    out_q.push_back({got, x.r0, x.r1, x.c0, x.c1});
+    return CRTG_OK;
   };
   // called after every queued input piece (ev = its landing event)
   auto piece_queued = [&](cudaEvent_t ev) -> int {
     ++pieces_queued;
+    if (stage_c) CRTG_TRY(service_out(false), "D2H C");
     if (!gate_open && pieces_queued > gate_piece) {
       gate_open = true;
       CRTG_TRY(cudaStreamWaitEvent(d2h, ev, 0), "wait");
@@ -1514,6 +1584,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   }
   for (const auto& x : pending_d2h) CRTG_TRY(enqueue_d2h(x), "D2H C");
   pending_d2h.clear();
+  if (stage_c) CRTG_TRY(service_out(true), "D2H C");  // C complete on return
   cudaEvent_t evD = E.get();
   CRTG_TRY(cudaEventRecord(evD, d2h), "record");
   CRTG_TRY(cudaStreamWaitEvent(s, evD, 0), "wait");

@@ -195,6 +195,11 @@ def run_complex_host(ha: torch.Tensor, hb: torch.Tensor, cfg: EmuConfig,
     lib = nat.load()
     ws = _workspace(lib.crtg_host_workspace_size(prec, mode, m, n, k, nmod, cfg.n_block), dev)
     odt = torch.complex64 if cfg.precision == "single" else torch.complex128
+    # the result lands in pinned host memory (torch's caching host allocator
+    # reuses it across calls: 16384^3 numpy in / numpy out 0.25 s per call in
+    # steady state).  A pageable C also works -- the library then stages the
+    # copy-back through pinned slots -- but measured 0.45 s per call (fresh pages
+    # touched every call) against 1.1 s instead of 2.4 s for the first call.
     out = torch.empty((m, n), dtype=odt, pin_memory=True)
     diag = torch.zeros(nat.DIAG_LEN, dtype=torch.int64, device=dev)
     nat.call("crtg_gemm_complex_host", prec, mode, m, n, k, ha.data_ptr(), ha.stride(0),
