@@ -1142,14 +1142,15 @@ int load_tree(const Plan& P, void* ws, cudaStream_t s, PwTree& tree);  // below
 }  // namespace
 
 namespace {
-// true when p is page-locked host memory (cudaHostAlloc / cudaHostRegister)
+// false only for plain pageable host memory (the staged path); page-locked,
+// device or managed memory goes to the copy engine directly
 bool host_pinned(const void* p) {
   cudaPointerAttributes at{};
   if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return at.type == cudaMemoryTypeHost;
+  return at.type != cudaMemoryTypeUnregistered;
 }
 
 // Pageable host operands: pieces are gathered by host threads (OpenMP) into a
