@@ -122,6 +122,9 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
 // t ^ 0x80 -- one LOP per four values instead of four subtractions.
 // ---------------------------------------------------------------------------
 constexpr int kResRows = 16;
+#ifndef CRTG_RES_MINB
+#define CRTG_RES_MINB 4  // CTAs per SM the register residue kernel is built for
+#endif
 #ifndef CRTG_RES_UNROLL
 #define CRTG_RES_UNROLL 1
 #endif
@@ -314,7 +317,7 @@ __device__ __forceinline__ uint32_t pack_real(const Val3 (&v)[8], int i0, const 
 }
 
 template <typename T, int OPERAND, bool REAL, bool SYM>
-__global__ void __launch_bounds__(256, 4) k_residues(const T* __restrict__ X, int64_t ldx, int rows,
+__global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __restrict__ X, int64_t ldx, int rows,
                                                   int kdim, int64_t col0,
                                                   const int32_t* __restrict__ exps,
                                                   const __grid_constant__ DevConsts dc,
