@@ -324,6 +324,21 @@ __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr
     if (wrapped && row_ok && g.overflow) atomicAdd(g.overflow, 1ull);
     return;
   }
+#ifdef CRTG_EPI_NOP
+  // timing experiment only (results wrong): drain TMEM, skip the math and stores
+  if (MODE == EPI_KARATSUBA) {
+    uint32_t v[32];
+    uint32_t acc = 0;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      tmem_ld32(taddr + c * 32, v);
+      tmem_wait_ld();
+      acc ^= v[c];
+    }
+    st[0] ^= acc;
+    return;
+  }
+#endif
   if (CRTG_EPI_X16 && NCH == 8) {
     if (mc.nphase == 2)
       split_phase16<NCH>(g, taddr, s, l, row, row_ok, col_base, mc, st);
