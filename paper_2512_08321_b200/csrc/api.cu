@@ -1599,6 +1599,8 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     }
     std::sort(tl.begin(), tl.end());
     for (auto& x : tl) std::fprintf(stderr, "[crtg trace] %8.2f ms  %s\n", x.first, x.second.c_str());
+    for (auto& mk : marks) cudaEventDestroy(mk.second);
+    cudaEventDestroy(t0ev);
   }
   if (sync_check) return check_diag(dg, s);
   return CRTG_OK;
