@@ -302,7 +302,26 @@ ResConst make_res(int p, uint32_t off) {
 // split = true: moduli with a square root of -1 use the 2-product form (the
 // production pipeline); false keeps the reference's [re, im, re+im] planes for
 // every modulus (the crtg_residues parity hook unpacks them)
+DevConsts make_dev_uncached(const crtg_consts& K, bool split);
+
+// the constant tables take ~0.1 ms of host integer arithmetic to build (modular
+// inverses, powers, square roots of -1); small calls would pay that every time,
+// so the last few (constants, split) pairs are cached per thread
 DevConsts make_dev(const crtg_consts& K, bool split = true) {
+  struct Entry {
+    crtg_consts key;
+    bool split;
+    DevConsts val;
+  };
+  static thread_local std::vector<Entry> cache;
+  for (const auto& e : cache)
+    if (e.split == split && std::memcmp(&e.key, &K, sizeof(K)) == 0) return e.val;
+  if (cache.size() >= 8) cache.erase(cache.begin());
+  cache.push_back({K, split, make_dev_uncached(K, split)});
+  return cache.back().val;
+}
+
+DevConsts make_dev_uncached(const crtg_consts& K, bool split) {
   DevConsts d{};
   d.n = K.num_moduli;
   for (int l = 0; l < d.n; ++l) {
@@ -415,6 +434,35 @@ const HostTree& pairwise_tree(int64_t n) {
     t.level_start.push_back(t.level_start.back() + cnt);
   }
   return cache.emplace(n, std::move(t)).first->second;
+}
+
+// the same tree in device memory, uploaded once per (device, k) and kept: the
+// per-call pageable uploads cost ~10 us each on small products
+int device_tree(int64_t k, PwTree& out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int64_t>, PwTree> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, k});
+  if (it != cache.end()) {
+    out = it->second;
+    return CRTG_OK;
+  }
+  const HostTree& ht = pairwise_tree(k);
+  const size_t lb = ht.leaves.size() * sizeof(int2), nb = ht.nodes.size() * sizeof(int2),
+               sb = ht.level_start.size() * sizeof(int);
+  char* tb = nullptr;
+  CRTG_TRY(cudaMalloc(&tb, lb + nb + sb + 16), "tree alloc");
+  CRTG_TRY(cudaMemcpy(tb, ht.leaves.data(), lb, cudaMemcpyHostToDevice), "tree copy");
+  if (nb) CRTG_TRY(cudaMemcpy(tb + lb, ht.nodes.data(), nb, cudaMemcpyHostToDevice), "tree copy");
+  CRTG_TRY(cudaMemcpy(tb + lb + nb, ht.level_start.data(), sb, cudaMemcpyHostToDevice), "tree copy");
+  PwTree t{int(ht.leaves.size()), int(ht.nodes.size()), int(ht.level_start.size()) - 1,
+           reinterpret_cast<const int2*>(tb), reinterpret_cast<const int2*>(tb + lb),
+           reinterpret_cast<const int*>(tb + lb + nb)};
+  cache[{dev, k}] = t;
+  out = t;
+  return CRTG_OK;
 }
 
 size_t tree_bytes(int64_t k) { return size_t(16) * (k / 64 + 4) + 4 * 64 + 256; }
@@ -563,21 +611,7 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
   double* colabs = at<double>(ws, P.colabs);
   PwTree tree{};
   if (mode == CRTG_FAST) {
-    const HostTree& ht = pairwise_tree(P.k);
-    char* tb = at<char>(ws, P.tree);
-    const size_t lb = ht.leaves.size() * sizeof(int2), nb = ht.nodes.size() * sizeof(int2),
-                 sb = ht.level_start.size() * sizeof(int);
-    if (lb + nb + sb + 64 > P.tree.bytes) return fail(CRTG_ERR_WORKSPACE, "tree region too small");
-    CRTG_TRY(cudaMemcpyAsync(tb, ht.leaves.data(), lb, cudaMemcpyHostToDevice, s), "tree copy");
-    if (nb) CRTG_TRY(cudaMemcpyAsync(tb + lb, ht.nodes.data(), nb, cudaMemcpyHostToDevice, s), "tree copy");
-    CRTG_TRY(cudaMemcpyAsync(tb + lb + nb, ht.level_start.data(), sb, cudaMemcpyHostToDevice, s),
-             "tree copy");
-    tree.nleaves = int(ht.leaves.size());
-    tree.nnodes = int(ht.nodes.size());
-    tree.nlevels = int(ht.level_start.size()) - 1;
-    tree.leaves = reinterpret_cast<const int2*>(tb);
-    tree.nodes = reinterpret_cast<const int2*>(tb + lb);
-    tree.level_start = reinterpret_cast<const int*>(tb + lb + nb);
+    if (int e = device_tree(P.k, tree)) return e;
     {
       StageTimer timer(CRTG_STAGE_SCALING, s);
       CRTG_TRY(launch_row_stats(single ? E_C64 : E_C128, true, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu,
@@ -1616,19 +1650,9 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
 // ---------------------------------------------------------------------------
 namespace {
 int load_tree(const Plan& P, void* ws, cudaStream_t s, PwTree& tree) {
-  const HostTree& ht = pairwise_tree(P.k);
-  char* tb = at<char>(ws, P.tree);
-  const size_t lb = ht.leaves.size() * sizeof(int2), nbt = ht.nodes.size() * sizeof(int2),
-               sb = ht.level_start.size() * sizeof(int);
-  if (lb + nbt + sb + 64 > P.tree.bytes) return fail(CRTG_ERR_WORKSPACE, "tree region too small");
-  CRTG_TRY(cudaMemcpyAsync(tb, ht.leaves.data(), lb, cudaMemcpyHostToDevice, s), "tree copy");
-  if (nbt) CRTG_TRY(cudaMemcpyAsync(tb + lb, ht.nodes.data(), nbt, cudaMemcpyHostToDevice, s), "tree copy");
-  CRTG_TRY(cudaMemcpyAsync(tb + lb + nbt, ht.level_start.data(), sb, cudaMemcpyHostToDevice, s),
-           "tree copy");
-  tree = PwTree{int(ht.leaves.size()), int(ht.nodes.size()), int(ht.level_start.size()) - 1,
-                reinterpret_cast<const int2*>(tb), reinterpret_cast<const int2*>(tb + lb),
-                reinterpret_cast<const int*>(tb + lb + nbt)};
-  return CRTG_OK;
+  (void)ws;
+  (void)s;
+  return device_tree(P.k, tree);
 }
 }  // namespace
 
