@@ -264,7 +264,7 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
 }
 
 // the per-modulus loop of one tile (complex operands)
-template <int OPERAND, int FORM, bool SYM>
+template <int OPERAND, int FORM, bool SYM, bool MSPLIT = false>
 __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&vi)[8],
                                              const DevConsts& dc, const ResConst* rcs,
                                              int8_t* __restrict__ out, int64_t plane_bytes,
@@ -272,6 +272,9 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
                                              uint8_t (*stage)[kResRows * 128]) {
   // unrolled over the modulus index: each modulus's constants become immediate
   // constant-bank operands instead of per-iteration LDC loads
+  // small operands: blockIdx.y of gridDim.y CTAs share a tile, each taking the
+  // moduli l == blockIdx.y (mod gridDim.y)
+  int it = 0;  // moduli processed by this CTA (smem stage buffer parity)
 #if CRTG_RES_UNROLL
 #pragma unroll
   for (int l = 0; l < CRTG_MAX_MODULI; ++l) {
@@ -279,6 +282,7 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
 #else
   for (int l = 0; l < dc.n; ++l) {
 #endif
+    if (MSPLIT && l % int(gridDim.y) != int(blockIdx.y)) continue;
     const ResConst c = rcs[l];
     uint32_t w[3][2];
     residue_words<FORM, SYM>(vr, vi, c, w);
@@ -294,7 +298,7 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
       // double-buffered stage: modulus l uses buffer l & 1, so one barrier per
       // modulus suffices (a thread writing buffer b again for l + 2 has passed
       // the barrier of l + 1, which every thread reaches only after copying l out)
-      uint8_t (*sb)[kResRows * 128] = stage + 3 * (l & 1);
+      uint8_t (*sb)[kResRows * 128] = stage + 3 * ((MSPLIT ? it++ : l) & 1);
       *reinterpret_cast<uint2*>(&sb[0][soff]) = make_uint2(w[0][0], w[0][1]);
       *reinterpret_cast<uint2*>(&sb[1][soff]) = make_uint2(w[1][0], w[1][1]);
       if (!c.split) *reinterpret_cast<uint2*>(&sb[2][soff]) = make_uint2(w[2][0], w[2][1]);
@@ -413,6 +417,7 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
   if constexpr (REAL) {
     // one plane per modulus (emulate_gemm_real: no imaginary part / Karatsuba sum)
     for (int l = 0; l < dc.n; ++l) {
+      if (gridDim.y > 1 && l % int(gridDim.y) != int(blockIdx.y)) continue;
       const ResConst c = dc.rc[l];
       uint32_t w0, w1;
       if (huge) {
@@ -436,6 +441,11 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
         __syncthreads();
       }
     }
+  } else if (gridDim.y > 1) {  // small operands: this CTA's share of the moduli
+    if (huge)
+      store_moduli<OPERAND, 3, SYM, true>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    else
+      store_moduli<OPERAND, 2, SYM, true>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   } else if (huge) {
     store_moduli<OPERAND, 3, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   } else if (medium) {
@@ -754,7 +764,18 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
     const int64_t extent = fill_rows > 0 ? fill_rows : rb_count * 128 - row_base;
     const int n_kb = int((kdim + 127) / 128), n_rt = int((extent + kResRows - 1) / kResRows);
     const int64_t tiles = int64_t(n_kb) * n_rt;
-    const unsigned grid = unsigned(max_ctas > 0 && max_ctas < tiles ? max_ctas : tiles);
+    const unsigned grid1 = unsigned(max_ctas > 0 && max_ctas < tiles ? max_ctas : tiles);
+    // few tiles (small operands): split the moduli over gridDim.y CTAs per tile
+    static int nsm_r = [] {
+      int d = 0, v = 148;
+      cudaGetDevice(&d);
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+      return v;
+    }();
+    const int msplit = (max_ctas > 0 || tiles >= 2 * nsm_r)
+                           ? 1
+                           : int(std::min<int64_t>(dc.n, (2 * nsm_r + tiles - 1) / tiles));
+    const dim3 grid(grid1, unsigned(std::max(1, msplit)));
     // symmetric residues for the real path and the parity hook (dc.sym), the
     // 128-offset representative in the complex pipeline
     if (REAL || dc.sym) {
