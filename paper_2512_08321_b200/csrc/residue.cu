@@ -444,8 +444,10 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
   } else if (gridDim.y > 1) {  // small operands: this CTA's share of the moduli
     if (huge)
       store_moduli<OPERAND, 3, SYM, true>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
-    else
+    else if (medium)
       store_moduli<OPERAND, 2, SYM, true>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    else
+      store_moduli<OPERAND, 1, SYM, true>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   } else if (huge) {
     store_moduli<OPERAND, 3, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   } else if (medium) {
