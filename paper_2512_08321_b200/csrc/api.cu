@@ -124,14 +124,21 @@ bool pair_enabled() {
   return on;
 }
 
-// Wide 256 x 256 Karatsuba tiles (default); CRTG_GEMM=one selects the
-// 128 x 256 double-buffered kernel
-bool wide_enabled() {
-  static const bool on = [] {
+// Wide 256 x 256 Karatsuba tiles for large products; the 128 x 256
+// double-buffered kernel for short K loops (k < 8192) over fewer than 1024 wide
+// tiles, where its TMEM double buffer hides the epilogue and its twice-as-many
+// tiles fill the 148 SMs better (fast, N=14: 4096^3 3.15 vs 3.31 ms, 6144^3 8.73 vs
+// 8.93, 8192^3 19.6 vs 19.4, 16384^3 162 vs 136; tools/small_ab.py).
+// CRTG_GEMM=wide / one forces either kernel; all are bitwise identical.
+bool wide_enabled(const GemmArgs& g) {
+  static const int force = [] {
     const char* v = std::getenv("CRTG_GEMM");
-    return !(v && (std::string(v) == "one" || std::string(v) == "pair"));
+    if (!v) return -1;
+    const std::string s(v);
+    return s == "wide" ? 1 : (s == "one" || s == "pair") ? 0 : -1;
   }();
-  return on;
+  if (force >= 0) return force == 1;
+  return int64_t(g.kb) * 128 >= 8192 || int64_t(g.mt / 2) * g.nt >= 1024;
 }
 
 int env_int(const char* name, int dflt) {
@@ -148,7 +155,7 @@ int run_gemm(int mode, const GemmArgs& g0, cudaStream_t s) {
   if (pair_enabled() && mode != EPI_BOUND && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
     return launch_gemm_pair(mode, g, sm_count(), s);
   static const bool mc = env_int("CRTG_MC", 0) != 0;
-  if (wide_enabled() && (mode == EPI_KARATSUBA || mode == EPI_REAL) && (g.mt % 2) == 0 &&
+  if (wide_enabled(g) && (mode == EPI_KARATSUBA || mode == EPI_REAL) && (g.mt % 2) == 0 &&
       (g.mt0 % 2) == 0) {
     if (mc && mode == EPI_KARATSUBA && (g.nt % 2) == 0) return launch_gemm_wide_mc(g, sm_count(), s);
     return launch_gemm_wide(mode, g, sm_count(), s);

@@ -549,8 +549,13 @@ int launch_row_stats(int elem, bool fast, const void* A, int64_t lda, int64_t m,
 int launch_col_absmax(int elem, const void* B, int64_t ldb, int64_t k, int64_t n,
                       double* colabs, unsigned long long* diag, cudaStream_t s) {
   if (n <= 0) return 0;
-  const int rows_per_chunk = 1024;
-  dim3 grid(unsigned((n + 127) / 128), unsigned((k + rows_per_chunk - 1) / rows_per_chunk));
+  // enough row chunks for ~4 CTAs per SM (a narrow B at k = 1024 otherwise ran
+  // 8 CTAs of 1024-long chains: 216 us at 1024^3); atomicMax is order-free
+  const int64_t xb = (n + 127) / 128;
+  const int64_t chunks = std::max<int64_t>(1, (4 * 148 + xb - 1) / xb);
+  const int rows_per_chunk =
+      int(std::min<int64_t>(1024, std::max<int64_t>(16, round_up((k + chunks - 1) / chunks, 16))));
+  dim3 grid(unsigned(xb), unsigned((k + rows_per_chunk - 1) / rows_per_chunk));
   CRTG_ELEM_DISPATCH(elem, {
     k_col_absmax<T, R><<<grid, 128, 0, s>>>(static_cast<const T*>(B), ldb, int(k), int(n),
                                             rows_per_chunk, colabs, diag);
