@@ -180,6 +180,31 @@ cudaStream_t side_stream(cudaStream_t s) {
   return st;
 }
 
+// Small products (one column block, output 1024^2..4096^2) leave most SMs
+// idle in the latency-bound statistics and residue kernels, so B's column
+// statistics and residues run on a forked per-thread stream beside A's (joined
+// before the GEMM).  Bitwise neutral: the two chains are independent.  Fast,
+// N=14: 1024^3 245 -> 229 us, 2048^3 639 -> 620 us, 4096^3 3.08 -> 3.02 ms;
+// below 1024^2 the extra events cost more than the overlap gains, at 8192^2
+// it is noise (profiles/r01_fork_ab.jsonl).  CRTG_FORK=0 disables it.
+cudaStream_t fork_stream() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  thread_local std::map<int, cudaStream_t> streams;
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t st = nullptr;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  streams[dev] = st;
+  return st;
+}
+
+bool fork_wanted(int64_t m_pad, int64_t n_pad, int64_t n, int64_t nb) {
+  static const bool on = env_int("CRTG_FORK", 1) != 0;
+  const int64_t out = m_pad * n_pad;
+  return on && nb >= n && out >= int64_t(1024) * 1024 && out <= int64_t(4096) * 4096;
+}
+
 struct Events {
   std::vector<cudaEvent_t> ev;
   cudaEvent_t get() {
@@ -652,7 +677,7 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
 int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const void* B,
                  int64_t ldb, void* C, int64_t ldc, const DevConsts& dc, const int32_t* mu,
                  const int32_t* nu, void* ws, unsigned long long* dg, cudaStream_t s,
-                 cudaStream_t side, Events& E) {
+                 cudaStream_t side, Events& E, cudaStream_t first_b = nullptr) {
   const int64_t m = P.m, n = P.n, k = P.k;
   const int N = int(P.N);
   const bool in32 = (precision & CRTG_IN_C64) != 0;
@@ -679,12 +704,14 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
   auto eim = [&](int64_t j) { return at<int8_t>(ws, P.e_im) + (j % nbuf) * ebuf; };
   auto residues_b = [&](int64_t j, int max_ctas) -> int {
     const int64_t j0 = j * P.nb, w = std::min(P.nb, n - j0), w_pad = round_up(w, 256);
-    StageTimer timer(CRTG_STAGE_RESIDUE_B, side);
+    // block 0 may go to the caller's fork stream (small products)
+    cudaStream_t rs = (j == 0 && first_b) ? first_b : side;
+    StageTimer timer(CRTG_STAGE_RESIDUE_B, rs);
     CRTG_TRY(launch_pack(in32 ? E_C64 : E_C128, 1, PACK_RESIDUE, B, ldb, w, k, j0, nu + j0, dc, bpack(j),
-                         w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, side, max_ctas),
+                         w_pad * P.k_pad, w_pad / 128, dg + CRTG_DIAG_OVERFLOW_B, rs, max_ctas),
              "residues B");
     ev_r[j] = E.get();
-    return int(cudaEventRecord(ev_r[j], side));
+    return int(cudaEventRecord(ev_r[j], rs));
   };
   CRTG_TRY(residues_b(0, 0), "event");
   if (nblk > 1 && nbuf == 2) CRTG_TRY(residues_b(1, nsm), "event");
@@ -828,18 +855,22 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
   const DevConsts dc = make_dev(*K);
   Events E;
   cudaStream_t side = side_stream(s);
+  // B's chain (column statistics, residues of block 0) on `aux`
+  const bool forked = side == s && fork_wanted(P.m_pad, P.n_pad, n, P.nb);
+  cudaStream_t aux = forked ? fork_stream() : side;
   cudaEvent_t ev0 = E.get();
   CRTG_TRY(cudaEventRecord(ev0, s), "record");
-  CRTG_TRY(cudaStreamWaitEvent(side, ev0, 0), "wait");
-  if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s, side)) return e;
+  CRTG_TRY(cudaStreamWaitEvent(aux, ev0, 0), "wait");
+  if (int e = run_scaling(P, precision, mode, A, lda, B, ldb, dc, ws, dg, s, aux)) return e;
   if (mode == CRTG_ACCURATE) {  // exponents were produced on s
     cudaEvent_t ev1 = E.get();
     CRTG_TRY(cudaEventRecord(ev1, s), "record");
-    CRTG_TRY(cudaStreamWaitEvent(side, ev1, 0), "wait");
+    CRTG_TRY(cudaStreamWaitEvent(aux, ev1, 0), "wait");
   }
   int32_t* mu = at<int32_t>(ws, P.mu);
   int32_t* nu = at<int32_t>(ws, P.nu);
-  if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s, side, E))
+  if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s, side, E,
+                           forked ? aux : nullptr))
     return e;
   if (mu_out) CRTG_TRY(cudaMemcpyAsync(mu_out, mu, 4 * m, cudaMemcpyDeviceToDevice, s), "copy");
   if (nu_out) CRTG_TRY(cudaMemcpyAsync(nu_out, nu, 4 * n, cudaMemcpyDeviceToDevice, s), "copy");
