@@ -130,6 +130,39 @@ def test_split_moduli_equal_karatsuba_form(crt, tmp_path):
     assert res["0"] == res["1"]
 
 
+@pytest.mark.parametrize("knob,values", [("CRTG_FORK", ("0", "1")),
+                                         ("CRTG_GEMM", ("one", "wide"))])
+def test_launch_knobs_bitwise_neutral(crt, knob, values):
+    """Schedule choices are bitwise neutral: the forked B chain for small
+    products (CRTG_FORK) and the 128x256 vs 256x256 K3 kernels (CRTG_GEMM),
+    on shapes where the default picks the fork / the 128x256 kernel and one
+    with k >= 8192 where it picks the wide kernel."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import hashlib, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "import paper_2512_08321_b200 as crt\n"
+        "from oracle import ozaki2 as orc\n"
+        "out = []\n"
+        "for m, k, n, N, mode in ((1024, 1024, 1100, 14, 'fast'), (1024, 1024, 1100, 14, 'accurate'),\n"
+        "                         (256, 8192, 512, 15, 'fast')):\n"
+        "    a = orc.gen_matrix(m, k, 0.5, 5, 'double'); b = orc.gen_matrix(k, n, 0.5, 6, 'double')\n"
+        "    cfg = crt.EmuConfig(domain='complex', mode=mode, num_moduli=N)\n"
+        "    out.append(hashlib.sha256(crt.emulate_gemm_complex(a, b, cfg).tobytes()).hexdigest())\n"
+        "print(' '.join(out))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for v in values:
+        env = dict(os.environ, **{knob: v})
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        res[v] = r.stdout.strip().split()[-3:]
+    assert res[values[0]] == res[values[1]]
+
+
 def test_complex_gemm_mod_full_range_k_cap(crt):
     # extreme residues at the complex k cap: int32 D-E would overflow without
     # reducing D, E, F first (reference kernel.py:46-50)
