@@ -1782,8 +1782,8 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
       const int64_t a_plane = P.m_pad * P.k_pad, b_plane = P.n_pad * P.k_pad;
       int8_t* abars = at<int8_t>(ws, P.a_bars);
       int8_t* bbars = at<int8_t>(ws, P.b_bars);
-      // bars of a real operand: planes (A, 0, A) so the complex bound product
-      // max(cross + diff, cross) reduces to the real bound A*B (scaling.py:257-258)
+      // bars of a real operand: sum and difference planes are both A, so the
+      // complex bound (X + |D|)/2 reduces to the real bound A*B (scaling.py:257-258)
       CRTG_TRY(launch_pack(elem, a_colmajor ? 1 : 0, PACK_BARS, A, lda, m, k, 0, bar_mu, dc, abars,
                            a_plane, P.m_pad / 128, dg + CRTG_DIAG_OVERFLOW_A, s), "bars A");
       CRTG_TRY(launch_pack(elem, b_colmajor ? 0 : 1, PACK_BARS, B, ldb, n, k, 0, bar_nu, dc, bbars,

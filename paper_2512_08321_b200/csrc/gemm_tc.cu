@@ -18,8 +18,11 @@
 //     packed bytes in registers, and writes e_R = sym(D-E) and e_I = sym(F-D-E)
 //     as int8 — INT32 products never leave the SM.
 //   EPI_RAW: writes the int32 accumulators (parity hook for gemm_i8_i32).
-//   EPI_BOUND: cross = AI*BR + AR*BI (buffer 0) and diff = AD*BD (buffer 1);
-//     bound = max(cross+diff, cross); row / column maxima by atomicMax.
+//   EPI_BOUND: X = (AR+AI)*(BR+BI) (unsigned bytes, buffer 0) and D = AD*BD
+//     (buffer 1).  The reference's cross = AI*BR + AR*BI = (X - D)/2 and
+//     cross + diff = AR*BR + AI*BI = (X + D)/2, so its bound
+//     max(cross + diff, cross) (scaling.py:251-258) is exactly (X + |D|)/2:
+//     two products instead of three.  Row / column maxima by atomicMax.
 #include <cstdio>
 #include <cstdlib>
 
@@ -48,9 +51,8 @@ struct Seg {
 template <int MODE>
 __device__ __forceinline__ Seg seg_of(int s) {
   if (MODE == EPI_BOUND) {
-    // cross = AI*BR + AR*BI -> buffer 0; diff = AD*BD -> buffer 1 (scaling.py:251-256)
-    if (s == 0) return {1, 0, 0, 0};
-    if (s == 1) return {0, 1, 0, 1};
+    // X = AS*BS -> buffer 0 (unsigned); D = AD*BD -> buffer 1
+    if (s == 0) return {0, 0, 0, 0};
     return {2, 2, 1, 0};
   }
   return {s, s, -1, 0};
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm, tn;
       decode_tile(t, g, l, tm, tn);
-      const int nseg = MODE == EPI_BOUND ? 3 : tile_segments<MODE>(g, l);
+      const int nseg = MODE == EPI_BOUND ? 2 : tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const Seg sg = seg_of<MODE>(s);
         const int8_t* a = g.a + (int64_t)(l * g.planes_per_l + sg.a_plane) * g.a_plane;
@@ -129,13 +131,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     // unsigned operands (bits 7 / 10 clear): residues stored as t in [0, p)
-    const uint32_t idesc = g.unsigned_ops ? idesc_i8(128, 256) & ~((1u << 7) | (1u << 10))
-                                          : idesc_i8(128, 256);
+    const uint32_t idesc_s = idesc_i8(128, 256);
+    const uint32_t idesc_u = idesc_s & ~((1u << 7) | (1u << 10));
+    const uint32_t idesc = g.unsigned_ops ? idesc_u : idesc_s;
     uint32_t stage = 0, phase = 0, gslot = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm, tn;
       decode_tile(t, g, l, tm, tn);
-      const int nseg = MODE == EPI_BOUND ? 3 : tile_segments<MODE>(g, l);
+      const int nseg = MODE == EPI_BOUND ? 2 : tile_segments<MODE>(g, l);
       if (MODE == EPI_BOUND) {
         const uint32_t par = ((gslot >> 1) & 1) ^ 1;
         mbar_wait(smem_u32(&tempty_bar[0]), par);
@@ -163,7 +166,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
           for (int kk = 0; kk < 4; ++kk) {
             // advance 32 bytes of K inside the 128-byte swizzle atom
             if (MODE != EPI_RAW || g.repeat_mma >= 0)
-              mma_i8(d, ad + 2 * kk, bd + 2 * kk, idesc, (kb | kk | sg.accumulate) != 0);
+              mma_i8(d, ad + 2 * kk, bd + 2 * kk,
+                     (MODE == EPI_BOUND && s == 0) ? idesc_u : idesc,
+                     (kb | kk | sg.accumulate) != 0);
             if (MODE == EPI_RAW && g.repeat_mma > 0) {
               // power experiment: a second MMA on operands already in smem --
               // 1: same A and B, 2: same A / next B slice, 3: next A and B slices
@@ -176,8 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
         if (MODE == EPI_BOUND) {
-          if (s == 1) mma_commit(smem_u32(&tfull_bar[0]));
-          if (s == 2) mma_commit(smem_u32(&tfull_bar[1]));
+          mma_commit(smem_u32(&tfull_bar[s]));
         } else {
           mma_commit(smem_u32(&tfull_bar[buf]));
           ++gslot;
@@ -208,15 +212,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
         int32_t rmax = 0;
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
-          uint32_t cr[32], df[32];
-          tmem_ld32(lane_addr + c * 32, cr);
+          uint32_t xs[32], df[32];
+          tmem_ld32(lane_addr + c * 32, xs);
           tmem_ld32(lane_addr + 256 + c * 32, df);
           tmem_wait_ld();
           int32_t mine = 0;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            const int32_t cross = int32_t(cr[i]);
-            const int32_t bnd = max(cross + int32_t(df[i]), cross);
+            // X <= k * 128^2 <= 2^30 and |D| <= k * 64^2: no int32 overflow
+            const int32_t bnd = (int32_t(xs[i]) + abs(int32_t(df[i]))) >> 1;
             rmax = max(rmax, bnd);
             const int32_t cm = __reduce_max_sync(0xffffffffu, bnd);
             if (lane == i) mine = cm;

@@ -5,7 +5,7 @@
 //   quantize           scaling.py:277-293   a' = trunc(ldexp(a, e))
 //   residue_decompose  crt.py:199-218       r_l = sym(a' mod p_l) for every modulus
 //   Karatsuba sums     kernel.py:101-103    s_l = sym(r_re + r_im mod p_l)
-//   _bound_matrices    scaling.py:216-226   ceil(|x| 2^bar) and their difference
+//   _bound_matrices    scaling.py:216-226   ceil(|x| 2^bar): their sum and difference
 // Integer residues are exact for |a'| < 2^90: a' = M * 2^s with a 53-bit integer
 // significand M; M mod p is folded on 32-bit lanes through 2^32 mod p and
 // 2^16 mod p, then multiplied by 2^s mod p.  The congruence class equals the
@@ -84,23 +84,25 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
   const int64_t goff = (int64_t(kb) * rb_count + (r0 >> 7)) * kBlockBytes + (r0 & 127) * 128;
 
   {
-    // bound operands: ceil(|x| 2^bar) in [0, 64] and their difference
-    uint32_t w[3][4] = {};
+    // bound operands from R = ceil(|re| 2^bar), I = ceil(|im| 2^bar) in [0, 64]:
+    // plane 0 the sum R + I in [0, 128] (an unsigned byte), plane 2 the
+    // difference R - I in [-64, 64]; plane 1 is not used (the bound GEMM
+    // needs the two products (R+I)(R'+I') and (R-I)(R'-I'), gemm_tc.cu)
+    uint32_t w[2][4] = {};
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
       const int vr = int(ceil(ldexp_rn(fabs(re[t]), e)));
       const int vi = int(ceil(ldexp_rn(fabs(im[t]), e)));
-      w[0][t >> 2] |= uint32_t(vr & 0xFF) << (8 * (t & 3));
-      w[1][t >> 2] |= uint32_t(vi & 0xFF) << (8 * (t & 3));
-      w[2][t >> 2] |= uint32_t((vr - vi) & 0xFF) << (8 * (t & 3));
+      w[0][t >> 2] |= uint32_t((vr + vi) & 0xFF) << (8 * (t & 3));
+      w[1][t >> 2] |= uint32_t((vr - vi) & 0xFF) << (8 * (t & 3));
     }
 #pragma unroll
-    for (int q = 0; q < 3; ++q)
+    for (int q = 0; q < 2; ++q)
       *reinterpret_cast<uint4*>(&stage[q][soff]) = make_uint4(w[q][0], w[q][1], w[q][2], w[q][3]);
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 3; ++q)
-      reinterpret_cast<uint4*>(out + q * plane_bytes + goff)[threadIdx.x] =
+    for (int q = 0; q < 2; ++q)
+      reinterpret_cast<uint4*>(out + 2 * q * plane_bytes + goff)[threadIdx.x] =
           reinterpret_cast<const uint4*>(stage[q])[threadIdx.x];
   }
 }
