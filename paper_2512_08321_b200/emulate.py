@@ -238,7 +238,8 @@ def run_complex(at: torch.Tensor, bt: torch.Tensor, cfg: EmuConfig,
     odt = torch.complex64 if cfg.precision == "single" else torch.complex128
     if out is None:
         out = torch.empty((m, n), dtype=odt, device=dev)
-    diag = torch.zeros(nat.DIAG_LEN, dtype=torch.int64, device=dev)
+    # crtg_gemm_complex zeroes the counters on the stream itself
+    diag = torch.empty(nat.DIAG_LEN, dtype=torch.int64, device=dev)
     mu = torch.empty(m, dtype=torch.int32, device=dev) if return_exponents else None
     nu = torch.empty(n, dtype=torch.int32, device=dev) if return_exponents else None
     nat.call("crtg_gemm_complex", prec, mode, m, n, k, at.data_ptr(), at.stride(0),
