@@ -322,7 +322,10 @@ __device__ __forceinline__ uint32_t pack_real(const Val3 (&v)[8], int i0, const 
                       res_t<FORM>(v[i0 + 3], c), c.off);
 }
 
-template <typename T, int OPERAND, bool REAL, bool SYM>
+// MS: the moduli are split over gridDim.y CTAs per tile (small operands); a
+// separate instantiation so the large-operand kernel does not carry the extra
+// register pressure
+template <typename T, int OPERAND, bool REAL, bool SYM, bool MS = false>
 __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __restrict__ X, int64_t ldx, int rows,
                                                   int kdim, int64_t col0,
                                                   const int32_t* __restrict__ exps,
@@ -419,7 +422,7 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
   if constexpr (REAL) {
     // one plane per modulus (emulate_gemm_real: no imaginary part / Karatsuba sum)
     for (int l = 0; l < dc.n; ++l) {
-      if (gridDim.y > 1 && l % int(gridDim.y) != int(blockIdx.y)) continue;
+      if (MS && l % int(gridDim.y) != int(blockIdx.y)) continue;
       const ResConst c = dc.rc[l];
       uint32_t w0, w1;
       if (huge) {
@@ -443,19 +446,12 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
         __syncthreads();
       }
     }
-  } else if (gridDim.y > 1) {  // small operands: this CTA's share of the moduli
-    if (huge)
-      store_moduli<OPERAND, 3, SYM, true>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
-    else if (medium)
-      store_moduli<OPERAND, 2, SYM, true>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
-    else
-      store_moduli<OPERAND, 1, SYM, true>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
-  } else if (huge) {
-    store_moduli<OPERAND, 3, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+  } else if (huge) {  // MS: this CTA's share of the moduli
+    store_moduli<OPERAND, 3, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   } else if (medium) {
-    store_moduli<OPERAND, 2, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    store_moduli<OPERAND, 2, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   } else {
-    store_moduli<OPERAND, 1, SYM>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    store_moduli<OPERAND, 1, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
   }
   }  // tile loop
 }
@@ -782,10 +778,12 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
     const dim3 grid(grid1, unsigned(std::max(1, msplit)));
     // symmetric residues for the real path and the parity hook (dc.sym), the
     // 128-offset representative in the complex pipeline
+#define CRTG_RES_LAUNCH(R, S, M)                                                              \
+  k_residues<T, OP, R, S, M><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),      \
+                                                  int(kdim), col0, exps, dc, out, plane_bytes,   \
+                                                  rb_count, overflow, n_kb, n_rt, int(row_base))
     if (REAL || dc.sym) {
-      k_residues<T, OP, REAL, true><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),
-                                                        int(kdim), col0, exps, dc, out, plane_bytes,
-                                                        rb_count, overflow, n_kb, n_rt, int(row_base));
+      if (msplit > 1) CRTG_RES_LAUNCH(REAL, true, true); else CRTG_RES_LAUNCH(REAL, true, false);
     } else if (tc_residues_enabled()) {
       // persistent: 3 CTAs per SM (128 TMEM columns each), grid-stride over tiles
       static int nsm = [] {
@@ -802,11 +800,12 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
       k_residues_tc<T, OP><<<g2, 256, smem, s>>>(static_cast<const T*>(X), ldx, int(rows),
                                                  int(kdim), col0, exps, dc, out, plane_bytes,
                                                  rb_count, overflow, n_kb, n_rt, int(row_base));
-    } else
-      k_residues<T, OP, false, false><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),
-                                                          int(kdim), col0, exps, dc, out, plane_bytes,
-                                                          rb_count, overflow, n_kb, n_rt,
-                                                          int(row_base));
+    } else if (msplit > 1) {
+      CRTG_RES_LAUNCH(false, false, true);
+    } else {
+      CRTG_RES_LAUNCH(false, false, false);
+    }
+#undef CRTG_RES_LAUNCH
   } else {
   // cover every padded row of the plane so the GEMM reads zeros there
   dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kTileRows));
