@@ -21,7 +21,7 @@
 #define CRTG_CRT_UNROLL 0
 #endif
 #ifndef CRTG_CRT_BATCH
-#define CRTG_CRT_BATCH 6
+#define CRTG_CRT_BATCH 8
 #endif
 
 namespace crtg {
