@@ -69,8 +69,15 @@ def parse():
                     help="cfg5 strong scaling: ONE product of --shape (default 32768^3) sharded "
                          "by output tiles over the ranks; rank 0 holds A and B, scatters the "
                          "row / column blocks and gathers C over NCCL inside the timed step")
-    ap.add_argument("--cpu-sample", type=int, default=128,
+    ap.add_argument("--no-strong", action="store_true",
+                    help="N>1: skip the cfg5 strong-scaling (one sharded 32768^3 product) leg")
+    ap.add_argument("--strong-size", type=int, default=32768)
+    ap.add_argument("--strong-steps", type=int, default=3)
+    ap.add_argument("--strong-warmup", type=int, default=1)
+    ap.add_argument("--cpu-sample", type=int, default=64,
                     help="rows/cols of the CPU sample block (k kept full)")
+    ap.add_argument("--no-cpu-cfg1", action="store_true",
+                    help="reference arm: skip the full cfg1 (1024^3) CPU runs")
     a = ap.parse_args()
     if a.strong and a.shape == [16384, 16384, 16384]:
         a.shape = [32768, 32768, 32768]
@@ -155,6 +162,14 @@ def profile_traffic():
         return None
 
 
+def fingerprint(torch, t) -> int:
+    """Order-independent 64-bit signature of a tensor's bytes (wrapping int64 sum
+    of its words and of the words times their index)."""
+    w = t.reshape(-1).view(torch.int64)
+    idx = torch.arange(w.numel(), device=w.device, dtype=torch.int64)
+    return (int(w.sum().item()) ^ (int((w * idx).sum().item()) << 1)) & ((1 << 64) - 1)
+
+
 def synth(torch, rows, cols, phi, seed, dtype, dev):
     """(u - 0.5) * exp(z * phi) per part, the reference generator's distribution
     (bench.py:50-54 there), drawn on the device."""
@@ -170,37 +185,107 @@ def synth(torch, rows, cols, phi, seed, dtype, dev):
 
 
 # --------------------------------------------------------------------------- CPU leg
-def cpu_sample(a, reps: int = 1):
-    """The reference algorithm on the host cores (oracle port, float64-BLAS INT8
-    engine): a row/column-local block `s x s x k` of the same product."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def load_reference():
+    """The UNMODIFIED reference package `crtgemm`, pip-installed into
+    baseline/_ref.  -> (module, kind); falls back to the
+    oracle port (kind "port") only if the install is absent."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "crtg_numba_cache"))
+    if os.path.isdir(os.path.join(REF_DIR, "crtgemm")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        try:
+            import crtgemm  # noqa: F401
+            return crtgemm, "reference"
+        except Exception as e:  # pragma: no cover - reported in the line
+            print(f"reference import failed ({e!r}); timing the oracle port", file=sys.stderr)
+    return None, "port"
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _ref_call(ref, kind, A, B, a, num_moduli, mode, prec):
+    if kind == "reference":
+        cfg = ref.EmuConfig(precision=prec, domain="complex", mode=mode, num_moduli=num_moduli)
+        return ref.emulate_gemm_complex(A, B, cfg)
     from oracle import ozaki2 as orc
+    return orc.emulate_complex(A, B, num_moduli, mode, prec)
+
+
+def _ref_inputs(ref, kind, rows, k, cols, phi, prec, seed):
+    if kind == "reference":
+        A = ref.gen_matrix(ref.GenSpec(rows, k, phi, seed, prec, "complex"))
+        B = ref.gen_matrix(ref.GenSpec(k, cols, phi, seed + 1, prec, "complex"))
+        return A, B
+    from oracle import ozaki2 as orc
+    return orc.gen_matrix(rows, k, phi, seed, prec), orc.gen_matrix(k, cols, phi, seed + 1, prec)
+
+
+def cpu_sample(a, reps: int = 1, ref=None, kind=None):
+    """The reference's own CPU implementation (crtgemm.emulate_gemm_complex from
+    baseline/_ref: numpy + OpenBLAS + numba on all host threads) on a bounded
+    row/column-local block `s x s x k` of the same product (k kept full; fast
+    mode's exponents are row/column local, so the block is the same work per
+    output element as the full product)."""
+    if ref is None and kind is None:
+        ref, kind = load_reference()
     s = min(a.cpu_sample, a.m, a.n)
     prec = a.precision
-    A = orc.gen_matrix(s, a.k, a.phi, 11, prec)
-    B = orc.gen_matrix(a.k, s, a.phi, 12, prec)
+    A, B = _ref_inputs(ref, kind, s, a.k, s, a.phi, prec, 11)
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        orc.emulate_complex(A, B, a.moduli, a.mode, prec)
+        _ref_call(ref, kind, A, B, a, a.moduli, a.mode, prec)
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
     return {"value": 8.0 * s * s * a.k / t / 1e12, "unit": UNIT, "cores": os.cpu_count(),
-            "kind": "port",
+            "kind": kind, "cpu_model": cpu_model(),
+            "impl": ("crtgemm.emulate_gemm_complex (unmodified reference, baseline/_ref)"
+                     if kind == "reference" else "oracle port (reference not installed)"),
             "sample": f"{s}x{s}x{a.k} block of the {a.m}x{a.n}x{a.k} product "
                       f"({a.mode}, N={a.moduli}, phi={a.phi}), median of {reps}, "
-                      f"{t:.2f} s each, numpy+OpenBLAS on {os.cpu_count()} threads"}
+                      f"{t:.2f} s each, on {os.cpu_count()} host threads"}
+
+
+def cpu_cfg1(ref, kind):
+    """BASELINE.md section 2's CPU reference run: cfg1 = ZGEMM 1024^3, N=14,
+    phi=0.5, seeds 0/1, fast and accurate, the FULL product (one call each
+    after a warm-up call)."""
+    A, B = _ref_inputs(ref, kind, 1024, 1024, 1024, 0.5, "double", 0)
+    res = {}
+    for mode in ("fast", "accurate"):
+        _ref_call(ref, kind, A, B, None, 14, mode, "double")
+        t0 = time.perf_counter()
+        _ref_call(ref, kind, A, B, None, 14, mode, "double")
+        t = time.perf_counter() - t0
+        res[mode] = {"seconds": t, "tflops": 8.0 * 1024 ** 3 / t / 1e12}
+    return {"workload": "zgemm_1024x1024x1024_N14 (cfg1), full product", **res}
 
 
 def run_reference(a, rank: int):
+    """`--impl reference`: the reference's own CPU path on the host cores, rank 0
+    only (other ranks exit without work)."""
     if rank != 0:
         return
-    base = cpu_sample(a, reps=1)  # warm numpy/BLAS
+    ref, kind = load_reference()
+    for _ in range(max(1, a.warmup)):
+        cpu_sample(a, ref=ref, kind=kind)  # warm numpy / BLAS / numba
     vals = []
-    for _ in range(max(0, a.warmup - 1)):
-        cpu_sample(a)
     for _ in range(a.steps):
-        vals.append(cpu_sample(a)["value"])
+        vals.append(cpu_sample(a, ref=ref, kind=kind)["value"])
     v = statistics.median(vals)
+    base = cpu_sample(a, ref=ref, kind=kind)
     s = min(a.cpu_sample, a.m, a.n)
     ms = 8.0 * s * s * a.k / (v * 1e12) * 1e3
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
@@ -211,8 +296,11 @@ def run_reference(a, rank: int):
                        "num_moduli": a.moduli, "mode": a.mode, "precision": a.precision,
                        "phi": a.phi},
             "impl": "reference",
-            "cpu_baseline": {**base, "value": v},
+            "cpu_baseline": {**base, "value": v,
+                             "sample": f"each step: {base['sample'].split(', median')[0]}"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not a.no_cpu_cfg1:
+        line["cpu_baseline"]["cfg1"] = cpu_cfg1(ref, kind)
     print(json.dumps(line), flush=True)
 
 
@@ -227,14 +315,7 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     ndev = torch.cuda.device_count()
     dev = torch.device("cuda", local_rank % max(ndev, 1))
     torch.cuda.set_device(dev)
-    if world > 1:
-        # NCCL over NVLink on the box; CRTG_BENCH_BACKEND=gloo lets the multi-rank
-        # logic be exercised with several ranks sharing one GPU (CI only)
-        backend = os.environ.get("CRTG_BENCH_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
+    init_dist(world, dev)
     # 2-D grid of output tiles for weak scaling
     R = 1 << (int(math.log2(world)) // 2)
     Cc = world // R
@@ -248,7 +329,17 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     ws = None
     out = torch.empty((a.m, a.n), dtype=cdt, device=dev)
 
+    emu = None
+    if world > 1 and a.mode == "accurate":
+        # accurate mode: exponents are global over the grid row / column -> the
+        # MAX all-reduce of the bound maxima (dist.ShardedEmulator)
+        from paper_2512_08321_b200 import dist as cdist
+        emu = cdist.ShardedEmulator(cfg, cdist.TileGrid(R, Cc), rank)
+
     def step():
+        if emu is not None:
+            out.copy_(emu.tile(A, B, sync_check=False))
+            return
         crt.run_complex(A, B, cfg, None, dev, sync_check=False, ws=ws_holder[0], out=out)
 
     ws_holder = [None]
@@ -351,17 +442,21 @@ def run_ours(a, rank: int, world: int, local_rank: int):
               "roofline": roof, "clocks": clocks}
 
     # cuBLAS native baseline on the same device (rank 0)
+    # fingerprint of the emulated result: nothing below may write into `out`
+    # (asserted before its error is computed)
+    out_sig = fingerprint(torch, out)
     if rank == 0 and not a.no_native:
         torch.backends.cuda.matmul.allow_tf32 = False
+        nat_out = torch.empty_like(out)  # cuBLAS writes its own buffer
         for _ in range(2):
-            torch.matmul(A, B, out=out)
+            torch.matmul(A, B, out=nat_out)
         torch.cuda.synchronize()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
         reps = 3
         f0.record(stream)
         for _ in range(reps):
-            torch.matmul(A, B, out=out)
+            torch.matmul(A, B, out=nat_out)
         f1.record(stream)
         torch.cuda.synchronize()
         nat_ms = f0.elapsed_time(f1) / reps
@@ -369,6 +464,8 @@ def run_ours(a, rank: int, world: int, local_rank: int):
         result["native_cublas"] = {"op": "torch.matmul " + str(cdt).replace("torch.", ""),
                                    "ms": nat_ms, "tflops": nat_tf,
                                    "speedup_per_gpu": (value / world) / nat_tf}
+    else:
+        nat_out = None
 
     # the reference's EmuConfig default (N=14) on the same inputs, for context
     if rank == 0 and a.moduli != 14 and a.precision == "double" and a.mode == "fast":
@@ -398,16 +495,22 @@ def run_ours(a, rank: int, world: int, local_rank: int):
         ref = acc.reference_gemm_dd(A.to(torch.complex128), B.to(torch.complex128))
         torch.cuda.synchronize()
         t_dd = time.time() - t0
-        native = torch.matmul(A, B)
+        native = nat_out if nat_out is not None else torch.matmul(A, B)
+        if fingerprint(torch, out) != out_sig:
+            raise RuntimeError("the emulated result buffer changed after the timed steps")
+        if torch.equal(out, native):
+            raise RuntimeError("accuracy leg: emulated and cuBLAS results are the same tensor")
         accr = {"metric": "max relative error over all entries (reference oracle.py:131-169)",
                 "reference": "GPU double-double GEMM, bit-identical to reference_gemm_dd",
                 "emulated": acc.max_relative_error(out, ref),
-                "native_cublas": acc.max_relative_error(native, ref), "dd_seconds": t_dd}
+                "native_cublas": acc.max_relative_error(native, ref), "dd_seconds": t_dd,
+                "emulated_buffer": f"written only by the timed steps (fingerprint {out_sig:#x} "
+                                   "checked); cuBLAS wrote a separate buffer"}
         if out14 is not None:
             accr["emulated_N14"] = acc.max_relative_error(out14, ref)
         accr["emulated_le_native"] = accr["emulated"] <= accr["native_cublas"]
         result["accuracy"] = accr
-        del ref, native
+        del ref, native, nat_out
         torch.cuda.empty_cache()
 
     # the north star's CGEMM target at the same shape: emulated CGEMM (complex64,
@@ -496,6 +599,17 @@ def run_ours(a, rank: int, world: int, local_rank: int):
                          "api": "paper_2512_08321_b200.emulate_gemm_complex(pinned host tensors)"
                                 " -> crtg_gemm_complex_host (A row chunks / B column blocks streamed in a staircase, C tiles back, on the copy engines)"}
 
+    # cfg5 (BASELINE configs[4]) at N > 1: ONE 32768^3 product sharded by output
+    # tiles, NCCL scatter + tiles + gather inside each step
+    if world > 1 and not a.no_strong:
+        del A, B, out
+        ws_holder[0] = None
+        torch.cuda.empty_cache()
+        m5 = a.strong_size
+        result["strong_cfg5"] = strong_measure(a, rank, world, dev, m5, m5, m5,
+                                               a.strong_steps, a.strong_warmup,
+                                               sample_clocks=False)
+
     if rank == 0 and world == 1 and not a.no_cpu:
         result["cpu_baseline"] = cpu_sample(a, reps=1)
     if rank == 0:
@@ -505,12 +619,26 @@ def run_ours(a, rank: int, world: int, local_rank: int):
         dist.destroy_process_group()
 
 
-def run_strong(a, rank: int, world: int, local_rank: int):
+def init_dist(world: int, dev):
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        # NCCL over NVLink on the box; CRTG_BENCH_BACKEND=gloo lets the multi-rank
+        # logic be exercised with several ranks sharing one GPU (CI only)
+        backend = os.environ.get("CRTG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+
+def strong_measure(a, rank: int, world: int, dev, m: int, n: int, k: int, steps: int,
+                   warmup: int, sample_clocks: bool = True) -> dict:
     """cfg5: one (m x k) @ (k x n) product sharded by output tiles over `world`
     ranks (paper_2512_08321_b200.dist).  The timed step is what a caller of the
     sharded product pays with operands resident on rank 0: scatter of A's row
-    blocks and B's column blocks (NCCL send/recv over NVLink), each rank's tile,
-    gather of C to rank 0.  Tile compute alone is reported beside it."""
+    blocks and B's column blocks (NCCL over NVLink), each rank's tile (accurate
+    mode: with the MAX all-reduce of the bound maxima), gather of C to rank 0
+    (grouped receives).  Tile compute alone is reported beside it."""
     import torch
     import torch.distributed as dist
 
@@ -518,23 +646,14 @@ def run_strong(a, rank: int, world: int, local_rank: int):
     from paper_2512_08321_b200 import _native as nat
     from paper_2512_08321_b200 import dist as cdist
 
-    ndev = torch.cuda.device_count()
-    dev = torch.device("cuda", local_rank % max(ndev, 1))
-    torch.cuda.set_device(dev)
-    if world > 1:
-        backend = os.environ.get("CRTG_BENCH_BACKEND", "nccl")
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(backend)
     grid = cdist.TileGrid.for_world(world)
     cdt = torch.complex128 if a.precision == "double" else torch.complex64
     cfg = crt.EmuConfig(precision=a.precision, domain="complex", mode=a.mode,
                         num_moduli=a.moduli, n_block=a.n_block)
     A = B = None
     if rank == 0:
-        A = synth(torch, a.m, a.k, a.phi, 1000, cdt, dev)
-        B = synth(torch, a.k, a.n, a.phi, 2000, cdt, dev)
+        A = synth(torch, m, k, a.phi, 1000, cdt, dev)
+        B = synth(torch, k, n, a.phi, 2000, cdt, dev)
     emu = cdist.ShardedEmulator(cfg, grid, rank) if world > 1 else None
     groups = emu.groups if (emu and emu.groups) else (
         cdist.TileGroups(grid, rank) if world > 2 else None)
@@ -554,7 +673,7 @@ def run_strong(a, rank: int, world: int, local_rank: int):
             t1.record()
             tile_ms.append((t0, t1))
             return
-        a_loc, b_loc = cdist.scatter_operands(A, B, grid, rank, a.m, a.n, a.k, cdt, dev,
+        a_loc, b_loc = cdist.scatter_operands(A, B, grid, rank, m, n, k, cdt, dev,
                                               groups=groups)
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -562,28 +681,26 @@ def run_strong(a, rank: int, world: int, local_rank: int):
         c_loc = emu.tile(a_loc, b_loc, sync_check=False)
         t1.record()
         tile_ms.append((t0, t1))
-        cdist.gather_tiles(c_loc, grid, rank, a.m, a.n)
+        cdist.gather_tiles(c_loc, grid, rank, m, n)
 
-    for _ in range(a.warmup):
+    for _ in range(warmup):
         step()
     barrier()
     tile_ms.clear()
-    nat.profile_enable(True)
-    nat.profile_read()
     launches0 = nat.launch_count()
-    sampler = ClockSampler(dev.index)
-    sampler.start()
+    sampler = ClockSampler(dev.index) if sample_clocks else None
+    if sampler:
+        sampler.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record()
-    for _ in range(a.steps):
+    for _ in range(steps):
         step()
     e1.record()
     barrier()
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler else None
     launches = nat.launch_count() - launches0
-    nat.profile_enable(False)
 
     def max_over_ranks(x: float) -> float:
         if world == 1:
@@ -593,26 +710,42 @@ def run_strong(a, rank: int, world: int, local_rank: int):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    ms_step = max_over_ranks(e0.elapsed_time(e1)) / a.steps
-    ms_tile = max_over_ranks(sum(x.elapsed_time(y) for x, y in tile_ms)) / a.steps
-    flops = 8.0 * a.m * a.n * a.k
-    result = {"metric": METRIC_STRONG, "value": flops / (ms_step * 1e-3) / 1e12, "unit": UNIT,
-              "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
-              "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-              "dtype": "int8 tensor / f64" if a.precision == "double" else "int8 tensor / f32",
-              "data": "synthetic (u-0.5)*exp(z*phi), drawn on device (rank 0)",
-              "config": {"workload": f"zgemm_{a.m}x{a.n}x{a.k}_{a.mode}_N{a.moduli}_sharded"
-                                     if a.precision == "double" else
-                                     f"cgemm_{a.m}x{a.n}x{a.k}_{a.mode}_N{a.moduli}_sharded",
-                         "m": a.m, "n": a.n, "k": a.k, "num_moduli": a.moduli, "mode": a.mode,
-                         "grid": f"{grid.R}x{grid.C}", "parallelism": f"output-tile x{world}",
-                         "l2": "operands far larger than the 126 MB L2; no flush"},
-              "tile_compute_ms": ms_tile,
-              "tile_compute_tflops": flops / (ms_tile * 1e-3) / 1e12,
-              "comm_ms": ms_step - ms_tile,
-              "gpu_launches": int(launches), "clocks": clocks}
+    ms_step = max_over_ranks(e0.elapsed_time(e1)) / steps
+    ms_tile = max_over_ranks(sum(x.elapsed_time(y) for x, y in tile_ms)) / steps
+    flops = 8.0 * m * n * k
+    kind = "zgemm" if a.precision == "double" else "cgemm"
+    res = {"metric": METRIC_STRONG, "value": flops / (ms_step * 1e-3) / 1e12, "unit": UNIT,
+           "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": ms_step,
+           "higher_is_better": True, "scaling": "strong",
+           "config": {"workload": f"{kind}_{m}x{n}x{k}_{a.mode}_N{a.moduli}_sharded",
+                      "m": m, "n": n, "k": k, "num_moduli": a.moduli, "mode": a.mode,
+                      "grid": f"{grid.R}x{grid.C}", "parallelism": f"output-tile x{world}",
+                      "l2": "operands far larger than the 126 MB L2; no flush"},
+           "tile_compute_ms": ms_tile,
+           "tile_compute_tflops": flops / (ms_tile * 1e-3) / 1e12,
+           "comm_ms": ms_step - ms_tile, "gpu_launches": int(launches)}
+    if clocks is not None:
+        res["clocks"] = clocks
+    del A, B
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_strong(a, rank: int, world: int, local_rank: int):
+    """`--strong`: the cfg5 line on its own (default 32768^3)."""
+    import torch
+    import torch.distributed as dist
+
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", local_rank % max(ndev, 1))
+    torch.cuda.set_device(dev)
+    init_dist(world, dev)
+    res = strong_measure(a, rank, world, dev, a.m, a.n, a.k, a.steps, a.warmup)
+    res.update({"vs_baseline": None,
+                "dtype": "int8 tensor / f64" if a.precision == "double" else "int8 tensor / f32",
+                "data": "synthetic (u-0.5)*exp(z*phi), drawn on device (rank 0)"})
     if rank == 0:
-        print(json.dumps(result), flush=True)
+        print(json.dumps(res), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

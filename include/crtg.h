@@ -201,7 +201,11 @@ int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim,
                   uint64_t* diag, void* stream);
 
 /* Exact int8 x int8 -> int32 on tcgen05 (replaces gemm_i8_i32,
- * kernel.py:20-35).  A: m x k row-major, B: k x n row-major, C: m x n. */
+ * kernel.py:20-35).  A: m x k row-major, B: k x n row-major, C: m x n.
+ * k <= 65536, where |C| <= k * 128^2 <= 2^30 cannot overflow (CRTG_ERR_DIMENSION
+ * above).  The reference accepts k <= 2^17 and raises ArithmeticError when an
+ * entry leaves int32 (kernel.py:30-34); callers split larger k into two calls
+ * and check the int64 sum, as paper_2512_08321_b200.gemm_i8_i32 does. */
 size_t crtg_i8_workspace_size(int64_t m, int64_t n, int64_t k, int nplanes);
 int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A,
                      const int8_t* B, int32_t* C, void* ws, size_t ws_bytes,

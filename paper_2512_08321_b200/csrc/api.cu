@@ -97,33 +97,6 @@ int sm_count() {
   return n;
 }
 
-// Overlap of B's statistics / residues and the CRT with the GEMM on a side
-// stream.  Measured on B200 (profiles/r01_overlap_experiment.json): the GEMM is
-// power-capped (sw_power_cap, ~1.3 GHz), so co-running integer/FP64 work steals
-// its clock and the step got slower (190 vs 163 ms).  Off by default; opt in
-// with CRTG_OVERLAP=1.
-bool overlap_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("CRTG_OVERLAP");
-    return v && v[0] == '1';
-  }();
-  return on;
-}
-
-// K3 kernel choice.  Default: the 1-CTA 128x256 kernel (gemm_tc.cu).  The
-// CTA-pair kernel (cta_group::2, 256x256, gemm_pair.cu; CRTG_GEMM=pair) is
-// bit-identical and moves a third less L2->SMEM data, but measured no faster
-// on B200 (148 vs 152 ms/GEMM-step, both at the sw_power_cap clock): the
-// kernel is bound by MAC energy under the 1 kW cap
-// (profiles/r01_gemm_pair_experiment.json).
-bool pair_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("CRTG_GEMM");
-    return v && std::string(v) == "pair";
-  }();
-  return on;
-}
-
 // Wide 256 x 256 Karatsuba tiles for large products; the 128 x 256
 // double-buffered kernel for short K loops (k < 8192) over fewer than 1024 wide
 // tiles, where its TMEM double buffer hides the epilogue and its twice-as-many
@@ -135,7 +108,7 @@ bool wide_enabled(const GemmArgs& g) {
     const char* v = std::getenv("CRTG_GEMM");
     if (!v) return -1;
     const std::string s(v);
-    return s == "wide" ? 1 : (s == "one" || s == "pair") ? 0 : -1;
+    return s == "wide" ? 1 : s == "one" ? 0 : -1;
   }();
   if (force >= 0) return force == 1;
   return int64_t(g.kb) * 128 >= 8192 || int64_t(g.mt / 2) * g.nt >= 1024;
@@ -152,33 +125,15 @@ int run_gemm(int mode, const GemmArgs& g0, cudaStream_t s) {
   GemmArgs g = g0;
   static const int group_m = env_int("CRTG_GROUP_M", 0);
   g.group_m = group_m;
-  if (pair_enabled() && mode != EPI_BOUND && (g.mt % 2) == 0 && (g.mt0 % 2) == 0)
-    return launch_gemm_pair(mode, g, sm_count(), s);
-  static const bool mc = env_int("CRTG_MC", 0) != 0;
   if (wide_enabled(g) && (mode == EPI_KARATSUBA || mode == EPI_REAL) && (g.mt % 2) == 0 &&
-      (g.mt0 % 2) == 0) {
-    if (mc && mode == EPI_KARATSUBA && (g.nt % 2) == 0) return launch_gemm_wide_mc(g, sm_count(), s);
+      (g.mt0 % 2) == 0)
     return launch_gemm_wide(mode, g, sm_count(), s);
-  }
   return launch_gemm(mode, g, sm_count(), s);
 }
 
-// per-thread, per-device non-blocking side stream (overlap mode only); the
-// caller's stream otherwise
-cudaStream_t side_stream(cudaStream_t s) {
-  if (!overlap_enabled()) return s;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  thread_local std::map<int, cudaStream_t> streams;
-  auto it = streams.find(dev);
-  if (it != streams.end()) return it->second;
-  cudaStream_t st = nullptr;
-  int lo = 0, hi = 0;
-  cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, lo);
-  streams[dev] = st;
-  return st;
-}
+// B's chain runs on the caller's stream (a side stream co-running with the
+// power-capped GEMM lowered its clock: 190 vs 163 ms)
+cudaStream_t side_stream(cudaStream_t s) { return s; }
 
 // Small products (one column block, output 1024^2..4096^2) leave most SMs
 // idle in the latency-bound statistics and residue kernels, so B's column
@@ -528,10 +483,6 @@ Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_b
   p.k_pad = round_up(std::max<int64_t>(k, 1), 128);
   int64_t nb = n_block < 1 ? n : n_block;
   nb = std::min(round_up(nb, 256), p.n_pad);
-  // at least 4 column blocks for large n so residues / CRT of neighbouring
-  // blocks overlap the GEMM (bitwise neutral: every column is independent)
-  if (overlap_enabled() && p.n_pad >= 8192)
-    nb = std::min(nb, std::max<int64_t>(2048, round_up((n + 3) / 4, 256)));
   p.nb = nb;
   p.nb_pad = nb;
   add(p, p.diag, 8 * CRTG_DIAG_LEN);
@@ -542,7 +493,7 @@ Plan make_plan(int mode, int64_t m, int64_t n, int64_t k, int64_t N, int64_t n_b
   add(p, p.colsq, 16 * p.n_pad);
   add(p, p.tree, tree_bytes(k));
   add(p, p.a_pack, size_t(real ? N : 3 * N) * p.m_pad * p.k_pad);
-  const int nbuf = (overlap_enabled() && p.nb < p.n) ? 2 : 1;  // double buffers (overlap)
+  const int nbuf = 1;
   const int ppm = real ? 1 : 3;  // planes per modulus
   add(p, p.b_pack, size_t(nbuf) * size_t(ppm * N) * p.nb_pad * p.k_pad);
   add(p, p.e_re, size_t(nbuf) * size_t(N) * m * p.nb_pad);
@@ -917,7 +868,8 @@ size_t crtg_i8_workspace_size(int64_t m, int64_t n, int64_t k, int nplanes) {
 int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A, const int8_t* B, int32_t* C,
                      void* ws, size_t ws_bytes, void* stream) {
   if (m < 1 || n < 1 || k < 1) return fail(CRTG_ERR_DIMENSION, "m, n, k must be positive");
-  if (k > 131072) return fail(CRTG_ERR_DIMENSION, "inner dimension exceeds 131072");
+  // k * 128^2 <= 2^30: no int32 wrap is possible (larger k: two calls, int64 sum)
+  if (k > 65536) return fail(CRTG_ERR_DIMENSION, "inner dimension exceeds 65536");
   if (ws_bytes < crtg_i8_workspace_size(m, n, k, 1))
     return fail(CRTG_ERR_WORKSPACE, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -945,8 +897,6 @@ int crtg_gemm_i8_i32(int64_t m, int64_t n, int64_t k, const int8_t* A, const int
   g.raw = raw;
   g.raw_ld = n_pad;
   g.raw_plane = m * n_pad;
-  g.unsigned_ops = env_int("CRTG_RAW_UNSIGNED", 0);  // experiment knobs (power vs data)
-  g.repeat_mma = env_int("CRTG_RAW_REPEAT", 0);
   CRTG_TRY(run_gemm(EPI_RAW, g, s), "i8 gemm");
   CRTG_TRY(cudaMemcpy2DAsync(C, n * 4, raw, n_pad * 4, n * 4, m, cudaMemcpyDeviceToDevice, s),
            "copy out");

@@ -103,105 +103,6 @@ __device__ __forceinline__ void karatsuba_phase(const GemmArgs& g, uint32_t tadd
   }
 }
 
-// CRTG_EPI_X16=1: 16-column TMEM loads double-buffered (32 registers of
-// buffers instead of 64): the next half-chunk's load is in flight while the
-// current one is reduced, without the spills of the 32-column double buffer.
-#ifndef CRTG_EPI_X16
-#define CRTG_EPI_X16 0
-#endif
-
-template <int NCH, bool POW2>
-__device__ __forceinline__ void karatsuba_phase16(const GemmArgs& g, uint32_t taddr, int s, int l,
-                                                  int row, bool row_ok, int col_base,
-                                                  const ModConst& mc, uint32_t (&st)[NCH * 8]) {
-  int8_t* dst_base = nullptr;
-  if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
-  if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
-  const uint32_t bias = uint32_t(mc.bias), bias_h = mc.bias_h, h = mc.h;
-  constexpr int NH = 2 * NCH;  // 16-column half-chunks
-  uint32_t v[2][16];
-  tmem_ld16(taddr, v[0]);
-#pragma unroll
-  for (int c = 0; c < NH; ++c) {
-    tmem_wait_ld();
-    if (c + 1 < NH) tmem_ld16(taddr + (c + 1) * 16, v[(c + 1) & 1]);
-    const uint32_t (&cv)[16] = v[c & 1];
-    uint32_t out[4];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      uint32_t a[4], b[4];
-      const uint32_t sw = st[c * 4 + w];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t x = cv[4 * w + j];
-        const uint32_t prev = __byte_perm(sw, 0, 0x4440 + j);
-        if (s == 0) {
-          a[j] = ep_red<POW2>(x + bias, mc);
-        } else if (s == 1) {
-          a[j] = ep_red<POW2>(prev - x + bias_h, mc) - h;
-          b[j] = ep_red<POW2>(prev + x + bias, mc);
-        } else {
-          a[j] = ep_red<POW2>(x - prev + bias_h, mc) - h;
-        }
-      }
-      if (s == 0) {
-        st[c * 4 + w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
-      } else {
-        out[w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
-        if (s == 1) st[c * 4 + w] = ep_pack_bytes(b[0], b[1], b[2], b[3]);
-      }
-    }
-    if (s != 0 && row_ok)
-      *reinterpret_cast<uint4*>(dst_base + c * 16) = make_uint4(out[0], out[1], out[2], out[3]);
-  }
-}
-
-template <int NCH>
-__device__ __forceinline__ void split_phase16(const GemmArgs& g, uint32_t taddr, int s, int l,
-                                              int row, bool row_ok, int col_base,
-                                              const ModConst& mc, uint32_t (&st)[NCH * 8]) {
-  int8_t* dre = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
-  int8_t* dim = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
-  const uint32_t bias = uint32_t(mc.bias), h = mc.h, p = uint32_t(mc.p);
-  const uint32_t inv2 = mc.inv2, inv2j = mc.inv2j;
-  constexpr int NH = 2 * NCH;
-  uint32_t v[2][16];
-  tmem_ld16(taddr, v[0]);
-#pragma unroll
-  for (int c = 0; c < NH; ++c) {
-    tmem_wait_ld();
-    if (c + 1 < NH) tmem_ld16(taddr + (c + 1) * 16, v[(c + 1) & 1]);
-    const uint32_t (&cv)[16] = v[c & 1];
-    uint32_t ore[4], oim[4];
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      uint32_t a[4], b[4];
-      const uint32_t sw = st[c * 4 + w];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t x = cv[4 * w + j];
-        if (s == 0) {
-          a[j] = ep_red<false>(x + bias, mc);
-        } else {
-          const uint32_t xm = __byte_perm(sw, 0, 0x4440 + j);
-          const uint32_t ym = ep_red<false>(x + bias, mc);
-          a[j] = ep_red<false>((xm + ym) * inv2 + h, mc) - h;
-          b[j] = ep_red<false>((xm + p - ym) * inv2j + h, mc) - h;
-        }
-      }
-      if (s == 0) {
-        st[c * 4 + w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
-      } else {
-        ore[w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
-        oim[w] = ep_pack_bytes(b[0], b[1], b[2], b[3]);
-      }
-    }
-    if (s != 0 && row_ok) {
-      *reinterpret_cast<uint4*>(dre + c * 16) = make_uint4(ore[0], ore[1], ore[2], ore[3]);
-      *reinterpret_cast<uint4*>(dim + c * 16) = make_uint4(oim[0], oim[1], oim[2], oim[3]);
-    }
-  }
-}
 
 // Split modulus (ModConst::nphase == 2, j^2 == -1 mod p):
 //   phase 0 (X = U*U'):  xm  = (X + bias) mod p                  -> st
@@ -339,15 +240,6 @@ __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr
     return;
   }
 #endif
-  if (CRTG_EPI_X16 && NCH == 8) {
-    if (mc.nphase == 2)
-      split_phase16<NCH>(g, taddr, s, l, row, row_ok, col_base, mc, st);
-    else if (mc.is_pow2)
-      karatsuba_phase16<NCH, true>(g, taddr, s, l, row, row_ok, col_base, mc, st);
-    else
-      karatsuba_phase16<NCH, false>(g, taddr, s, l, row, row_ok, col_base, mc, st);
-    return;
-  }
   if (mc.nphase == 2)
     split_phase<NCH>(g, taddr, s, l, row, row_ok, col_base, mc, st);
   else if (mc.is_pow2)

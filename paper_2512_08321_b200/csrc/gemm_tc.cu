@@ -130,10 +130,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    // unsigned operands (bits 7 / 10 clear): residues stored as t in [0, p)
-    const uint32_t idesc_s = idesc_i8(128, 256);
-    const uint32_t idesc_u = idesc_s & ~((1u << 7) | (1u << 10));
-    const uint32_t idesc = g.unsigned_ops ? idesc_u : idesc_s;
+    // unsigned operands (bits 7 / 10 clear): the accurate-mode X = (R+I)(R'+I')
+    // bytes of the bound product (<= 128)
+    const uint32_t idesc = idesc_i8(128, 256);
+    const uint32_t idesc_u = idesc & ~((1u << 7) | (1u << 10));
     uint32_t stage = 0, phase = 0, gslot = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       int l, tm, tn;
@@ -165,17 +165,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
             // advance 32 bytes of K inside the 128-byte swizzle atom
-            if (MODE != EPI_RAW || g.repeat_mma >= 0)
-              mma_i8(d, ad + 2 * kk, bd + 2 * kk,
-                     (MODE == EPI_BOUND && s == 0) ? idesc_u : idesc,
-                     (kb | kk | sg.accumulate) != 0);
-            if (MODE == EPI_RAW && g.repeat_mma > 0) {
-              // power experiment: a second MMA on operands already in smem --
-              // 1: same A and B, 2: same A / next B slice, 3: next A and B slices
-              const int ka = g.repeat_mma == 3 ? (kk + 1) & 3 : kk;
-              const int kbb = g.repeat_mma >= 2 ? (kk + 1) & 3 : kk;
-              mma_i8(d, ad + 2 * ka, bd + 2 * kbb, idesc, 1);
-            }
+            mma_i8(d, ad + 2 * kk, bd + 2 * kk,
+                   (MODE == EPI_BOUND && s == 0) ? idesc_u : idesc,
+                   (kb | kk | sg.accumulate) != 0);
           }
           mma_commit(smem_u32(&empty_bar[stage]));  // frees the smem slot when MMAs finish
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -430,165 +422,14 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
   }
 }
 
-// ---------------------------------------------------------------------------
-// Wide tiles in clusters of 2 along N: both CTAs of a cluster compute the same
-// 256 rows (adjacent 256-column tiles), so CTA r loads only A rows
-// [128 r, 128 r + 128) of each K block and multicasts them into both CTAs'
-// stage; B stays per CTA.  L2 -> SM reads per CTA: 48 KiB per 64 KiB stage.
-// A stage may be refilled only when both CTAs' MMAs have consumed it, so every
-// MMA commit arrives on the empty barrier of both CTAs (count 2).
-// ---------------------------------------------------------------------------
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-    k_gemm_wc(const __grid_constant__ GemmArgs g) {
-  extern __shared__ uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full_bar[kWStages];
-  __shared__ __align__(8) uint64_t empty_bar[kWStages];
-  __shared__ __align__(8) uint64_t tfull_bar, tempty_bar;
-  __shared__ uint32_t tmem_slot;
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
-  const uint32_t smem_base = (smem_u32(smem_raw) + 1023u) & ~1023u;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kWStages; ++s) {
-      mbar_init(smem_u32(&full_bar[s]), 1);
-      mbar_init(smem_u32(&empty_bar[s]), 2);  // both CTAs' MMA commits
-    }
-    mbar_init(smem_u32(&tfull_bar), 1);
-    mbar_init(smem_u32(&tempty_bar), kEpiThreads);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(&tmem_slot));
-  tc_fence_before();
-  cluster_sync();  // peers' barriers exist before any multicast lands
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-  // pair tiles: (l, tm2, column pair); CTA rank r takes column tile 2 * pair + r
-  GemmArgs gp = g;
-  gp.nt = g.nt >> 1;
-  gp.nt0 = 0;
-  const int total = g.nl * (g.mt >> 1) * gp.nt;
-  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-
-  if (warp == 0 && lane == 0) {
-    uint32_t stage = 0, phase = 0;
-    for (int t = cid; t < total; t += ncl) {
-      int l, tm2, tp;
-      decode_tile_w(t, gp, l, tm2, tp);
-      const int tn = 2 * tp + int(rank) + g.nt0;
-      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
-      for (int s = 0; s < nseg; ++s) {
-        const int8_t* a = g.a + (int64_t)(l * g.planes_per_l + s) * g.a_plane;
-        const int8_t* b = g.b + (int64_t)(l * g.planes_per_l + s) * g.b_plane;
-        for (int kb = 0; kb < g.kb; ++kb) {
-          mbar_wait_cluster(smem_u32(&empty_bar[stage]), phase ^ 1);
-          const uint32_t fb = smem_u32(&full_bar[stage]);
-          const uint32_t sa = smem_base + stage * kWStageBytes;
-          mbar_expect_tx(fb, kWStageBytes);
-          // my half of the shared A block -> both CTAs
-          bulk_g2s_mc(sa + rank * kBlockBytes,
-                      a + ((int64_t)kb * g.a_rb + 2 * tm2 + rank) * kBlockBytes, kBlockBytes, fb,
-                      uint16_t(0x3));
-          bulk_g2s(sa + kWStageA, b + ((int64_t)kb * g.b_rb + 2 * tn) * kBlockBytes, kWStageB, fb);
-          if (++stage == kWStages) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1 && lane == 0) {
-    const uint32_t idesc = idesc_i8(128, 256);
-    uint32_t stage = 0, phase = 0, gslot = 0;
-    for (int t = cid; t < total; t += ncl) {
-      int l, tm2, tp;
-      decode_tile_w(t, gp, l, tm2, tp);
-      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
-      for (int s = 0; s < nseg; ++s) {
-        mbar_wait(smem_u32(&tempty_bar), (gslot & 1) ^ 1);
-        tc_fence_after();
-        for (int kb = 0; kb < g.kb; ++kb) {
-          mbar_wait(smem_u32(&full_bar[stage]), phase);
-          tc_fence_after();
-          const uint32_t sa = smem_base + stage * kWStageBytes;
-          const uint64_t a0 = smem_desc_sw128(sa);
-          const uint64_t a1 = smem_desc_sw128(sa + kWStageA / 2);
-          const uint64_t bd = smem_desc_sw128(sa + kWStageA);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t acc = (kb | kk) != 0;
-            mma_i8(tmem, a0 + 2 * kk, bd + 2 * kk, idesc, acc);
-            mma_i8(tmem + 256, a1 + 2 * kk, bd + 2 * kk, idesc, acc);
-          }
-          mma_commit_mc(smem_u32(&empty_bar[stage]), uint16_t(0x3));
-          if (++stage == kWStages) { stage = 0; phase ^= 1; }
-        }
-        mma_commit(smem_u32(&tfull_bar));
-        ++gslot;
-      }
-    }
-  } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
-    const uint32_t lane_addr = tmem + (uint32_t(32 * q) << 16) + uint32_t(256 * half);
-    uint32_t gslot = 0;
-    uint32_t st[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) st[i] = 0;
-    for (int t = cid; t < total; t += ncl) {
-      int l, tm2, tp;
-      decode_tile_w(t, gp, l, tm2, tp);
-      const int row = tm2 * 256 + 128 * half + 32 * q + lane;
-      const bool row_ok = row < g.m;
-      const int col_base = (2 * tp + int(rank) + g.nt0) * 256;
-      const ModConst mc = g.mc[l];
-      const int nseg = tile_segments<EPI_KARATSUBA>(g, l);
-      for (int s = 0; s < nseg; ++s) {
-        mbar_wait(smem_u32(&tfull_bar), gslot & 1);
-        tc_fence_after();
-        epilogue_phase<EPI_KARATSUBA, 8>(g, lane_addr, s, l, row, row_ok, col_base, mc, st);
-        tc_fence_before();
-        mbar_arrive(smem_u32(&tempty_bar));
-        ++gslot;
-      }
-    }
-  }
-
-  tc_fence_before();
-  cluster_sync();  // no CTA leaves while its peer may still multicast into it
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem);
-  }
-}
-
-int launch_gemm_wide_mc(const GemmArgs& g, int num_sms, cudaStream_t stream) {
-  const int pairs = g.nl * (g.mt >> 1) * (g.nt >> 1);
-  if (pairs <= 0) return 0;
-  const int grid = 2 * (pairs < num_sms / 2 ? pairs : num_sms / 2);
-  const size_t smem = size_t(kWStages) * kWStageBytes + 1024;
-  const cudaError_t err =
-      cudaFuncSetAttribute(k_gemm_wc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (err != cudaSuccess) return int(err);
-  k_gemm_wc<<<grid, kThreads, smem, stream>>>(g);
-  return launched(1);
-}
-
 size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + 1024; }
 
 template <int MODE>
-int launch_wide_mode(const GemmArgs& g, int grid, size_t smem, int ew, cudaStream_t stream) {
-  cudaError_t err;
-  if (ew == 16) {
-    err = cudaFuncSetAttribute(k_gemm_w<MODE, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem));
-    if (err != cudaSuccess) return int(err);
-    k_gemm_w<MODE, 16><<<grid, 128 + 32 * 16, smem, stream>>>(g);
-  } else {
-    err = cudaFuncSetAttribute(k_gemm_w<MODE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               int(smem));
-    if (err != cudaSuccess) return int(err);
-    k_gemm_w<MODE, 8><<<grid, 128 + 32 * 8, smem, stream>>>(g);
-  }
+int launch_wide_mode(const GemmArgs& g, int grid, size_t smem, cudaStream_t stream) {
+  const cudaError_t err = cudaFuncSetAttribute(
+      k_gemm_w<MODE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (err != cudaSuccess) return int(err);
+  k_gemm_w<MODE, 8><<<grid, 128 + 32 * 8, smem, stream>>>(g);
   return launched(1);
 }
 
@@ -597,14 +438,10 @@ int launch_gemm_wide(int mode, const GemmArgs& g, int num_sms, cudaStream_t stre
   if (total <= 0) return 0;
   const int grid = total < num_sms ? total : num_sms;
   const size_t smem = size_t(kWStages) * kWStageBytes + 1024;
-  // CRTG_EPI_WARPS=16 halves the non-overlapped drain but measured 10% slower
-  // (96-register cap -> spills, more issue energy under the power cap)
-  static const int ew = [] {
-    const char* v = std::getenv("CRTG_EPI_WARPS");
-    return v && std::atoi(v) == 16 ? 16 : 8;
-  }();
-  return mode == EPI_REAL ? launch_wide_mode<EPI_REAL>(g, grid, smem, ew, stream)
-                          : launch_wide_mode<EPI_KARATSUBA>(g, grid, smem, ew, stream);
+  // 8 epilogue warps (16 halve the non-overlapped drain but hit the 96-register
+  // cap and spill: 10% slower)
+  return mode == EPI_REAL ? launch_wide_mode<EPI_REAL>(g, grid, smem, stream)
+                          : launch_wide_mode<EPI_KARATSUBA>(g, grid, smem, stream);
 }
 
 int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {

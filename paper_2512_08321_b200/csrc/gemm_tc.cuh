@@ -31,8 +31,6 @@ struct GemmArgs {
   int32_t* col_max;  // BOUND: [nt*256]
   unsigned long long* overflow;  // REAL: int32 accumulator overflow (kernel.py:33-34)
   int group_m;       // raster: row tiles per column sweep (0 -> 16)
-  int unsigned_ops;  // u8 x u8 products (accumulator read as u32)
-  int repeat_mma;    // RAW experiments: >0 every MMA issued twice, -1 no MMA (load-only)
   ModConst mc[CRTG_MAX_MODULI];
 };
 
@@ -42,10 +40,5 @@ int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream);
 // wide-tile KARATSUBA (split) / REAL variant (256 x 256 per CTA, gemm_tc.cu); g.mt and
 // g.mt0 must be even
 int launch_gemm_wide(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream);
-// wide tiles in 2-CTA clusters along N sharing A by multicast; g.nt even
-int launch_gemm_wide_mc(const GemmArgs& g, int num_sms, cudaStream_t stream);
-// CTA-pair variant (cta_group::2, 256x256 tiles; KARATSUBA and RAW); g.mt and
-// g.mt0 must be even (rows padded to 256)
-int launch_gemm_pair(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream);
 
 }  // namespace crtg

@@ -456,263 +456,6 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
   }  // tile loop
 }
 
-// ---------------------------------------------------------------------------
-// Tensor-core residues (complex pipeline, 128-offset bytes).  The per-modulus
-// limb sums u_l = sum_b byte_b(v) * (2^(8b) mod p_l), v = a' + 2^63, are an
-// INT8 product: [values x 8 bytes] x [8 bytes x moduli].  Four values share a
-// 32-byte K row (slots re_2j, im_2j, re_2j+1, im_2j+1 of one thread's 8 complex
-// elements) against a block-diagonal constant operand (N = 4 moduli x 4 slots),
-// so each tcgen05.mma (M=128, N=16, K=32, u8 x u8 -> s32) gives u for 512 values
-// x 4 moduli in TMEM; the CUDA cores keep only the magic reduction per
-// value-modulus (the two dp2a of the register form, ~35% of the FMA-heavy pipe,
-// move to the idle tensor cores).  u < 8 * 255^2 < 2^20.  Thread (warp w, lane i)
-// owns TMEM lane 32 (w % 4) + i and blocks 4 (w / 4) + j, j < 4: it reads back
-// exactly the values it wrote.  Tiles holding any |a'| >= 2^63 take the
-// register (six-limb) form.
-// ---------------------------------------------------------------------------
-constexpr int kTcBlock = 4096;   // bytes of one 128-row x 32-byte VA block
-constexpr int kTcVA = 8 * kTcBlock;
-constexpr int kTcPasses = (CRTG_MAX_MODULI + 3) / 4;
-constexpr int kTcCB = kTcPasses * 512;  // passes x (16 rows x 32 bytes)
-
-template <int OPERAND>
-__device__ __forceinline__ void store_words(const uint32_t (&w)[3][2], bool split, int l,
-                                            int8_t* __restrict__ out, int64_t plane_bytes,
-                                            int64_t goff, int soff, int cq, int cs,
-                                            uint8_t (*stage)[kResRows * 128]) {
-  if (OPERAND == 0) {
-    int8_t* base = out + int64_t(3 * l) * plane_bytes + goff + soff;
-    *reinterpret_cast<uint2*>(base) = make_uint2(w[0][0], w[0][1]);
-    *reinterpret_cast<uint2*>(base + plane_bytes) = make_uint2(w[1][0], w[1][1]);
-    if (!split) *reinterpret_cast<uint2*>(base + 2 * plane_bytes) = make_uint2(w[2][0], w[2][1]);
-  } else {
-    uint8_t (*sb)[kResRows * 128] = stage + 3 * (l & 1);
-    *reinterpret_cast<uint2*>(&sb[0][soff]) = make_uint2(w[0][0], w[0][1]);
-    *reinterpret_cast<uint2*>(&sb[1][soff]) = make_uint2(w[1][0], w[1][1]);
-    if (!split) *reinterpret_cast<uint2*>(&sb[2][soff]) = make_uint2(w[2][0], w[2][1]);
-    __syncthreads();
-    int8_t* base = out + int64_t(3 * l) * plane_bytes + goff;
-    reinterpret_cast<uint4*>(base + cq * plane_bytes)[cs] =
-        reinterpret_cast<const uint4*>(sb[cq])[cs];
-    if (cq == 0 && !split)
-      reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
-          reinterpret_cast<const uint4*>(sb[2])[cs];
-  }
-}
-
-// planes of one modulus from t = (a' + off) mod p of the 8 complex elements
-__device__ __forceinline__ void words_from_t(const uint32_t (&tr)[8], const uint32_t (&ti)[8],
-                                             const ResConst& c, uint32_t (&w)[3][2]) {
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    const uint32_t* r = tr + 4 * half;
-    const uint32_t* m = ti + 4 * half;
-    if (c.split) {
-      uint32_t tu[4], tv[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        tu[j] = mod_small(mad_lo(m[j], c.gj, r[j] + c.gku), c);
-        tv[j] = mod_small(mad_lo(m[j], c.gjn, r[j] + c.gkv), c);
-      }
-      w[0][half] = pack_t<false>(tu[0], tu[1], tu[2], tu[3], c.off);
-      w[1][half] = pack_t<false>(tv[0], tv[1], tv[2], tv[3], c.off);
-    } else {
-      uint32_t ts[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t x = r[j] + m[j] + c.sum_k;
-        const uint32_t y = min(x, x + c.neg_p);
-        ts[j] = min(y, y + c.neg_p);
-      }
-      w[0][half] = pack_t<false>(r[0], r[1], r[2], r[3], c.off);
-      w[1][half] = pack_t<false>(m[0], m[1], m[2], m[3], c.off);
-      w[2][half] = pack_t<false>(ts[0], ts[1], ts[2], ts[3], c.off);
-    }
-  }
-}
-
-template <typename T, int OPERAND>
-__global__ void __launch_bounds__(256, 3) k_residues_tc(const T* __restrict__ X, int64_t ldx,
-                                                     int rows, int kdim, int64_t col0,
-                                                     const int32_t* __restrict__ exps,
-                                                     const __grid_constant__ DevConsts dc,
-                                                     int8_t* __restrict__ out,
-                                                     int64_t plane_bytes, int64_t rb_count,
-                                                     unsigned long long* __restrict__ overflow,
-                                                     int n_kb, int n_rt, int row_base) {
-  extern __shared__ __align__(1024) uint8_t tc_smem[];  // VA blocks | CB | 2 x stage
-  __shared__ __align__(8) uint64_t mma_bar;
-  __shared__ uint32_t tmem_slot;
-  uint8_t* va = tc_smem;
-  uint8_t* cb = tc_smem + kTcVA;
-  uint8_t (*stage)[kResRows * 128] =
-      reinterpret_cast<uint8_t (*)[kResRows * 128]>(tc_smem + kTcVA + kTcCB);
-  const ResConst* rcs = dc.rx;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = warp >> 2, quarter = warp & 3;
-  const int tlane = 32 * quarter + lane;  // TMEM lane = VA row inside each block
-
-  // constant operand: pass p, row n = 4 ml + slot holds (2^(8b) mod p_l), l = 4p + ml,
-  // in K bytes [8 slot, 8 slot + 8); canonical no-swizzle layout (core matrices of
-  // 8 rows x 16 bytes; K-adjacent cores 128 B apart, row groups 256 B apart)
-  for (int chunk = threadIdx.x; chunk < kTcPasses * 32; chunk += blockDim.x) {  // (pass, n, kc)
-    const int pass = chunk >> 5, n = (chunk >> 1) & 15, kc = chunk & 1;
-    const int l = 4 * pass + (n >> 2), slot = n & 3;
-    uint32_t wds[4] = {0, 0, 0, 0};
-    if (l < dc.n && (slot >> 1) == kc) {
-      const uint32_t P = 0u - dc.rx[l].neg_p;  // neg_p = (uint32)(-p)
-      uint32_t cbyte = 1u % P;
-      const int w0 = (slot & 1) * 2;  // byte offset (slot - 2 kc) * 8 -> word 0 or 2
-      for (int b = 0; b < 8; ++b) {
-        wds[w0 + (b >> 2)] |= (cbyte & 0xFF) << (8 * (b & 3));
-        cbyte = (cbyte * 256u) % P;
-      }
-    }
-    *reinterpret_cast<uint4*>(cb + pass * 512 + (n >> 3) * 256 + kc * 128 + (n & 7) * 16) =
-        make_uint4(wds[0], wds[1], wds[2], wds[3]);
-  }
-  if (threadIdx.x == 0) {
-    mbar_init(smem_u32(&mma_bar), 1);
-    fence_mbar_init();
-  }
-  if (warp == 0) tmem_alloc<128>(smem_u32(&tmem_slot));
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-  uint32_t mma_phase = 0;
-  const uint32_t idesc = (2u << 4) | (uint32_t(16 >> 3) << 17) | (uint32_t(128 >> 4) << 24);
-  const int npass = (dc.n + 3) >> 2;
-
-  for (int tile = blockIdx.x; tile < n_kb * n_rt; tile += gridDim.x) {
-    const int kb = OPERAND == 0 ? tile % n_kb : tile / n_rt;
-    const int r0 = (OPERAND == 0 ? tile / n_kb : tile % n_rt) * kResRows;
-    int r, seg;
-    if (OPERAND == 0) {
-      r = threadIdx.x >> 4;
-      seg = threadIdx.x & 15;
-    } else {
-      r = threadIdx.x & 15;
-      seg = threadIdx.x >> 4;
-    }
-    const int row = r0 + r;
-    const int h0 = kb * 128 + seg * 8;
-    const bool row_ok = row < rows;
-    const int e = row_ok ? exps[row] : 0;
-    const double scale = __longlong_as_double(e >= -1022 ? int64_t(e + 1023) << 52
-                                                         : int64_t(1) << (e + 1074));
-    double qr[8], qi[8];
-    int bad = 0;
-    bool huge = false;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int h = h0 + t;
-      double re = 0.0, im = 0.0;
-      if (row_ok && h < kdim) {
-        const T* p = (OPERAND == 0) ? X + 2 * (int64_t(row) * ldx + h)
-                                    : X + 2 * (int64_t(h) * ldx + col0 + row);
-        load_c<T, false>(p, re, im);
-      }
-      qr[t] = __dmul_rn(re, scale);
-      qi[t] = __dmul_rn(im, scale);
-      if (!(fabs(qr[t]) < 0x1p90)) { bad = 1; qr[t] = 0.0; }
-      if (!(fabs(qi[t]) < 0x1p90)) { bad = 1; qi[t] = 0.0; }
-      huge |= fmax(fabs(qr[t]), fabs(qi[t])) >= 0x1p63;
-    }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(overflow, 1ull);
-    const int chunk = seg >> 1;
-    const int soff = (r >> 3) * 1024 + (r & 7) * 128 + ((chunk ^ (r & 7)) << 4) + (seg & 1) * 8;
-    const int gr0 = r0 + row_base;
-    const int64_t goff = (int64_t(kb) * rb_count + (gr0 >> 7)) * kBlockBytes + (gr0 & 127) * 128;
-    const int cq = threadIdx.x >> 7;
-    const int cs = threadIdx.x & 127;
-
-    if (__syncthreads_or(huge)) {
-      // some |a'| >= 2^63 in the tile: the register six-limb form
-      Val3 vr[8], vi[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        vr[t] = split_wide(trunc(qr[t]));
-        vi[t] = split_wide(trunc(qi[t]));
-      }
-      for (int l = 0; l < dc.n; ++l) {
-        const ResConst c = rcs[l];
-        uint32_t w[3][2];
-        residue_words<3, false>(vr, vi, c, w);
-        store_words<OPERAND>(w, c.split != 0, l, out, plane_bytes, goff, soff, cq, cs, stage);
-      }
-      __syncthreads();
-      continue;
-    }
-    // v = a' + 2^63 of the 8 complex elements -> 4 VA rows (slots re, im, re, im)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t v0 = uint64_t(__double2ll_rz(qr[2 * j])) ^ 0x8000000000000000ull;
-      const uint64_t v1 = uint64_t(__double2ll_rz(qi[2 * j])) ^ 0x8000000000000000ull;
-      const uint64_t v2 = uint64_t(__double2ll_rz(qr[2 * j + 1])) ^ 0x8000000000000000ull;
-      const uint64_t v3 = uint64_t(__double2ll_rz(qi[2 * j + 1])) ^ 0x8000000000000000ull;
-      uint8_t* rowp = va + (4 * grp + j) * kTcBlock + (tlane >> 3) * 256 + (tlane & 7) * 16;
-      *reinterpret_cast<uint4*>(rowp) =
-          make_uint4(uint32_t(v0), uint32_t(v0 >> 32), uint32_t(v1), uint32_t(v1 >> 32));
-      *reinterpret_cast<uint4*>(rowp + 128) =
-          make_uint4(uint32_t(v2), uint32_t(v2 >> 32), uint32_t(v3), uint32_t(v3 >> 32));
-    }
-    fence_proxy_async_smem();  // generic-proxy stores -> visible to tcgen05.mma
-    tc_fence_before();
-    __syncthreads();  // VA written
-    auto issue = [&](int pass) {
-      tc_fence_after();
-      const uint64_t bd = smem_desc_noswz(smem_u32(cb + pass * 512), 128, 256);
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const uint64_t ad = smem_desc_noswz(smem_u32(va + b * kTcBlock), 128, 256);
-        mma_i8(tmem + 64 * (b >> 2) + 16 * (b & 3), ad, bd, idesc, 0);
-      }
-      mma_commit(smem_u32(&mma_bar));
-    };
-    if (threadIdx.x == 0) issue(0);
-    const uint32_t ta = tmem + (uint32_t(32 * quarter) << 16) + 64 * grp;
-    for (int pass = 0; pass < npass; ++pass) {
-      mbar_wait(smem_u32(&mma_bar), mma_phase);
-      mma_phase ^= 1;
-      tc_fence_after();
-      // all of this pass's u into registers, then the next pass's MMAs overwrite
-      // TMEM while the reductions run (software pipeline over the passes)
-      uint32_t u[4][16];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) tmem_ld16(ta + 16 * j, u[j]);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncthreads();  // every thread holds its u
-      if (threadIdx.x == 0 && pass + 1 < npass) issue(pass + 1);
-#pragma unroll
-      for (int ml = 0; ml < 4; ++ml) {
-        const int l = 4 * pass + ml;
-        if (l >= dc.n) break;
-        const ResConst c = rcs[l];
-        uint32_t tr[8], ti[8];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          tr[2 * j] = mod_small(u[j][4 * ml] + c.k63, c);
-          ti[2 * j] = mod_small(u[j][4 * ml + 1] + c.k63, c);
-          tr[2 * j + 1] = mod_small(u[j][4 * ml + 2] + c.k63, c);
-          ti[2 * j + 1] = mod_small(u[j][4 * ml + 3] + c.k63, c);
-        }
-        uint32_t w[3][2];
-        words_from_t(tr, ti, c, w);
-        store_words<OPERAND>(w, c.split != 0, l, out, plane_bytes, goff, soff, cq, cs, stage);
-      }
-    }
-    __syncthreads();  // stage buffers and VA are reused by the next tile
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc<128>(tmem);
-  }
-}
-
 // plain int8 -> packed plane (test hooks); one thread per 16-byte chunk
 __global__ void k_pack_i8(const int8_t* __restrict__ X, int trans, int64_t rows, int64_t kdim,
                           int64_t kpad, int8_t* __restrict__ out, int64_t rb_count,
@@ -738,19 +481,6 @@ __global__ void k_unpack_i8(const int8_t* __restrict__ packed, int64_t rows, int
   if (t >= rows * kdim) return;
   const int64_t r = t / kdim, h = t % kdim;
   out[t] = packed[pack_offset(r, h, rb_count)];
-}
-
-// CRTG_TC_RESIDUES=1 selects the tensor-core limb sums (k_residues_tc) for the
-// complex pipeline.  Bit-identical but measured slower on B200 (pipelined: A
-// 5.6 -> 6.8 ms, B 6.1 -> 7.2 ms at 16384^3 N=15): VA staging, the per-pass
-// barriers and the TMEM reads cost more than the two dp2a they replace.  Off by
-// default.
-bool tc_residues_enabled() {
-  static const bool on = [] {
-    const char* v = std::getenv("CRTG_TC_RESIDUES");
-    return v && v[0] == '1';
-  }();
-  return on;
 }
 
 template <typename T, int OP, int KIND, bool REAL>
@@ -784,22 +514,6 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
                                                   rb_count, overflow, n_kb, n_rt, int(row_base))
     if (REAL || dc.sym) {
       if (msplit > 1) CRTG_RES_LAUNCH(REAL, true, true); else CRTG_RES_LAUNCH(REAL, true, false);
-    } else if (tc_residues_enabled()) {
-      // persistent: 3 CTAs per SM (128 TMEM columns each), grid-stride over tiles
-      static int nsm = [] {
-        int d = 0, v = 148;
-        cudaGetDevice(&d);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
-        return v;
-      }();
-      const unsigned tgrid = unsigned(std::min<int64_t>(tiles, int64_t(3) * nsm));
-      const unsigned g2 = max_ctas > 0 ? std::min(tgrid, unsigned(max_ctas)) : tgrid;
-      const size_t smem = kTcVA + kTcCB + 6 * kResRows * 128;
-      cudaFuncSetAttribute(k_residues_tc<T, OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(smem));
-      k_residues_tc<T, OP><<<g2, 256, smem, s>>>(static_cast<const T*>(X), ldx, int(rows),
-                                                 int(kdim), col0, exps, dc, out, plane_bytes,
-                                                 rb_count, overflow, n_kb, n_rt, int(row_base));
     } else if (msplit > 1) {
       CRTG_RES_LAUNCH(false, false, true);
     } else {

@@ -117,6 +117,10 @@ def _send(t: torch.Tensor, dst: int) -> None:
     dist.send(t.cpu() if (_staged() and t.is_cuda) else t, dst)
 
 
+def _isend_op(t: torch.Tensor, dst: int):
+    return dist.P2POp(dist.isend, t.cpu() if (_staged() and t.is_cuda) else t, dst)
+
+
 def _recv(t: torch.Tensor, src: int) -> None:
     if _staged() and t.is_cuda:
         buf = torch.empty(t.shape, dtype=t.dtype)
@@ -142,6 +146,7 @@ def scatter_operands(a, b, grid: TileGrid, rank: int, m: int, n: int, k: int,
     r_me, c_me = grid.coords(rank)
     if groups is None or grid.world <= 2:
         if rank == root:
+            ops = []
             for dst in range(grid.world):
                 di0, di1 = grid.rows(m, dst)
                 dj0, dj1 = grid.cols(n, dst)
@@ -150,8 +155,8 @@ def scatter_operands(a, b, grid: TileGrid, rank: int, m: int, n: int, k: int,
                 if dst == root:
                     a_loc, b_loc = ablk, bblk
                 else:
-                    _send(ablk, dst)
-                    _send(bblk, dst)
+                    ops += [_isend_op(ablk, dst), _isend_op(bblk, dst)]
+            _batched(ops)  # all peers' blocks leave the root concurrently
             return a_loc, b_loc
         a_loc = torch.empty((i1 - i0, k), dtype=dtype, device=device)
         b_loc = torch.empty((k, j1 - j0), dtype=dtype, device=device)
@@ -163,20 +168,22 @@ def scatter_operands(a, b, grid: TileGrid, rank: int, m: int, n: int, k: int,
     a_loc = b_loc = None
     # level 1: root -> leaders (one block each)
     if rank == root:
+        ops = []
         for r in range(grid.R):
             di0, di1 = grid.rows(m, grid.row_members(r)[0])
             blk = a[di0:di1].contiguous().to(device)
             if grid.row_members(r)[0] == root:
                 a_loc = blk
             else:
-                _send(blk, grid.row_members(r)[0])
+                ops.append(_isend_op(blk, grid.row_members(r)[0]))
         for c in range(grid.C):
             dj0, dj1 = grid.cols(n, grid.col_members(c)[0])
             blk = b[:, dj0:dj1].contiguous().to(device)
             if grid.col_members(c)[0] == root:
                 b_loc = blk
             else:
-                _send(blk, grid.col_members(c)[0])
+                ops.append(_isend_op(blk, grid.col_members(c)[0]))
+        _batched(ops)
     if a_loc is None:
         a_loc = torch.empty((i1 - i0, k), dtype=dtype, device=device)
         if rank == a_lead:
@@ -202,22 +209,38 @@ def _bcast(t: torch.Tensor, src: int, group) -> None:
         dist.broadcast(t, src, group=group)
 
 
+def _batched(ops) -> None:
+    """Post point-to-point ops together (one NCCL group: the transfers to / from
+    different peers run concurrently over NVSwitch) and wait for all of them."""
+    if not ops:
+        return
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+
+
 def gather_tiles(c_loc: torch.Tensor, grid: TileGrid, rank: int, m: int, n: int,
                  root: int = 0):
-    """Every rank sends its C tile to root; root returns the assembled C."""
+    """Every rank sends its C tile to root; root posts all receives at once
+    (grouped) and returns the assembled C."""
     if rank != root:
         _send(c_loc.contiguous(), root)
         return None
     out = torch.empty((m, n), dtype=c_loc.dtype, device=c_loc.device)
+    staged = _staged() and c_loc.is_cuda
+    ops, bufs = [], []
     for src in range(grid.world):
         i0, i1 = grid.rows(m, src)
         j0, j1 = grid.cols(n, src)
         if src == root:
             out[i0:i1, j0:j1] = c_loc
-        else:
-            buf = torch.empty((i1 - i0, j1 - j0), dtype=c_loc.dtype, device=c_loc.device)
-            _recv(buf, src)
-            out[i0:i1, j0:j1] = buf
+            continue
+        buf = torch.empty((i1 - i0, j1 - j0), dtype=c_loc.dtype,
+                          device="cpu" if staged else c_loc.device)
+        ops.append(dist.P2POp(dist.irecv, buf, src))
+        bufs.append(((i0, i1, j0, j1), buf))
+    _batched(ops)
+    for (i0, i1, j0, j1), buf in bufs:
+        out[i0:i1, j0:j1].copy_(buf)
     return out
 
 

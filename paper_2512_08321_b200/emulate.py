@@ -91,12 +91,42 @@ def _workspace(nbytes: int, dev) -> torch.Tensor:
 # ----------------------------------------------------------------------------
 # the hot path
 # ----------------------------------------------------------------------------
+def _empty_product(a, b, cfg: EmuConfig, complex_out: bool):
+    """Zero-extent operands, as the reference behaves (no kernel launched): fast
+    mode with m = 0 or n = 0 (k > 0) returns an empty (m, n) result of the
+    output dtype; every other zero extent fails in numpy's max-reduction inside
+    the reference's scaling (a ValueError) -> DimensionError (a ValueError).
+    Returns None when no extent is zero."""
+    ash = tuple(a.shape) if isinstance(a, torch.Tensor) else np.shape(a)
+    bsh = tuple(b.shape) if isinstance(b, torch.Tensor) else np.shape(b)
+    if len(ash) != 2 or len(bsh) != 2 or min(ash + bsh) > 0:
+        return None
+    if ash[1] != bsh[0]:
+        raise DimensionError(f"inner dimensions differ: {ash} x {bsh}")
+    m, k = ash
+    n = bsh[1]
+    if k == 0 or cfg.mode != "fast":
+        raise DimensionError("zero-size array to reduction operation maximum which has no identity")
+    single = cfg.precision == "single"
+    if isinstance(a, torch.Tensor) and isinstance(b, torch.Tensor):
+        dt = ((torch.complex64 if single else torch.complex128) if complex_out
+              else (torch.float32 if single else torch.float64))
+        dev = a.device if a.is_cuda else (b.device if b.is_cuda else _device())
+        return torch.empty((m, n), dtype=dt, device=dev)
+    dt = (np.complex64 if single else np.complex128) if complex_out else (
+        np.float32 if single else np.float64)
+    return np.empty((m, n), dtype=dt)
+
+
 def emulate_gemm_complex(a, b, cfg: EmuConfig | None = None,
                          diagnostics: dict | None = None):
     """Emulated complex matrix product A @ B (reference emulate.py:193-240)."""
     cfg = cfg or EmuConfig(domain="complex")
     if cfg.domain != "complex":
         raise ConfigError("config domain must be 'complex'")
+    empty = _empty_product(a, b, cfg, True)
+    if empty is not None:
+        return empty
     dev = _device()
     on_dev = [isinstance(x, torch.Tensor) and x.is_cuda for x in (a, b)]
     if not any(on_dev):
@@ -314,6 +344,12 @@ def emulate_gemm_real(a, b, cfg: EmuConfig | None = None, diagnostics: dict | No
     cfg = cfg or EmuConfig()
     if cfg.domain != "real":
         raise ConfigError("config domain must be 'real'")
+    for x, name in ((a, "A"), (b, "B")):
+        if x.is_complex() if isinstance(x, torch.Tensor) else np.iscomplexobj(x):
+            raise DomainError(f"{name} must be real for real-domain emulation")
+    empty = _empty_product(a, b, cfg, False)
+    if empty is not None:
+        return empty
     dev = _device()
     ash = tuple(a.shape) if isinstance(a, torch.Tensor) else np.shape(a)
     bsh = tuple(b.shape) if isinstance(b, torch.Tensor) else np.shape(b)

@@ -151,3 +151,40 @@ class TestSplitModuli:
         assert sum(products_per_modulus(crt.select_moduli(20))) == 53
         monkeypatch.setenv("CRTG_SPLIT", "0")
         assert sum(products_per_modulus(ms)) == 45
+
+
+# ---------------------------------------------------------------- empty extents
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("domain", ["complex", "real"])
+def test_empty_rows_or_cols_fast(prec, domain):
+    """Reference behaviour (run against crtgemm 0.1.0): fast mode with m = 0 or
+    n = 0 returns an empty result of the output dtype; no device work."""
+    import numpy as np
+
+    import paper_2512_08321_b200 as crt
+    cfg = crt.EmuConfig(precision=prec, domain=domain, mode="fast")
+    fn = crt.emulate_gemm_complex if domain == "complex" else crt.emulate_gemm_real
+    cplx = domain == "complex"
+    want = {("complex", "double"): np.complex128, ("complex", "single"): np.complex64,
+            ("real", "double"): np.float64, ("real", "single"): np.float32}[(domain, prec)]
+    for sa, sb in (((0, 5), (5, 3)), ((4, 5), (5, 0))):
+        a = np.ones(sa, np.complex128 if cplx else np.float64)
+        b = np.ones(sb, np.complex128 if cplx else np.float64)
+        c = fn(a, b, cfg)
+        assert c.shape == (sa[0], sb[1]) and c.dtype == want
+
+
+@pytest.mark.parametrize("mode", ["fast", "accurate"])
+def test_empty_extents_raise_like_reference(mode):
+    """Zero k (any mode) and zero m / n in accurate mode fail in the reference's
+    max-reduction with a ValueError; DimensionError is a ValueError."""
+    import numpy as np
+
+    import paper_2512_08321_b200 as crt
+    cfg = crt.EmuConfig(domain="complex", mode=mode)
+    cases = [((4, 0), (0, 3)), ((0, 0), (0, 0))]
+    if mode == "accurate":
+        cases += [((0, 5), (5, 3)), ((4, 5), (5, 0))]
+    for sa, sb in cases:
+        with pytest.raises(ValueError):
+            crt.emulate_gemm_complex(np.ones(sa, complex), np.ones(sb, complex), cfg)
