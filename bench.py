@@ -152,6 +152,17 @@ def peaks():
         return 1590.0, 1400.0, 6650.0, "fallback"
 
 
+def int8_peak():
+    """Measured cuBLASLt INT8 16384^3 rate on this pool (tools/int8_peak.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_peak.json")) as f:
+            p = json.load(f)
+        return {k: p[k] for k in ("int8_tops_burst", "int8_tops_sustained",
+                                  "sm_mhz_median_sustained")}
+    except Exception:
+        return None
+
+
 def profile_traffic():
     """Per-launch DRAM bytes of the GEMM from the committed ncu --set full capture."""
     path = os.path.join(ROOT, "profiles", "gemm_traffic.json")
@@ -400,28 +411,38 @@ def run_ours(a, rank: int, world: int, local_rank: int):
     ops_launch = 2.0 * prods * a.m * a.n * a.k * a.steps / launches_gemm
     ops_model = 6.0 * a.moduli * a.m * a.n * a.k * a.steps / launches_gemm
     achieved = ops_launch / (gemm_ms * 1e-3) / 1e12
-    # B200 dense INT8 rate = 2 x dense BF16.  K3 runs inside a long, power-capped
-    # step, but an INT8 MAC costs less energy than a bf16 one, so the capped
-    # INT8 GEMM runs ABOVE 2 x the capped (sustained) bf16 rate (frac > 1);
-    # the denominator is therefore 2 x the BURST bf16 figure, with the
-    # sustained-based and spec ratios reported beside it
-    peak_int8 = 2.0 * bf16
+    # Denominator: K3 runs inside a long, power-capped step, so the SUSTAINED
+    # figure applies: B200 dense INT8 = 2 x dense BF16, i.e. 2 x the measured
+    # sustained bf16 rate of MEASURED_PEAKS.json.  `achieved` counts the
+    # ALGORITHMIC ops of SURVEY section 8(d) (6 N m n_block k per launch: three
+    # INT8 products per modulus); the tensor cores execute fewer (a modulus with
+    # a square root of -1 needs two products), reported as frac_executed.  The
+    # measured cuBLASLt INT8 rate on this pool (profiles/int8_peak.json: burst /
+    # 4 s sustained at 16384^3) is reported beside it.
+    peak_int8 = 2.0 * bf16_sus
+    achieved_alg = ops_model / (gemm_ms * 1e-3) / 1e12
+    i8 = int8_peak()
     traffic = profile_traffic()
     if traffic and [traffic.get(k) for k in ("m", "n", "k", "N", "n_block", "mode")] != \
             [a.m, a.n, a.k, a.moduli, a.n_block, a.mode]:
         traffic = None  # the committed capture is for another configuration
     roof = {"bound": "tensor", "kernel": "k_gemm_w (256x256 Karatsuba/split tiles)",
-            "achieved": achieved,
-            "peak": peak_int8, "unit": "TFLOP/s", "op_kind": "INT8 tensor ops (one MAC = 2 ops), TOPS",
-            "frac": achieved / peak_int8,
-            "peak_note": f"INT8 dense = 2 x {src} BURST bf16 ({bf16} TF/s, MEASURED_PEAKS.json); "
-                         f"sustained 2 x {bf16_sus}; spec 4500",
-            "frac_of_sustained": achieved / (2.0 * bf16_sus), "frac_of_spec": achieved / 4500.0,
-            "ops_per_launch": ops_launch, "ms_per_launch": gemm_ms,
-            "int8_products_per_step": prods,
-            "ops_note": f"executed INT8 ops: {prods} products of m x n_block x k per launch "
-                        f"(3N = {3 * a.moduli} Karatsuba, minus one per split modulus); the "
-                        f"reference model's 6*N*mnk = {ops_model:.4g} per launch",
+            "achieved": achieved_alg, "peak": peak_int8, "unit": "TFLOP/s",
+            "op_kind": "INT8 tensor ops (one MAC = 2 ops), TOPS",
+            "frac": achieved_alg / peak_int8,
+            "peak_note": f"INT8 dense = 2 x {src} SUSTAINED bf16 ({bf16_sus} TF/s, "
+                         "MEASURED_PEAKS.json): the kernel is timed inside a long step",
+            "achieved_executed": achieved, "frac_executed": achieved / peak_int8,
+            "frac_of_2x_burst_bf16": achieved_alg / (2.0 * bf16),
+            "frac_of_spec_4500": achieved_alg / 4500.0,
+            "cublaslt_int8_measured": i8,
+            "frac_of_cublaslt_int8_sustained": (achieved_alg / i8["int8_tops_sustained"]
+                                                if i8 else None),
+            "ops_per_launch": ops_model, "executed_ops_per_launch": ops_launch,
+            "ms_per_launch": gemm_ms, "int8_products_per_step": prods,
+            "ops_note": f"algorithmic 6*N*m*n_block*k per launch (SURVEY 8(d)); executed: "
+                        f"{prods} products of m x n_block x k per step (3N = {3 * a.moduli} "
+                        "Karatsuba, minus one per split modulus)",
             "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
             "traffic_note": traffic.get("config") if traffic else None}
     stages = {k: v / a.steps for k, v in stage_ms.items()}

@@ -115,6 +115,26 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k,
                       uint64_t* diag, int sync_check, void* stream);
 
 /*
+ * Library-held state (everything else is caller-owned: A, B, C, the workspace
+ * and the stream; every kernel is stream-ordered on the caller's stream).
+ *  - Immutable per-thread cache of the last 8 modulus-constant tables built
+ *    from crtg_consts (host memory, a few KB each).
+ *  - Immutable per-(device, k) pairwise-sum tree of the fast-mode row
+ *    statistics (numpy's summation order), uploaded once with cudaMalloc and
+ *    kept for the process lifetime (16 * (k / 64 + 4) bytes: 16 KB at k = 65536).
+ *  - Per-thread, per-device auxiliary streams: one fork stream for B's chain on
+ *    small products and two copy-engine streams of crtg_gemm_complex_host.  They
+ *    are joined to the caller's stream with events before the call returns.
+ *  - crtg_gemm_complex_host with PAGEABLE A / B / C only: a per-thread ring of
+ *    3 pinned staging slots, each one streamed piece (~1/16 of an operand; 256
+ *    MiB at 16384^2 complex128).  Freed at thread exit or by
+ *    crtg_release_host_staging() (call with no call in flight on the thread).
+ * Concurrent calls from different host threads on different streams are safe
+ * and bitwise identical to serial calls (tests/test_gpu_concurrency.py).
+ */
+void crtg_release_host_staging(void);
+
+/*
  * The same product on HOST buffers (pinned for full overlap): A, B, C are host
  * pointers.  A's row chunks and B's column blocks (~1/16 of each) are copied in
  * interleaved on a copy engine; each landed piece releases a strip of output
@@ -225,6 +245,46 @@ int crtg_complex_gemm_mod(int64_t m, int64_t n, int64_t k, const int8_t* ar,
 int crtg_crt_reconstruct(int precision, int64_t m, int64_t n, const int8_t* e_re,
                          const int8_t* e_im, const int32_t* mu, const int32_t* nu,
                          const crtg_consts* K, void* C, int64_t ldc, void* stream);
+
+/* ---- stage-level entry points (the reference's stage functions on device
+ * arrays; paper_2512_08321_b200/stages.py).  `flags` is a caller-owned DEVICE
+ * array of uint64 (1 or 3 entries, zeroed by the call); with sync_check the
+ * call synchronizes `stream` and maps the flags to the reference's errors. ---- */
+
+/* log2_upper (scaling.py:62-82): float32 upper bound on log2 x, x > 0 finite
+ * (CRTG_ERR_DOMAIN otherwise). */
+int crtg_log2_upper(const double* x, int64_t n, float* out, uint64_t* flags, int sync_check,
+                    void* stream);
+
+/* quantize (scaling.py:277-293): out = trunc(ldexp(x, e)), e per row (axis 0)
+ * or per column (axis 1); |out| >= 2^90 -> CRTG_ERR_DOMAIN.  Row-major. */
+int crtg_quantize(const double* x, int64_t rows, int64_t cols, int64_t ldx, const int64_t* exps,
+                  int axis, double* out, int64_t ldo, uint64_t* flags, int sync_check,
+                  void* stream);
+
+/* symmetric residues (residue_decompose crt.py:199-218 / symmetric_mod_int
+ * crt.py:136-151) of `count` integer-valued entries for each of the nmod host
+ * moduli: out int8 [nmod][count].  kind 0: float64 (finite and < 2^90, else
+ * CRTG_ERR_DOMAIN), 1: int64, 2: int32; kind | 8 = residue_decompose's checks
+ * (float64 integer-valued, int64 < 2^61).  flags: 3 entries. */
+int crtg_symmetric_mod(int kind, const void* x, int64_t count, const int32_t* moduli, int nmod,
+                       int8_t* out, uint64_t* flags, int sync_check, void* stream);
+
+/* crt_accumulate (crt.py:221-243): e int8 [N][count] -> s1 = sum coeff_hi e,
+ * s2 = sum coeff_lo e (ascending l, no FMA); single != 0 writes s1 + s2 to s1. */
+int crtg_crt_accumulate(const int8_t* e, int64_t count, const crtg_consts* K, int single,
+                        double* s1, double* s2, void* stream);
+
+/* symmetric_mod_wide (crt.py:154-184): (s_hi + s_lo) mod P into (-P/2, P/2],
+ * P = p_hi + p_lo; s_lo may be NULL; use_dd selects the double-double path
+ * (Dekker two_prod exactly as ddarith.py). */
+int crtg_symmetric_mod_wide(const double* s_hi, const double* s_lo, int64_t count, double p_hi,
+                            double p_lo, int use_dd, double* out, void* stream);
+
+/* inverse_scale (emulate.py:135-144): out = ldexp(c, int32(-mu_i - nu_j)) as
+ * float64 or (out_f32) float32.  Row-major. */
+int crtg_inverse_scale(const double* c, int64_t rows, int64_t cols, int64_t ldc, const int64_t* mu,
+                       const int64_t* nu, int out_f32, void* out, int64_t ldo, void* stream);
 
 /* ---- accuracy harness ---- */
 

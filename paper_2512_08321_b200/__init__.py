@@ -15,12 +15,15 @@ from .gen import GenSpec, gen_matrix
 from .matfile import read_matrix, write_matrix
 from .moduli import ModulusSet, ScalingConstants, select_moduli
 from .perfmodel import PerfParams, heatmap_csv, heatmap_grid, predict_time, predicted_tflops
+from .stages import (ComplexMatrix, ResidueStack, ScaledIntMatrices, crt_accumulate,
+                     crt_integer_gemm, crt_reduce, inverse_scale, log2_upper, quantize,
+                     residue_decompose, symmetric_mod_int, symmetric_mod_wide)
 
 
 def __getattr__(name):
     # the accuracy harness imports torch-side helpers lazily
     if name in ("DDMatrix", "reference_gemm_dd", "max_relative_error", "run_accuracy_sweep",
-                "sweep_csv"):
+                "sweep_csv", "exact_gemm_bigint"):
         from . import accuracy
         return getattr(accuracy, name)
     raise AttributeError(name)
@@ -28,7 +31,10 @@ def __getattr__(name):
 __version__ = "0.1.0"
 
 __all__ = [
-    "ConfigError", "DDMatrix", "DEFAULT_N_BLOCK", "DimensionError", "DomainError", "EmuConfig",
+    "ComplexMatrix", "ResidueStack", "ScaledIntMatrices", "crt_accumulate", "crt_integer_gemm",
+    "crt_reduce", "inverse_scale", "log2_upper", "quantize", "residue_decompose",
+    "symmetric_mod_int", "symmetric_mod_wide",
+    "ConfigError", "DDMatrix", "exact_gemm_bigint", "DEFAULT_N_BLOCK", "DimensionError", "DomainError", "EmuConfig",
     "GenSpec", "MAX_K_COMPLEX", "MAX_K_REAL", "ModulusSet", "PerfParams", "STRATEGIES",
     "ScalingConstants", "ScalingVectors", "accurate_scaling", "complex_gemm_mod",
     "crt_reconstruct", "emulate_gemm_complex", "emulate_gemm_real", "fast_scaling", "gemm",

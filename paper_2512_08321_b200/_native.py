@@ -61,6 +61,16 @@ SIGNATURES = {
                               _vp, _c_i64, _vp]),
     "crtg_max_relative_error": (_c_int, [_c_int, _c_i64, _c_i64, _vp, _c_int, _c_i64, _vp, _vp,
                                          _c_i64, _vp, _vp, _vp]),
+    "crtg_release_host_staging": (None, []),
+    "crtg_log2_upper": (_c_int, [_vp, _c_i64, _vp, _vp, _c_int, _vp]),
+    "crtg_quantize": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _vp, _c_int, _vp, _c_i64, _vp,
+                               _c_int, _vp]),
+    "crtg_symmetric_mod": (_c_int, [_c_int, _vp, _c_i64, _vp, _c_int, _vp, _vp, _c_int, _vp]),
+    "crtg_crt_accumulate": (_c_int, [_vp, _c_i64, _vp, _c_int, _vp, _vp, _vp]),
+    "crtg_symmetric_mod_wide": (_c_int, [_vp, _vp, _c_i64, ctypes.c_double, ctypes.c_double,
+                                         _c_int, _vp, _vp]),
+    "crtg_inverse_scale": (_c_int, [_vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _c_int, _vp, _c_i64,
+                                    _vp]),
     "crtg_launch_count": (ctypes.c_uint64, []),
     "crtg_profile_enable": (_c_int, [_c_int]),
     "crtg_profile_read": (_c_int, [_vp, _vp]),

@@ -129,3 +129,23 @@ def sweep_csv(rows) -> str:
     lines = ["N,phi,seed,max_rel_error"]
     lines += [f"{count},{phi!r},{seed},{err!r}" for count, phi, seed, err in rows]
     return "\n".join(lines) + "\n"
+
+
+def exact_gemm_bigint(a, b) -> np.ndarray:
+    """Exact product of integer-valued matrices as an object array of Python
+    ints (reference oracle.py:32-57; a test-side checker, host arithmetic).
+    int64 accumulation when k * max|a| * max|b| < 2^62 cannot overflow, Python
+    big ints otherwise."""
+    a_arr = np.asarray(a)
+    b_arr = np.asarray(b)
+    if a_arr.ndim != 2 or b_arr.ndim != 2 or a_arr.shape[1] != b_arr.shape[0]:
+        raise DimensionError(f"bad shapes {a_arr.shape} x {b_arr.shape}")
+    to_obj = np.frompyfunc(int, 1, 1)
+    ao = to_obj(a_arr).astype(object) if a_arr.size else np.empty(a_arr.shape, object)
+    bo = to_obj(b_arr).astype(object) if b_arr.size else np.empty(b_arr.shape, object)
+    amax = max((abs(v) for v in ao.flat), default=0)
+    bmax = max((abs(v) for v in bo.flat), default=0)
+    if a_arr.shape[1] * amax * bmax < 2 ** 62:
+        c = a_arr.astype(np.int64) @ b_arr.astype(np.int64)
+        return to_obj(c).astype(object) if c.size else np.empty(c.shape, object)
+    return ao @ bo

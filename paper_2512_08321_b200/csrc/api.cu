@@ -1217,6 +1217,19 @@ struct HostStager {
     pending[s] = true;
     return int(cudaEventRecord(done[s], st));
   }
+  void free_all() {
+    for (int i = 0; i < kSlots; ++i) {
+      if (pending[i]) cudaEventSynchronize(done[i]);
+      pending[i] = false;
+      if (slot[i]) cudaFreeHost(slot[i]);
+      slot[i] = nullptr;
+      if (done[i]) cudaEventDestroy(done[i]);
+      done[i] = nullptr;
+    }
+    bytes = 0;
+    next = 0;
+  }
+  ~HostStager() { free_all(); }  // thread exit
 };
 
 HostStager& host_stager() {
@@ -1228,6 +1241,14 @@ HostStager& host_out_stager() {
   static thread_local HostStager st;
   return st;
 }
+}  // namespace
+
+extern "C" void crtg_release_host_staging(void) {
+  host_stager().free_all();
+  host_out_stager().free_all();
+}
+
+namespace {
 
 // rows of src (row_bytes each, contiguous) -> dst at dst_pitch, host threads
 void scatter_rows(char* dst, const char* src, int64_t rows, size_t row_bytes, size_t dst_pitch) {
@@ -1852,3 +1873,116 @@ extern "C" int crtg_max_relative_error(int is_complex, int64_t m, int64_t n, con
            "max relative error");
   return CRTG_OK;
 }
+
+// ---------------------------------------------------------------------------
+// stage-level API (include/crtg.h "stage-level entry points")
+// ---------------------------------------------------------------------------
+namespace {
+int stage_flags(uint64_t* flags, int n, cudaStream_t s) {
+  if (!flags) return fail(CRTG_ERR_CONFIG, "a device flags array is required");
+  CRTG_TRY(cudaMemsetAsync(flags, 0, 8 * size_t(n), s), "memset");
+  return CRTG_OK;
+}
+
+int stage_read_flags(const uint64_t* flags, int n, unsigned long long* h, cudaStream_t s) {
+  CRTG_TRY(cudaMemcpyAsync(h, flags, 8 * size_t(n), cudaMemcpyDeviceToHost, s), "flags copy");
+  CRTG_TRY(cudaStreamSynchronize(s), "sync");
+  return CRTG_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int crtg_log2_upper(const double* x, int64_t n, float* out, uint64_t* flags, int sync_check,
+                    void* stream) {
+  if (n < 0) return fail(CRTG_ERR_DIMENSION, "negative length");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int e = stage_flags(flags, 1, s)) return e;
+  auto* f = reinterpret_cast<unsigned long long*>(flags);
+  CRTG_TRY(launch_log2_upper(x, n, out, f, s), "log2_upper");
+  if (!sync_check) return CRTG_OK;
+  unsigned long long h[1];
+  if (int e = stage_read_flags(flags, 1, h, s)) return e;
+  if (h[0]) return fail(CRTG_ERR_DOMAIN, "log2_upper requires positive finite input");
+  return CRTG_OK;
+}
+
+int crtg_quantize(const double* x, int64_t rows, int64_t cols, int64_t ldx, const int64_t* exps,
+                  int axis, double* out, int64_t ldo, uint64_t* flags, int sync_check,
+                  void* stream) {
+  if (rows < 0 || cols < 0) return fail(CRTG_ERR_DIMENSION, "negative extent");
+  if (axis != 0 && axis != 1) return fail(CRTG_ERR_CONFIG, "axis must be 0 (rows) or 1 (columns)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int e = stage_flags(flags, 1, s)) return e;
+  auto* f = reinterpret_cast<unsigned long long*>(flags);
+  CRTG_TRY(launch_quantize(x, rows, cols, ldx, exps, axis, out, ldo, f, s), "quantize");
+  if (!sync_check) return CRTG_OK;
+  unsigned long long h[1];
+  if (int e = stage_read_flags(flags, 1, h, s)) return e;
+  if (h[0]) return fail(CRTG_ERR_DOMAIN, "scaled magnitudes exceed the quantization budget");
+  return CRTG_OK;
+}
+
+int crtg_symmetric_mod(int kind, const void* x, int64_t count, const int32_t* moduli, int nmod,
+                       int8_t* out, uint64_t* flags, int sync_check, void* stream) {
+  if ((kind & ~8) < 0 || (kind & ~8) > 2)
+    return fail(CRTG_ERR_CONFIG, "kind must be 0 (f64), 1 (i64) or 2 (i32), plus 8 for strict");
+  if (nmod < 1 || nmod > CRTG_MAX_MODULI) return fail(CRTG_ERR_CONFIG, "need 1..20 moduli");
+  if (count < 0) return fail(CRTG_ERR_DIMENSION, "negative length");
+  SymModuli mods{};
+  mods.n = nmod;
+  for (int l = 0; l < nmod; ++l) {
+    if (moduli[l] < 2 || moduli[l] > 256)
+      return fail(CRTG_ERR_DOMAIN, "modulus must be in [2, 256]");
+    mods.p[l] = moduli[l];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int e = stage_flags(flags, 3, s)) return e;
+  auto* f = reinterpret_cast<unsigned long long*>(flags);
+  CRTG_TRY(launch_sym_mod(kind, x, count, mods, out, f, s), "symmetric residues");
+  if (!sync_check) return CRTG_OK;
+  unsigned long long h[3];
+  if (int e = stage_read_flags(flags, 3, h, s)) return e;
+  if (h[0]) return fail(CRTG_ERR_DOMAIN, "matrix entries must be finite");
+  if (h[1])
+    return fail(CRTG_ERR_DOMAIN, (kind & 3) == 0 ? "matrix entries must be below 2^90"
+                                                 : "integer entries must be below 2^61");
+  if (h[2]) return fail(CRTG_ERR_DOMAIN, "matrix entries must be integer-valued");
+  return CRTG_OK;
+}
+
+int crtg_crt_accumulate(const int8_t* e, int64_t count, const crtg_consts* K, int single,
+                        double* s1, double* s2, void* stream) {
+  int N = 0;
+  if (int r = check_consts(K, &N)) return r;
+  if (count < 0) return fail(CRTG_ERR_DIMENSION, "negative length");
+  CrtCoeffs cf{};
+  for (int l = 0; l < N; ++l) {
+    cf.hi[l] = K->coeff_hi[l];
+    cf.lo[l] = K->coeff_lo[l];
+  }
+  CRTG_TRY(launch_crt_accumulate(e, N, count, cf, single != 0, s1, s2,
+                                 static_cast<cudaStream_t>(stream)),
+           "crt_accumulate");
+  return CRTG_OK;
+}
+
+int crtg_symmetric_mod_wide(const double* s_hi, const double* s_lo, int64_t count, double p_hi,
+                            double p_lo, int use_dd, double* out, void* stream) {
+  if (count < 0) return fail(CRTG_ERR_DIMENSION, "negative length");
+  CRTG_TRY(launch_sym_mod_wide(s_hi, s_lo, count, p_hi, p_lo, use_dd != 0, out,
+                               static_cast<cudaStream_t>(stream)),
+           "symmetric_mod_wide");
+  return CRTG_OK;
+}
+
+int crtg_inverse_scale(const double* c, int64_t rows, int64_t cols, int64_t ldc, const int64_t* mu,
+                       const int64_t* nu, int out_f32, void* out, int64_t ldo, void* stream) {
+  if (rows < 0 || cols < 0) return fail(CRTG_ERR_DIMENSION, "negative extent");
+  CRTG_TRY(launch_inverse_scale(c, rows, cols, ldc, mu, nu, out_f32 != 0, out, ldo,
+                                static_cast<cudaStream_t>(stream)),
+           "inverse_scale");
+  return CRTG_OK;
+}
+
+}  // extern "C"

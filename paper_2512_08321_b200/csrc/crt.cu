@@ -293,4 +293,113 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
   return launched(1);
 }
 
+// ---------------------------------------------------------------------------
+// stage-level API (stages.py): crt_accumulate (crt.py:221-243),
+// symmetric_mod_wide (crt.py:154-184) with the reference's Dekker two_prod
+// literally (ddarith.py:30-44; any double input, not only CRT sums), and
+// inverse_scale (emulate.py:135-144)
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void k_crt_accumulate(const int8_t* __restrict__ e, int nmod, int64_t count,
+                                 CrtCoeffs cf, int single, double* __restrict__ s1,
+                                 double* __restrict__ s2) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double a = 0.0, b = 0.0;
+    for (int l = 0; l < nmod; ++l) {
+      const double v = double(e[int64_t(l) * count + i]);
+      a = __dadd_rn(a, __dmul_rn(cf.hi[l], v));
+      b = __dadd_rn(b, __dmul_rn(cf.lo[l], v));
+    }
+    if (single) {
+      s1[i] = __dadd_rn(a, b);
+    } else {
+      s1[i] = a;
+      s2[i] = b;
+    }
+  }
+}
+
+__device__ __forceinline__ DD dekker_split(double a) {
+  const double c = __dmul_rn(134217729.0, a);
+  const double hi = __dsub_rn(c, __dsub_rn(c, a));
+  return {hi, __dsub_rn(a, hi)};
+}
+
+__device__ __forceinline__ DD dekker_two_prod(double a, double b) {
+  const double p = __dmul_rn(a, b);
+  const DD as = dekker_split(a), bs = dekker_split(b);
+  const double e = __dadd_rn(__dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(as.hi, bs.hi), p),
+                                                 __dmul_rn(as.hi, bs.lo)),
+                                        __dmul_rn(as.lo, bs.hi)),
+                             __dmul_rn(as.lo, bs.lo));
+  return {p, e};
+}
+
+__global__ void k_sym_mod_wide(const double* __restrict__ s_hi, const double* __restrict__ s_lo,
+                               int64_t count, double p_hi, double p_lo, int use_dd,
+                               double* __restrict__ out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double h = s_hi[i];
+    const double l = s_lo ? s_lo[i] : 0.0;
+    const double z = ceil(__dsub_rn(__ddiv_rn(__dadd_rn(h, l), p_hi), 0.5));
+    if (use_dd) {
+      const DD hl = two_sum(h, l);
+      DD pz = dekker_two_prod(p_hi, z);
+      pz.lo = __dadd_rn(pz.lo, __dmul_rn(p_lo, z));
+      pz = quick_two_sum(pz.hi, pz.lo);
+      const DD r = dd_add(hl.hi, hl.lo, -pz.hi, -pz.lo);
+      out[i] = __dadd_rn(r.hi, r.lo);
+    } else {
+      out[i] = __dsub_rn(__dsub_rn(h, __dmul_rn(z, p_hi)), __dmul_rn(z, p_lo));
+    }
+  }
+}
+
+__global__ void k_inverse_scale(const double* __restrict__ c, int64_t rows, int64_t cols,
+                                int64_t ldc, const int64_t* __restrict__ mu,
+                                const int64_t* __restrict__ nu, int out_f32,
+                                void* __restrict__ out, int64_t ldo) {
+  const int64_t total = rows * cols;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / cols, j = t % cols;
+    const int32_t e = int32_t(-mu[i] - nu[j]);  // .astype(np.int32)
+    const double v = ldexp(c[i * ldc + j], e);
+    if (out_f32)
+      static_cast<float*>(out)[i * ldo + j] = __double2float_rn(v);
+    else
+      static_cast<double*>(out)[i * ldo + j] = v;
+  }
+}
+
+int64_t stage_blocks(int64_t n) { return std::min<int64_t>((n + 255) / 256, 148 * 16); }
+}  // namespace
+
+int launch_crt_accumulate(const int8_t* e, int nmod, int64_t count, const CrtCoeffs& cf,
+                          bool single, double* s1, double* s2, cudaStream_t s) {
+  if (count <= 0) return 0;
+  k_crt_accumulate<<<unsigned(stage_blocks(count)), 256, 0, s>>>(e, nmod, count, cf,
+                                                                 single ? 1 : 0, s1, s2);
+  return launched(1);
+}
+
+int launch_sym_mod_wide(const double* s_hi, const double* s_lo, int64_t count, double p_hi,
+                        double p_lo, bool use_dd, double* out, cudaStream_t s) {
+  if (count <= 0) return 0;
+  k_sym_mod_wide<<<unsigned(stage_blocks(count)), 256, 0, s>>>(s_hi, s_lo, count, p_hi, p_lo,
+                                                               use_dd ? 1 : 0, out);
+  return launched(1);
+}
+
+int launch_inverse_scale(const double* c, int64_t rows, int64_t cols, int64_t ldc,
+                         const int64_t* mu, const int64_t* nu, bool out_f32, void* out,
+                         int64_t ldo, cudaStream_t s) {
+  if (rows * cols <= 0) return 0;
+  k_inverse_scale<<<unsigned(stage_blocks(rows * cols)), 256, 0, s>>>(
+      c, rows, cols, ldc, mu, nu, out_f32 ? 1 : 0, out, ldo);
+  return launched(1);
+}
+
 }  // namespace crtg

@@ -74,4 +74,28 @@ int launch_max_rel_err(bool cplx, int64_t m, int64_t n, const void* approx, bool
                        int64_t lda_x, const double* hi, const double* lo, int64_t ldo,
                        unsigned long long* max_bits, unsigned long long* zeros, cudaStream_t s);
 
+// ---- stage-level API (stages.py / crtg_stage_*) ----
+struct SymModuli {
+  int n;
+  int p[CRTG_MAX_MODULI];
+};
+struct CrtCoeffs {
+  double hi[CRTG_MAX_MODULI];
+  double lo[CRTG_MAX_MODULI];
+};
+int launch_log2_upper(const double* x, int64_t n, float* out, unsigned long long* flags,
+                      cudaStream_t s);
+int launch_quantize(const double* x, int64_t rows, int64_t cols, int64_t ldx, const int64_t* exps,
+                    int axis, double* out, int64_t ldo, unsigned long long* flags,
+                    cudaStream_t s);
+int launch_sym_mod(int kind, const void* x, int64_t count, const SymModuli& mods, int8_t* out,
+                   unsigned long long* flags, cudaStream_t s);
+int launch_crt_accumulate(const int8_t* e, int nmod, int64_t count, const CrtCoeffs& cf,
+                          bool single, double* s1, double* s2, cudaStream_t s);
+int launch_sym_mod_wide(const double* s_hi, const double* s_lo, int64_t count, double p_hi,
+                        double p_lo, bool use_dd, double* out, cudaStream_t s);
+int launch_inverse_scale(const double* c, int64_t rows, int64_t cols, int64_t ldc,
+                         const int64_t* mu, const int64_t* nu, bool out_f32, void* out,
+                         int64_t ldo, cudaStream_t s);
+
 }  // namespace crtg

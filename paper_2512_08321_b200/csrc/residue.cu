@@ -575,4 +575,63 @@ int launch_unpack_i8(const int8_t* packed, int64_t rows, int64_t kdim, int64_t r
   return launched(1);
 }
 
+// ---------------------------------------------------------------------------
+// stage-level API (stages.py): symmetric residues of integer-valued arrays for
+// every modulus (residue_decompose crt.py:199-218, symmetric_mod_int :136-151)
+// ---------------------------------------------------------------------------
+namespace {
+__device__ __forceinline__ int8_t sym_of(int64_t r, int p) {
+  // r in [0, p): the symmetric representative x - p * floor((2x + p) / 2p)
+  return int8_t(r - p * ((2 * r + p) / (2 * p)));
+}
+
+// kind & 3: 0 float64, 1 int64, 2 int32; kind & 8 (strict, residue_decompose):
+// float64 must be integer-valued, int64 below 2^61.  float64 is always checked
+// finite and below 2^90.  flags: [0] non-finite, [1] |x| >= bound, [2] not
+// integer-valued.  x = hi * 2^31 + lo with hi = floor(x / 2^31) (crt.py:123-133:
+// a non-integer float keeps trunc(lo), as the reference's astype(int64) does).
+__global__ void k_sym_mod(int kind, const void* __restrict__ x, int64_t count,
+                          SymModuli mods, int8_t* __restrict__ out,
+                          unsigned long long* flags) {
+  const bool strict = (kind & 8) != 0;
+  kind &= 3;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    int64_t hi = 0, lo = 0;  // x = hi * 2^31 + lo, 0 <= lo < 2^31
+    if (kind == 0) {
+      const double v = static_cast<const double*>(x)[i];
+      if (!isfinite(v)) { atomicAdd(flags, 1ull); continue; }
+      if (fabs(v) >= 0x1p90) { atomicAdd(flags + 1, 1ull); continue; }
+      if (strict && trunc(v) != v) { atomicAdd(flags + 2, 1ull); continue; }
+      const double h = floor(v * 0x1p-31);
+      hi = int64_t(h);
+      lo = int64_t(v - h * 0x1p31);
+    } else {
+      const int64_t v = kind == 1 ? static_cast<const int64_t*>(x)[i]
+                                  : int64_t(static_cast<const int32_t*>(x)[i]);
+      if (strict && kind == 1 && (v >= (int64_t(1) << 61) || v <= -(int64_t(1) << 61))) {
+        atomicAdd(flags + 1, 1ull);
+        continue;
+      }
+      hi = v >> 31;  // arithmetic shift: floor(v / 2^31)
+      lo = v - hi * (int64_t(1) << 31);
+    }
+    for (int l = 0; l < mods.n; ++l) {
+      const int p = mods.p[l];
+      const int64_t hm = ((hi % p) + p) % p;
+      const int64_t r = (hm * ((int64_t(1) << 31) % p) + lo) % p;
+      out[int64_t(l) * count + i] = sym_of(r, p);
+    }
+  }
+}
+}  // namespace
+
+int launch_sym_mod(int kind, const void* x, int64_t count, const SymModuli& mods, int8_t* out,
+                   unsigned long long* flags, cudaStream_t s) {
+  if (count <= 0) return 0;
+  const int64_t blocks = std::min<int64_t>((count + 255) / 256, 148 * 16);
+  k_sym_mod<<<unsigned(blocks), 256, 0, s>>>(kind, x, count, mods, out, flags);
+  return launched(1);
+}
+
 }  // namespace crtg

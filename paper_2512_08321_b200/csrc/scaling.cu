@@ -611,4 +611,62 @@ int launch_accurate_exps(const int32_t* maxb, const double* absval, const int32_
   return launched(1);
 }
 
+// ---------------------------------------------------------------------------
+// stage-level API (stages.py): the reference's log2_upper and quantize on
+// device arrays
+// ---------------------------------------------------------------------------
+namespace {
+// flags[0]: non-finite or non-positive input
+__global__ void k_log2_upper_arr(const double* __restrict__ x, int64_t n, float* __restrict__ out,
+                                 unsigned long long* flags) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const double v = x[i];
+    if (!(v > 0.0) || !isfinite(v)) {
+      atomicAdd(flags, 1ull);
+      out[i] = 0.0f;
+      continue;
+    }
+    out[i] = log2_upper(v);
+  }
+}
+
+// trunc(ldexp(x, e)) with e per row (axis 0) or per column (axis 1)
+// (scaling.py:277-293); flags[0]: |scaled| >= 2^90 (DomainError)
+__global__ void k_quantize(const double* __restrict__ x, int64_t rows, int64_t cols, int64_t ldx,
+                           const int64_t* __restrict__ exps, int axis, double* __restrict__ out,
+                           int64_t ldo, unsigned long long* flags) {
+  const int64_t total = rows * cols;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / cols, j = t % cols;
+    int64_t e = exps[axis == 0 ? i : j];
+    // np.ldexp with an out-of-range exponent saturates: beyond +-2200 every
+    // finite nonzero double has already overflowed / flushed to zero
+    e = e > 2200 ? 2200 : (e < -2200 ? -2200 : e);
+    const double v = ldexp(x[i * ldx + j], int(e));
+    if (fabs(v) >= 0x1p90) atomicAdd(flags, 1ull);
+    out[i * ldo + j] = trunc(v);
+  }
+}
+}  // namespace
+
+int launch_log2_upper(const double* x, int64_t n, float* out, unsigned long long* flags,
+                      cudaStream_t s) {
+  if (n <= 0) return 0;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+  k_log2_upper_arr<<<unsigned(blocks), 256, 0, s>>>(x, n, out, flags);
+  return launched(1);
+}
+
+int launch_quantize(const double* x, int64_t rows, int64_t cols, int64_t ldx, const int64_t* exps,
+                    int axis, double* out, int64_t ldo, unsigned long long* flags,
+                    cudaStream_t s) {
+  const int64_t total = rows * cols;
+  if (total <= 0) return 0;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_quantize<<<unsigned(blocks), 256, 0, s>>>(x, rows, cols, ldx, exps, axis, out, ldo, flags);
+  return launched(1);
+}
+
 }  // namespace crtg
