@@ -20,6 +20,10 @@
 #ifndef CRTG_CRT_UNROLL
 #define CRTG_CRT_UNROLL 0
 #endif
+// the complex pipeline's CRT specialised on the modulus count (k_crt_n)
+#ifndef CRTG_CRT_TEMPLATED
+#define CRTG_CRT_TEMPLATED 1
+#endif
 #ifndef CRTG_CRT_BATCH
 #define CRTG_CRT_BATCH 8
 #endif
@@ -266,6 +270,142 @@ __global__ void __launch_bounds__(256, CRTG_CRT_MINB) k_crt(int64_t m, int64_t n
   }  // grid-stride loop
 }
 
+// ---------------------------------------------------------------------------
+// k_crt_n: the complex-pipeline CRT with the modulus count N a compile-time
+// constant.  Same arithmetic, in the same order, as k_crt<SINGLE, LIMBS=true,
+// REAL=false>; what changes is the instruction stream around it:
+//  * every modulus loop is fully unrolled, so coeff_lo[l] and the S1 limb pairs
+//    are constant-bank operands of the DMUL / IDP (no per-modulus LDC, no loop
+//    branches or bounds checks); all 2N residue words are loaded up front;
+//  * the quotient z = ceil(fl(fl(S / p_hi) - 0.5)) (crt.py:166-167) is formed as
+//    ceil(fl(S * (1/p_hi)) - 0.5) with one round-up add of 1.5 * 2^52 (valid for
+//    |d| < 2^51); the two quotients differ by < 2^-39 (|S / p_hi| < 2^13), so
+//    whenever the candidate z lies more than 2^-24 inside (d, d + 1) it equals the
+//    reference's ceil, and otherwise the exact division runs.  A zero z comes out
+//    as +0 where numpy's ceil gives -0: z only enters through p_hi * z and
+//    p_lo * z, and with S1 = +0 (integer limbs) every signed zero downstream is
+//    the same either way (K4).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double quotient_z_fast(double s, const DevConsts& dc) {
+  const double e = __dmul_rn(s, dc.inv_p);
+  const double d = __dsub_rn(e, 0.5);
+  const double z = __dsub_rn(__dadd_ru(d, 0x1.8p52), 0x1.8p52);  // ceil(d)
+  if (fabs(__dsub_rn(z, e)) < 0.5 - 0x1p-24) return z;
+  return ceil(__dsub_rn(__ddiv_rn(s, dc.p_hi), 0.5));
+}
+
+__device__ __forceinline__ double reduce_double_fast(double s1, double s2, const DevConsts& dc) {
+  const DD hl = two_sum(s1, s2);
+  const double z = quotient_z_fast(hl.hi, dc);
+  DD pz = two_prod_p(dc.p_hi, z);
+  pz.lo = __dadd_rn(pz.lo, __dmul_rn(dc.p_lo, z));
+  pz = quick_two_sum(pz.hi, pz.lo);
+  const DD r = dd_add(hl.hi, hl.lo, -pz.hi, -pz.lo);
+  return __dadd_rn(r.hi, r.lo);
+}
+
+__device__ __forceinline__ double reduce_single_fast(double s, const DevConsts& dc) {
+  const double z = quotient_z_fast(__dadd_rn(s, 0.0), dc);
+  return __dsub_rn(__dsub_rn(s, __dmul_rn(z, dc.p_hi)), __dmul_rn(z, dc.p_lo));
+}
+
+template <int N, bool SINGLE>
+__global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
+    k_crt_n(int64_t m, int64_t n, const int8_t* __restrict__ e_re, const int8_t* __restrict__ e_im,
+            int64_t e_plane, int64_t e_ld, const int32_t* __restrict__ mu,
+            const int32_t* __restrict__ nu, const __grid_constant__ DevConsts dc, void* C,
+            int64_t ldc) {
+  const int64_t nq = (n + 3) >> 2;
+  const int64_t jq = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (jq >= nq) return;
+  const int64_t j0 = jq * 4;
+  for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
+    const int8_t* pr = e_re + i * e_ld + j0;
+    const int8_t* pi = e_im + i * e_ld + j0;
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(pi) | uintptr_t(e_plane)) &
+         3) == 0 &&
+        j0 + 4 <= n;
+    uint32_t wr[N + (N & 1)], wi[N + (N & 1)];
+    if (aligned) {
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        wr[l] = __ldg(reinterpret_cast<const uint32_t*>(pr + l * e_plane));
+        wi[l] = __ldg(reinterpret_cast<const uint32_t*>(pi + l * e_plane));
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        wr[l] = load_word(pr + l * e_plane, false, j0, n);
+        wi[l] = load_word(pi + l * e_plane, false, j0, n);
+      }
+    }
+    if (N & 1) wr[N + (N & 1) - 1] = wi[N + (N & 1) - 1] = 0u;
+    // per modulus pair: S1 as exact integer limb sums (two moduli per dp2a), then
+    // S2 -- the rounded f64 sequence of crt.py:239-240, l ascending, no FMA
+    int32_t tr[3][4] = {}, ti[3][4] = {};
+    double s2r[4] = {0, 0, 0, 0}, s2i[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int l = 0; l < N; l += 2) {
+      const uint32_t r01 = __byte_perm(wr[l], wr[l + 1], 0x5140);
+      const uint32_t r23 = __byte_perm(wr[l], wr[l + 1], 0x7362);
+      const uint32_t i01 = __byte_perm(wi[l], wi[l + 1], 0x5140);
+      const uint32_t i23 = __byte_perm(wi[l], wi[l + 1], 0x7362);
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const uint32_t hp = dc.limb_pair[l >> 1][t];
+        tr[t][0] = dp2a_lo(hp, r01, tr[t][0]);
+        tr[t][1] = dp2a_hi(hp, r01, tr[t][1]);
+        tr[t][2] = dp2a_lo(hp, r23, tr[t][2]);
+        tr[t][3] = dp2a_hi(hp, r23, tr[t][3]);
+        ti[t][0] = dp2a_lo(hp, i01, ti[t][0]);
+        ti[t][1] = dp2a_hi(hp, i01, ti[t][1]);
+        ti[t][2] = dp2a_lo(hp, i23, ti[t][2]);
+        ti[t][3] = dp2a_hi(hp, i23, ti[t][3]);
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        if (l + b >= N) break;
+        const double cl = dc.coeff_lo[l + b];
+        const uint32_t xr = wr[l + b] ^ 0x80808080u, xi = wi[l + b] ^ 0x80808080u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, byte_to_f64(xr, q)));
+          s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, byte_to_f64(xi, q)));
+        }
+      }
+    }
+    const int32_t mi = mu[i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t j = j0 + q;
+      if (j >= n) break;
+      const int64_t ir = (int64_t(tr[2][q]) << 32) + (int64_t(tr[1][q]) << 16) + tr[0][q];
+      const int64_t ii = (int64_t(ti[2][q]) << 32) + (int64_t(ti[1][q]) << 16) + ti[0][q];
+      const double s1r = __dmul_rn(double(ir), dc.hi_scale);  // exact
+      const double s1i = __dmul_rn(double(ii), dc.hi_scale);
+      const int ex = -mi - nu[j];
+      if (SINGLE) {
+        const double cr = reduce_single_fast(__dadd_rn(s1r, s2r[q]), dc);
+        const double ci = reduce_single_fast(__dadd_rn(s1i, s2i[q]), dc);
+        const float re = __double2float_rn(ldexp_rn(cr, ex));
+        const float im = __double2float_rn(ldexp_rn(ci, ex));
+        float2 o;
+        o.x = __fadd_rn(re, __fsub_rn(__fmul_rn(0.0f, im), 0.0f));
+        o.y = __fadd_rn(0.0f, __fadd_rn(0.0f, im));
+        reinterpret_cast<float2*>(C)[i * ldc + j] = o;
+      } else {
+        const double re = ldexp_rn(reduce_double_fast(s1r, s2r[q], dc), ex);
+        const double im = ldexp_rn(reduce_double_fast(s1i, s2i[q], dc), ex);
+        double2 o;
+        o.x = __dadd_rn(re, __dsub_rn(__dmul_rn(0.0, im), 0.0));
+        o.y = __dadd_rn(0.0, __dadd_rn(0.0, im));
+        reinterpret_cast<double2*>(C)[i * ldc + j] = o;
+      }
+    }
+  }
+}
+
 }  // namespace
 
 int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
@@ -280,6 +420,25 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
   if (max_ctas > 0) gy = std::max<int64_t>(1, std::min<int64_t>(gy, max_ctas / int64_t(gx)));
   const dim3 grid(gx, unsigned(gy));
   const bool limbs = dc.hi_scale != 0.0;
+#if CRTG_CRT_TEMPLATED
+  if (!real && limbs && dc.n >= 1 && dc.n <= CRTG_MAX_MODULI) {
+#define CRTG_CRT_N(NN)                                                                      \
+  case NN:                                                                                  \
+    if (single)                                                                             \
+      k_crt_n<NN, true><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc); \
+    else                                                                                    \
+      k_crt_n<NN, false><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc); \
+    break;
+    switch (dc.n) {
+      CRTG_CRT_N(1) CRTG_CRT_N(2) CRTG_CRT_N(3) CRTG_CRT_N(4) CRTG_CRT_N(5)
+      CRTG_CRT_N(6) CRTG_CRT_N(7) CRTG_CRT_N(8) CRTG_CRT_N(9) CRTG_CRT_N(10)
+      CRTG_CRT_N(11) CRTG_CRT_N(12) CRTG_CRT_N(13) CRTG_CRT_N(14) CRTG_CRT_N(15)
+      CRTG_CRT_N(16) CRTG_CRT_N(17) CRTG_CRT_N(18) CRTG_CRT_N(19) CRTG_CRT_N(20)
+    }
+#undef CRTG_CRT_N
+    return launched(1);
+  }
+#endif
 #define CRTG_CRT(S, L, R) \
   k_crt<S, L, R><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
   if (real) {
