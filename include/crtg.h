@@ -10,8 +10,11 @@
  *
  * Conventions
  *   - All matrix pointers are DEVICE pointers; `stream` is a cudaStream_t (NULL =
- *     legacy default stream).  Every launch is stream-ordered; no call allocates
- *     memory: scratch comes from the caller-owned workspace `ws`.
+ *     legacy default stream).  Every launch is stream-ordered; scratch comes from
+ *     the caller-owned workspace `ws`.  The only memory the library allocates
+ *     itself is the small, documented "library-held state" below (a one-time
+ *     device tree per (device, k) and, for pageable host operands only, a pinned
+ *     staging ring released by crtg_release_host_staging()).
  *   - Complex matrices are interleaved (re, im) pairs, row-major, with a row
  *     stride `ld*` counted in complex elements.  Inputs are complex128, or
  *     complex64 with CRTG_IN_C64 (upcast exactly, emulate.py:159-166); the

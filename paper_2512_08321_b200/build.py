@@ -27,8 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
           "--expt-relaxed-constexpr"]
 EXACT = {"scaling.cu", "residue.cu", "crt.cu", "accuracy.cu"}
-SOURCES = ["api.cu", "gemm_tc.cu", "scaling.cu", "residue.cu", "crt.cu",
-           "accuracy.cu"]
+SOURCES = ["api.cu", "gemm_tc.cu", "scaling.cu", "residue.cu", "crt.cu", "accuracy.cu"]
 
 
 def nvcc() -> str:

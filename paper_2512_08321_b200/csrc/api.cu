@@ -783,31 +783,21 @@ int crtg_scaling(int precision, int mode, int64_t m, int64_t n, int64_t k, const
   return CRTG_OK;
 }
 
-int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, const void* A,
-                      int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
-                      const crtg_consts* K, int64_t n_block, void* ws, size_t ws_bytes,
-                      int32_t* mu_out, int32_t* nu_out, uint64_t* diag, int sync_check,
-                      void* stream) {
-  int N = 0;
-  if (int e = check_consts(K, &N)) return e;
-  if ((precision & ~(CRTG_SINGLE | CRTG_IN_C64)) != 0)
-    return fail(CRTG_ERR_CONFIG, "precision must be double or single");
-  if (mode != CRTG_FAST && mode != CRTG_ACCURATE) return fail(CRTG_ERR_CONFIG, "bad mode");
-  if (int e = check_dims(m, n, k, lda, ldb, ldc)) return e;
-  const Plan P = make_plan(mode, m, n, k, N, n_block);
-  if (!ws || ws_bytes < P.total)
-    return fail(CRTG_ERR_WORKSPACE, "workspace too small: need " + std::to_string(P.total));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool in32 = (precision & CRTG_IN_C64) != 0;
-  const bool single = (precision & CRTG_SINGLE) != 0;  // result type / CRT path
-  unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
-                                : at<unsigned long long>(ws, P.diag);
+}  // extern "C"
+
+namespace {
+
+// the launch sequence of one complex product (scaling, residues, GEMMs, CRT);
+// every launch is stream-ordered on s (plus the forked B chain joined back)
+int enqueue_complex(const Plan& P, int precision, int mode, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, void* C, int64_t ldc, const DevConsts& dc,
+                    void* ws, int32_t* mu_out, int32_t* nu_out, unsigned long long* dg,
+                    cudaStream_t s) {
   CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
-  const DevConsts dc = make_dev(*K);
   Events E;
   cudaStream_t side = side_stream(s);
   // B's chain (column statistics, residues of block 0) on `aux`
-  const bool forked = side == s && fork_wanted(P.m_pad, P.n_pad, n, P.nb);
+  const bool forked = side == s && fork_wanted(P.m_pad, P.n_pad, P.n, P.nb);
   cudaStream_t aux = forked ? fork_stream() : side;
   cudaEvent_t ev0 = E.get();
   CRTG_TRY(cudaEventRecord(ev0, s), "record");
@@ -823,10 +813,147 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
   if (int e = run_pipeline(P, precision, A, lda, B, ldb, C, ldc, dc, mu, nu, ws, dg, s, side, E,
                            forked ? aux : nullptr))
     return e;
-  if (mu_out) CRTG_TRY(cudaMemcpyAsync(mu_out, mu, 4 * m, cudaMemcpyDeviceToDevice, s), "copy");
-  if (nu_out) CRTG_TRY(cudaMemcpyAsync(nu_out, nu, 4 * n, cudaMemcpyDeviceToDevice, s), "copy");
-  if (sync_check) return check_diag(dg, s);
+  if (mu_out) CRTG_TRY(cudaMemcpyAsync(mu_out, mu, 4 * P.m, cudaMemcpyDeviceToDevice, s), "copy");
+  if (nu_out) CRTG_TRY(cudaMemcpyAsync(nu_out, nu, 4 * P.n, cudaMemcpyDeviceToDevice, s), "copy");
   return CRTG_OK;
+}
+
+// Small products are launch-bound: ~10 kernels, a dozen events and two streams
+// per call cost more host time than the GPU work below ~2048^3.  The second
+// call with identical arguments (pointers, shape, constants) captures the
+// launch sequence into a CUDA graph; later calls replay it with one
+// cudaGraphLaunch.  Replays run the same kernels on the same buffers, so the
+// results are bitwise those of the eager path.  Per host thread, at most
+// kGraphCache graphs are kept (least recently used evicted).
+struct GraphKey {
+  int precision, mode, dev;
+  int64_t m, n, k, lda, ldb, ldc, n_block;
+  const void *A, *B;
+  void *C, *ws;
+  size_t ws_bytes;
+  int32_t *mu_out, *nu_out;
+  unsigned long long* dg;
+  crtg_consts K;
+  bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+struct GraphEntry {
+  GraphKey key;
+  int seen = 0;
+  int kernels = 0;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t used = 0;
+};
+constexpr size_t kGraphCache = 16;
+
+cudaStream_t capture_stream() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  thread_local std::map<int, cudaStream_t> streams;
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t st = nullptr;
+  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  streams[dev] = st;
+  return st;
+}
+
+bool graph_wanted(const Plan& P, cudaStream_t s) {
+  static const bool on = env_int("CRTG_GRAPHS", 1) != 0;
+  if (!on || g_prof_on || P.nb < P.n) return false;
+  if (double(P.m) * double(P.n) * double(P.k) > 8.6e9) return false;  // above ~2048^3
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone)
+    return false;  // the caller is capturing: stay in its graph
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, const void* A,
+                      int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                      const crtg_consts* K, int64_t n_block, void* ws, size_t ws_bytes,
+                      int32_t* mu_out, int32_t* nu_out, uint64_t* diag, int sync_check,
+                      void* stream) {
+  int N = 0;
+  if (int e = check_consts(K, &N)) return e;
+  if ((precision & ~(CRTG_SINGLE | CRTG_IN_C64)) != 0)
+    return fail(CRTG_ERR_CONFIG, "precision must be double or single");
+  if (mode != CRTG_FAST && mode != CRTG_ACCURATE) return fail(CRTG_ERR_CONFIG, "bad mode");
+  if (int e = check_dims(m, n, k, lda, ldb, ldc)) return e;
+  const Plan P = make_plan(mode, m, n, k, N, n_block);
+  if (!ws || ws_bytes < P.total)
+    return fail(CRTG_ERR_WORKSPACE, "workspace too small: need " + std::to_string(P.total));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
+                                : at<unsigned long long>(ws, P.diag);
+  const DevConsts dc = make_dev(*K);
+  if (!graph_wanted(P, s)) {
+    if (int e = enqueue_complex(P, precision, mode, A, lda, B, ldb, C, ldc, dc, ws, mu_out, nu_out,
+                                dg, s))
+      return e;
+    return sync_check ? check_diag(dg, s) : CRTG_OK;
+  }
+  GraphKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.precision = precision;
+  key.mode = mode;
+  cudaGetDevice(&key.dev);
+  key.m = m; key.n = n; key.k = k; key.lda = lda; key.ldb = ldb; key.ldc = ldc;
+  key.n_block = n_block;
+  key.A = A; key.B = B; key.C = C; key.ws = ws; key.ws_bytes = ws_bytes;
+  key.mu_out = mu_out; key.nu_out = nu_out; key.dg = dg;
+  std::memcpy(&key.K, K, sizeof(crtg_consts));
+  static thread_local std::vector<GraphEntry> cache;
+  static thread_local uint64_t tick = 0;
+  GraphEntry* hit = nullptr;
+  for (auto& g : cache)
+    if (g.key == key) hit = &g;
+  if (!hit) {
+    if (cache.size() >= kGraphCache) {
+      auto lru = std::min_element(cache.begin(), cache.end(), [](const GraphEntry& a,
+                                                                 const GraphEntry& b) {
+        return a.used < b.used;
+      });
+      if (lru->exec) cudaGraphExecDestroy(lru->exec);
+      cache.erase(lru);
+    }
+    cache.push_back(GraphEntry{key});
+    hit = &cache.back();
+  }
+  hit->used = ++tick;
+  if (!hit->exec && ++hit->seen >= 2) {
+    // second identical call: capture the launch sequence (the first one ran
+    // eagerly and created every lazily initialised resource)
+    // captured on a private stream: the caller's may be the legacy default
+    // stream, which cannot be captured; the graph is then launched on s
+    const uint64_t before = crtg_launch_count();
+    cudaStream_t cs = capture_stream();
+    CRTG_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "capture");
+    const int e = enqueue_complex(P, precision, mode, A, lda, B, ldb, C, ldc, dc, ws, mu_out,
+                                  nu_out, dg, cs);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
+    if (e) {
+      if (graph) cudaGraphDestroy(graph);
+      return e;
+    }
+    CRTG_TRY(int(ec), "end capture");
+    const cudaError_t ei = cudaGraphInstantiate(&hit->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    CRTG_TRY(int(ei), "graph instantiate");
+    hit->kernels = int(crtg_launch_count() - before);
+    note_launches(-hit->kernels);  // counted when replayed below
+  }
+  if (hit->exec) {
+    CRTG_TRY(cudaGraphLaunch(hit->exec, s), "graph launch");
+    note_launches(hit->kernels);
+  } else if (int e = enqueue_complex(P, precision, mode, A, lda, B, ldb, C, ldc, dc, ws, mu_out,
+                                     nu_out, dg, s)) {
+    return e;
+  }
+  return sync_check ? check_diag(dg, s) : CRTG_OK;
 }
 
 int crtg_residues(int precision, int operand, int64_t rows, int64_t kdim, const void* X,

@@ -175,6 +175,23 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   } while (!done);
 }
 
+// Warp-collective wait: every lane leaves the spin together.  The plain per-lane
+// spin can leave a warp diverged (ptxas moves the retry loop out of line and a
+// __syncwarp after it may be elided), and the tcgen05.ld / wait::ld that follow
+// are .sync.aligned: executed by part of a warp they return undefined data.
+__device__ __forceinline__ void mbar_wait_warp(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!__all_sync(0xffffffffu, done));
+}
+
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (TMA engine)
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
                                          uint32_t bar) {

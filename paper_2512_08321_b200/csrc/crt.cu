@@ -309,6 +309,24 @@ __device__ __forceinline__ double reduce_single_fast(double s, const DevConsts& 
   return __dsub_rn(__dsub_rn(s, __dmul_rn(z, dc.p_hi)), __dmul_rn(z, dc.p_lo));
 }
 
+// residue byte q of a raw e-plane word (signed bytes) -> (double)e:
+//  0: 2^52 + (e + 128) built in a register pair, minus 2^52 + 128 (FP64 pipe)
+//  1: sign-extending PRMT + I2F.F64.S32 (conversion pipe)
+#ifndef CRTG_CRT_CVT
+#define CRTG_CRT_CVT 2
+#endif
+__device__ __forceinline__ double raw_byte_to_f64(uint32_t w, int q) {
+#if CRTG_CRT_CVT == 1
+  return double(int32_t(__byte_perm(w, 0, 0x8880 + q + 0x0000)));
+#elif CRTG_CRT_CVT == 2
+  double d;
+  asm("cvt.rn.f64.s8 %0, %1;" : "=d"(d) : "h"(static_cast<unsigned short>(w >> (8 * q))));
+  return d;
+#else
+  return byte_to_f64(w ^ 0x80808080u, q);
+#endif
+}
+
 template <int N, bool SINGLE>
 __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
     k_crt_n(int64_t m, int64_t n, const int8_t* __restrict__ e_re, const int8_t* __restrict__ e_im,
@@ -367,11 +385,10 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
       for (int b = 0; b < 2; ++b) {
         if (l + b >= N) break;
         const double cl = dc.coeff_lo[l + b];
-        const uint32_t xr = wr[l + b] ^ 0x80808080u, xi = wi[l + b] ^ 0x80808080u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, byte_to_f64(xr, q)));
-          s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, byte_to_f64(xi, q)));
+          s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, raw_byte_to_f64(wr[l + b], q)));
+          s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, raw_byte_to_f64(wi[l + b], q)));
         }
       }
     }

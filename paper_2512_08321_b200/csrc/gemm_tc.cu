@@ -198,8 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
       const int col_base = tn * 256 + 128 * half;
       if (MODE == EPI_BOUND) {
         const uint32_t par = (gslot >> 1) & 1;
-        mbar_wait(smem_u32(&tfull_bar[0]), par);
-        mbar_wait(smem_u32(&tfull_bar[1]), par);
+        mbar_wait_warp(smem_u32(&tfull_bar[0]), par);
+        mbar_wait_warp(smem_u32(&tfull_bar[1]), par);
         tc_fence_after();
         int32_t rmax = 0;
 #pragma unroll 1
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
       const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const uint32_t buf = gslot & 1;
-        mbar_wait(smem_u32(&tfull_bar[buf]), (gslot >> 1) & 1);
+        mbar_wait_warp(smem_u32(&tfull_bar[buf]), (gslot >> 1) & 1);
         tc_fence_after();
         epilogue_phase<MODE, 4>(g, lane_addr + buf * 256, s, l, row, row_ok, col_base, mc, st);
         tc_fence_before();
@@ -278,13 +278,24 @@ constexpr uint32_t kWStageBytes = kWStageA + kWStageB;
 #endif
 constexpr int kWStages = CRTG_W_STAGES;
 constexpr int kWGroupM = 8;  // 256-row tiles per column sweep
+#ifndef CRTG_MOD_INNER
+#define CRTG_MOD_INNER 0
+#endif
 
 __device__ __forceinline__ void decode_tile_w(int t, const GemmArgs& g, int& l, int& tm2,
                                               int& tn) {
   const int mt2 = g.mt >> 1;
   const int per = mt2 * g.nt;
+#if CRTG_MOD_INNER
+  // experiment: modulus index innermost, so the N moduli of
+  // one output tile run back to back (the ordering an in-CTA CRT would need)
+  l = t % g.nl;
+  const int r = t / g.nl;
+  (void)per;
+#else
   l = t / per;
   const int r = t - l * per;
+#endif
   const int G = g.group_m > 0 ? g.group_m : kWGroupM;
   const int grp = r / (G * g.nt);
   const int first = grp * G;
@@ -404,7 +415,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
       const ModConst mc = g.mc[l];
       const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
-        mbar_wait(smem_u32(&tfull_bar), gslot & 1);
+        mbar_wait_warp(smem_u32(&tfull_bar), gslot & 1);  // warp-converged for tcgen05.ld
         tc_fence_after();
         epilogue_phase<MODE, NCH>(g, lane_addr, s, l, row, row_ok, col_base, mc, st);
         tc_fence_before();
