@@ -246,6 +246,32 @@ void make_split(ModConst& mc, ResConst& rc, int p) {
   rc.gjn = uint32_t(p - j);
   rc.gku = uint32_t((p - (j * off) % p) % p);
   rc.gkv = uint32_t((p - ((p - j) * off) % p) % p);
+  // direct U / V tables (residue.cu: res_uv)
+  auto bytes_of = [&](uint32_t w, int i) { return (w >> (8 * i)) & 0xFFu; };
+  auto scale_tab = [&](uint32_t w, int n, int jj) {
+    uint32_t o = 0;
+    for (int i = 0; i < n; ++i) o |= ((uint32_t(jj) * bytes_of(w, i)) % uint32_t(p)) << (8 * i);
+    return o;
+  };
+  rc.uw0123 = scale_tab(rc.dw0123, 4, j);
+  rc.uw45 = scale_tab(rc.dw45, 2, j);
+  rc.vw0123 = scale_tab(rc.dw0123, 4, p - j);
+  rc.vw45 = scale_tab(rc.dw45, 2, p - j);
+  auto pow2_mod = [&](int e) {
+    uint64_t t = 1 % uint64_t(p);
+    for (int i = 0; i < e; ++i) t = (t * 2) % uint64_t(p);
+    return int64_t(t);
+  };
+  auto kk = [&](int jj, int e) {  // (off - (1 + jj) 2^e) mod p
+    const int64_t v = (int64_t(off) - (1 + jj) * pow2_mod(e)) % p;
+    return uint32_t(v < 0 ? v + p : v);
+  };
+  rc.ku31 = kk(j, 31);
+  rc.ku63 = kk(j, 63);
+  rc.kuw = kk(j, 90);
+  rc.kv31 = kk(p - j, 31);
+  rc.kv63 = kk(p - j, 63);
+  rc.kvw = kk(p - j, 90);
 }
 
 // residue-kernel constants of modulus p for the stored representative t - off

@@ -88,6 +88,10 @@ struct ResConst {
   // t_U = (t_re + j t_im + gku) mod p, t_V = (t_re + (p - j) t_im + gkv) mod p
   // with gku = (-j off) mod p, gkv = (-(p - j) off) mod p
   uint32_t split, gj, gjn, gku, gkv;
+  // the same planes straight from the value limbs: u_U = sum_i limb_i(re) c_i +
+  // sum_i limb_i(im) (j c_i mod p) + kU, congruent to re + j im + off (V: p - j)
+  uint32_t uw0123, uw45, vw0123, vw45;  // byte tables of j c_i, (p - j) c_i mod p
+  uint32_t ku31, ku63, kuw, kv31, kv63, kvw;  // (off - (1 + j) 2^31|63|90) mod p, V likewise
 };
 
 struct DevConsts {

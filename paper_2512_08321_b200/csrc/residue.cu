@@ -132,6 +132,29 @@ constexpr int kResRows = 16;
 #define CRTG_RES_UNROLL 1
 #endif
 
+// split modulus: t_U = (re + j im + off) mod p (V = 1: p - j) straight from the
+// limbs of both values (u < 2 * 6 * 2^16 * 255 + p < 2^28, one reduction)
+template <int FORM>
+__device__ __forceinline__ uint32_t res_uv(const Val3& vr, const Val3& vi, const ResConst& c,
+                                           int V) {
+  const uint32_t w = V ? c.vw0123 : c.uw0123;
+  uint32_t u;
+  if (FORM == 3) {
+    u = dp2a_lo(vi.w0, w, V ? c.kvw : c.kuw);
+    u = dp2a_hi(vi.w1, w, u);
+    u = dp2a_lo(vi.w2, V ? c.vw45 : c.uw45, u);
+    u = dp2a_lo(vr.w0, c.dw0123, u);
+    u = dp2a_hi(vr.w1, c.dw0123, u);
+    u = dp2a_lo(vr.w2, c.dw45, u);
+  } else if (FORM == 2) {
+    u = dp2a_hi(vi.w1, w, dp2a_lo(vi.w0, w, V ? c.kv63 : c.ku63));
+    u = dp2a_hi(vr.w1, c.dw0123, dp2a_lo(vr.w0, c.dw0123, u));
+  } else {
+    u = dp2a_lo(vr.w0, c.dw0123, dp2a_lo(vi.w0, w, V ? c.kv31 : c.ku31));
+  }
+  return mod_small(u, c);
+}
+
 // 4 values t_i in [0,p) -> packed int8 (t_i - off)
 template <bool SYM>
 __device__ __forceinline__ uint32_t pack_t(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
@@ -152,23 +175,24 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
                                               const ResConst& c, uint32_t (&w)[3][2]) {
 #pragma unroll
   for (int half = 0; half < 2; ++half) {
-    uint32_t tr[4], ti[4], ts[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      tr[j] = res_t<FORM>(re[4 * half + j], c);
-      ti[j] = res_t<FORM>(im[4 * half + j], c);
-    }
     if (c.split) {
+      // U = re + j im, V = re - j im, each one reduction of a limb sum over both
+      // values (no separate re / im residues)
       uint32_t tu[4], tv[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        // (re + j im) + off = (tr - off) + j (ti - off) + off  (mod p); likewise with p - j
-        tu[j] = mod_small(mad_lo(ti[j], c.gj, tr[j] + c.gku), c);
-        tv[j] = mod_small(mad_lo(ti[j], c.gjn, tr[j] + c.gkv), c);
+        tu[j] = res_uv<FORM>(re[4 * half + j], im[4 * half + j], c, 0);
+        tv[j] = res_uv<FORM>(re[4 * half + j], im[4 * half + j], c, 1);
       }
       w[0][half] = pack_t<SYM>(tu[0], tu[1], tu[2], tu[3], c.off);
       w[1][half] = pack_t<SYM>(tv[0], tv[1], tv[2], tv[3], c.off);
     } else {
+      uint32_t tr[4], ti[4], ts[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        tr[j] = res_t<FORM>(re[4 * half + j], c);
+        ti[j] = res_t<FORM>(im[4 * half + j], c);
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         // (re + im) + off = (tr - off) + (ti - off) + off  (mod p); x < 3p, so two

@@ -129,7 +129,7 @@ def emulate_gemm_complex(a, b, cfg: EmuConfig | None = None,
         return empty
     dev = _device()
     on_dev = [isinstance(x, torch.Tensor) and x.is_cuda for x in (a, b)]
-    if not any(on_dev):
+    if not any(on_dev) and cfg.strategy == "karatsuba":
         # host operands: stream them through the copy engines (crtg_gemm_complex_host)
         pins = _HostPins()
         try:
@@ -143,7 +143,10 @@ def emulate_gemm_complex(a, b, cfg: EmuConfig | None = None,
     at, a_torch = _to_device_matrix(a, "A", dev)
     bt, b_torch = _to_device_matrix(b, "B", dev)
     _check_shapes(at, bt)
-    out = run_complex(at, bt, cfg, diagnostics, dev)
+    if cfg.strategy != "karatsuba":
+        out = _emulate_complex_stages(at, bt, cfg, diagnostics)
+    else:
+        out = run_complex(at, bt, cfg, diagnostics, dev)
     if a_torch and b_torch:
         return out
     return out.cpu().numpy()
@@ -493,8 +496,9 @@ def _residue_bounds(p):
 
 def complex_gemm_mod(ar, ai, br, bi, p: int, strategy: str = "karatsuba",
                      n_block: int = 8192):
-    """Modular complex product on residue operands (reference kernel.py:70-120).
-    All strategies are bitwise identical; the GPU runs the Karatsuba form."""
+    """Modular complex product on residue operands (reference kernel.py:70-120):
+    Karatsuba (three tcgen05 products, crtg_complex_gemm_mod) or the expanded
+    formulations (one product on doubled operands, _expand_gemm_mod)."""
     if strategy not in STRATEGIES:
         raise DimensionError(f"unknown strategy {strategy!r}")
     if n_block < 1:
@@ -516,16 +520,105 @@ def complex_gemm_mod(ar, ai, br, bi, p: int, strategy: str = "karatsuba",
     for name, t in (("ar", art), ("ai", ait), ("br", brt), ("bi", bit)):
         if t.numel() and (int(t.min()) < lo or int(t.max()) > hi):
             raise DimensionError(f"{name} entries outside residue range of p={p}")
-    lib = nat.load()
-    ws = _workspace(lib.crtg_i8_workspace_size(m, n, k, 3), dev)
-    er = torch.empty((m, n), dtype=torch.int8, device=dev)
-    ei = torch.empty((m, n), dtype=torch.int8, device=dev)
-    nat.call("crtg_complex_gemm_mod", m, n, k, art.data_ptr(), ait.data_ptr(), brt.data_ptr(),
-             bit.data_ptr(), int(p), er.data_ptr(), ei.data_ptr(), ws.data_ptr(), ws.numel(),
-             _stream_ptr(dev))
+    if strategy == "karatsuba":
+        lib = nat.load()
+        ws = _workspace(lib.crtg_i8_workspace_size(m, n, k, 3), dev)
+        er = torch.empty((m, n), dtype=torch.int8, device=dev)
+        ei = torch.empty((m, n), dtype=torch.int8, device=dev)
+        nat.call("crtg_complex_gemm_mod", m, n, k, art.data_ptr(), ait.data_ptr(), brt.data_ptr(),
+                 bit.data_ptr(), int(p), er.data_ptr(), ei.data_ptr(), ws.data_ptr(), ws.numel(),
+                 _stream_ptr(dev))
+    else:
+        er, ei = _expand_gemm_mod(art, ait, brt, bit, int(p), strategy, n_block)
     if all(isinstance(x, torch.Tensor) for x in (ar, ai, br, bi)):
         return er, ei
     return er.cpu().numpy(), ei.cpu().numpy()
+
+
+def _sym_i8(t: torch.Tensor, p: int) -> torch.Tensor:
+    """Symmetric residues (symmetric_mod_int, crt.py:136-151) of an int32 / int64
+    device tensor, as int8, on the residue kernel."""
+    from .stages import _residues
+    kind = 2 if t.dtype == torch.int32 else 1
+    src = t if kind == 2 else t.to(torch.int64)
+    return _residues(src.contiguous().reshape(-1), kind, (p,))[0].reshape(t.shape)
+
+
+def _expand_gemm_mod(art, ait, brt, bit, p: int, strategy: str, n_block: int):
+    """The reference's expanded formulations (kernel.py:54-67): ONE integer GEMM
+    per column block on doubled operands -- [[ar, -ai], [ai, ar]] @ [br; bi]
+    (expand-rows) or [ai, ar] @ [[br, -bi], [bi, br]] (expand-cols) -- on the
+    tcgen05 gemm_i8_i32, reduced to symmetric residues.  Inner length 2k: like
+    the reference, a dot product beyond int32 raises ArithmeticError
+    (kernel.py:33-34) where the Karatsuba form cannot overflow."""
+    m, k = art.shape
+    n = brt.shape[1]
+    er = torch.empty((m, n), dtype=torch.int8, device=art.device)
+    ei = torch.empty((m, n), dtype=torch.int8, device=art.device)
+    if strategy == "expand-rows":
+        neg_ai = _sym_i8(-ait.to(torch.int32), p)
+        a_hat = torch.cat([torch.cat([art, neg_ai], 1), torch.cat([ait, art], 1)], 0).contiguous()
+        for j0 in range(0, n, n_block):
+            j1 = min(j0 + n_block, n)
+            b_hat = torch.cat([brt[:, j0:j1], bit[:, j0:j1]], 0).contiguous()
+            c = gemm_i8_i32(a_hat, b_hat)
+            er[:, j0:j1] = _sym_i8(c[:m], p)
+            ei[:, j0:j1] = _sym_i8(c[m:], p)
+    else:
+        neg_bi = _sym_i8(-bit.to(torch.int32), p)
+        a_hat = torch.cat([ait, art], 1).contiguous()
+        for j0 in range(0, n, n_block):
+            j1 = min(j0 + n_block, n)
+            w = j1 - j0
+            brb, bib = brt[:, j0:j1], bit[:, j0:j1]
+            b_hat = torch.cat([torch.cat([brb, neg_bi[:, j0:j1]], 1), torch.cat([bib, brb], 1)],
+                              0).contiguous()
+            c = gemm_i8_i32(a_hat, b_hat)
+            er[:, j0:j1] = _sym_i8(c[:, w:], p)
+            ei[:, j0:j1] = _sym_i8(c[:, :w], p)
+    return er, ei
+
+
+def _emulate_complex_stages(at: torch.Tensor, bt: torch.Tensor, cfg: EmuConfig,
+                            diagnostics: dict | None):
+    """emulate_gemm_complex for the expand strategies, stage by stage exactly as
+    the reference composes it (emulate.py:193-240): device exponents, quantize,
+    residue_decompose, one complex_gemm_mod per modulus with cfg.strategy, CRT
+    accumulate / reduce, inverse scale, re + 1j*im.  Every stage is a libcrtg
+    kernel; the result is bitwise that of the fused Karatsuba pipeline (all
+    strategies are identical by contract) unless an expanded dot product
+    leaves int32, which raises ArithmeticError as in the reference."""
+    from . import stages as stg
+    ms = select_moduli(cfg.resolved_moduli)
+    if at.dtype != torch.complex128:
+        at = at.to(torch.complex128)
+    if bt.dtype != torch.complex128:
+        bt = bt.to(torch.complex128)
+    sv = _scaling(at, bt, ms, nat.FAST if cfg.mode == "fast" else nat.ACCURATE, diagnostics)
+    dev = at.device
+    mu = torch.from_numpy(sv.mu_exp).to(dev)
+    nu = torch.from_numpy(sv.nu_exp).to(dev)
+    ar = stg.quantize(at.real.contiguous(), mu, 0)
+    ai = stg.quantize(at.imag.contiguous(), mu, 0)
+    br = stg.quantize(bt.real.contiguous(), nu, 1)
+    bi = stg.quantize(bt.imag.contiguous(), nu, 1)
+    st = [stg.residue_decompose(x, ms).entries for x in (ar, ai, br, bi)]
+    m, n = ar.shape[0], br.shape[1]
+    e_re = torch.empty((len(ms), m, n), dtype=torch.int8, device=dev)
+    e_im = torch.empty((len(ms), m, n), dtype=torch.int8, device=dev)
+    for idx, p in enumerate(ms.moduli):
+        e_re[idx], e_im[idx] = complex_gemm_mod(st[0][idx], st[1][idx], st[2][idx], st[3][idx],
+                                                p, strategy=cfg.strategy, n_block=cfg.n_block)
+    path = cfg.precision
+    c_re = stg.crt_reduce(stg.crt_accumulate(stg.ResidueStack(e_re, ms), ms, path), ms)
+    c_im = stg.crt_reduce(stg.crt_accumulate(stg.ResidueStack(e_im, ms), ms, path), ms)
+    odt = torch.float64 if cfg.precision == "double" else torch.float32
+    re = stg.inverse_scale(c_re, sv, odt)
+    im = stg.inverse_scale(c_im, sv, odt)
+    # numpy's re + 1j*im: real = re + (0*im - 0), imag = 0 + (0 + im)
+    real = re + (0.0 * im - 0.0)
+    imag = 0.0 + (0.0 + im)
+    return torch.complex(real, imag)
 
 
 def _scaling(a, b, ms: ModulusSet, mode: int, diagnostics):
