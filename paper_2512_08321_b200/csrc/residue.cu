@@ -278,7 +278,15 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
                                                   int64_t rb_count,
                                                   unsigned long long* __restrict__ overflow,
                                                   int n_kb, int n_rt, int row_base) {
-  __shared__ __align__(16) uint8_t stage[6][kResRows * 128];  // 2 x (3 planes)
+  // B of the complex pipeline (TIN): the tile's 128 K x 16 columns of B are
+  // transposed on the way IN (coalesced 256-byte rows into a swizzled shared
+  // tile, then each thread reads its column's 8 consecutive K), so its planes
+  // are stored like A's -- straight from registers, whole 128-byte lines, no
+  // per-modulus barrier.  Other B launches stage the planes on the way out.
+  constexpr bool TIN = OPERAND == 1 && !REAL;
+  constexpr int kStageBytes = TIN ? 128 * 16 * 2 * int(sizeof(T)) : 6 * kResRows * 128;
+  __shared__ __align__(16) uint8_t smem_buf[kStageBytes];
+  uint8_t (*stage)[kResRows * 128] = reinterpret_cast<uint8_t (*)[kResRows * 128]>(smem_buf);
   // representative of the stored residues: the symmetric (rc) or the 128-offset (rx) tables
   const ResConst* rcs = SYM ? dc.rc : dc.rx;
   // grid-stride over (K block, 16-row tile): a full grid when launched alone, one
@@ -288,7 +296,7 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
   const int kb = OPERAND == 0 ? tile % n_kb : tile / n_rt;
   const int r0 = (OPERAND == 0 ? tile / n_kb : tile % n_rt) * kResRows;
   int r, seg;  // row within the tile, 8-element K segment (0..15)
-  if (OPERAND == 0) {
+  if (OPERAND == 0 || TIN) {
     r = threadIdx.x >> 4;
     seg = threadIdx.x & 15;
   } else {
@@ -299,6 +307,34 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
   const int h0 = kb * 128 + seg * 8;
   const bool row_ok = row < rows;
   const int e = row_ok ? exps[row] : 0;
+  if constexpr (TIN) {
+    // rows h of the tile: 16 columns x (re, im) = 16 x 2 sizeof(T) bytes, slot of
+    // column c at c ^ (h / 8) (the reads below are then bank-conflict free)
+    constexpr int kEl = 2 * int(sizeof(T));
+    __syncthreads();  // the previous tile's reads are done
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = i * 256 + int(threadIdx.x);
+      const int hl = idx >> 4, c = idx & 15;
+      const int h = kb * 128 + hl;
+      const int col = r0 + c;
+      uint8_t* dst = smem_buf + hl * (16 * kEl) + ((c ^ ((hl >> 3) & 15)) * kEl);
+      if (h < kdim && col < rows) {
+        if constexpr (sizeof(T) == 8)
+          *reinterpret_cast<double2*>(dst) =
+              *reinterpret_cast<const double2*>(X + 2 * (int64_t(h) * ldx + col0 + col));
+        else
+          *reinterpret_cast<float2*>(dst) =
+              *reinterpret_cast<const float2*>(X + 2 * (int64_t(h) * ldx + col0 + col));
+      } else {
+        if constexpr (sizeof(T) == 8)
+          *reinterpret_cast<double2*>(dst) = make_double2(0.0, 0.0);
+        else
+          *reinterpret_cast<float2*>(dst) = make_float2(0.f, 0.f);
+      }
+    }
+    __syncthreads();
+  }
   // 2^e for e in [-1023, 1023] is representable (2^-1023 subnormal): one
   // correctly rounded multiply == np.ldexp
   const double scale = __longlong_as_double(e >= -1022 ? int64_t(e + 1023) << 52
@@ -312,7 +348,12 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
   for (int t = 0; t < 8; ++t) {
     const int h = h0 + t;
     double re = 0.0, im = 0.0;
-    if (row_ok && h < kdim) {
+    if constexpr (TIN) {
+      constexpr int kEl = 2 * int(sizeof(T));
+      const int hl = seg * 8 + t;
+      load_c<T, false>(reinterpret_cast<const T*>(smem_buf + hl * (16 * kEl) +
+                                                  ((r ^ seg) * kEl)), re, im);
+    } else if (row_ok && h < kdim) {
       const T* p = (OPERAND == 0) ? X + (REAL ? 1 : 2) * (int64_t(row) * ldx + h)
                                   : X + (REAL ? 1 : 2) * (int64_t(h) * ldx + col0 + row);
       load_c<T, REAL>(p, re, im);
@@ -391,11 +432,14 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
       }
     }
   } else if (huge) {  // MS: this CTA's share of the moduli
-    store_moduli<OPERAND, 3, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    store_moduli<TIN ? 0 : OPERAND, 3, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq,
+                                                cs, stage);
   } else if (medium) {
-    store_moduli<OPERAND, 2, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    store_moduli<TIN ? 0 : OPERAND, 2, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq,
+                                                cs, stage);
   } else {
-    store_moduli<OPERAND, 1, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq, cs, stage);
+    store_moduli<TIN ? 0 : OPERAND, 1, SYM, MS>(vr, vi, dc, rcs, out, plane_bytes, goff, soff, cq,
+                                                cs, stage);
   }
   }  // tile loop
 }

@@ -136,7 +136,9 @@ def emulate_gemm_complex(a, b, cfg: EmuConfig | None = None,
             ha, a_torch = _host_matrix(a, "A", pins)
             hb, b_torch = _host_matrix(b, "B", pins)
             _check_shapes(ha, hb)
-            out = run_complex_host(ha, hb, cfg, diagnostics, dev)  # synchronous
+            # numpy in -> numpy out owning plain memory; torch in -> pinned tensor
+            out = run_complex_host(ha, hb, cfg, diagnostics, dev,
+                                   pageable_out=not (a_torch and b_torch))  # synchronous
         finally:
             pins.release()
         return out if (a_torch and b_torch) else out.numpy()
@@ -212,9 +214,13 @@ def _host_matrix(x, name: str, pins: _HostPins):
 
 
 def run_complex_host(ha: torch.Tensor, hb: torch.Tensor, cfg: EmuConfig,
-                     diagnostics: dict | None = None, dev=None):
-    """Host (pinned) operands in, pinned host result out; H2D of B's column blocks
-    and D2H of C's blocks overlap the GPU work (crtg_gemm_complex_host)."""
+                     diagnostics: dict | None = None, dev=None, pageable_out: bool = False):
+    """Host operands in, host result out; H2D of B's column blocks and D2H of C's
+    blocks overlap the GPU work (crtg_gemm_complex_host).  The result is a
+    pinned tensor from torch's caching host allocator, or with pageable_out a
+    plain (pageable) tensor that owns its memory (numpy callers: results they
+    keep do not hold page-locked memory; the library stages the copy-back
+    through its pinned ring)."""
     dev = dev or _device()
     if ha.dtype != hb.dtype:  # mixed complex64 / complex128: widen the narrow one
         ha, hb = ha.to(torch.complex128), hb.to(torch.complex128)
@@ -233,7 +239,7 @@ def run_complex_host(ha: torch.Tensor, hb: torch.Tensor, cfg: EmuConfig,
     # steady state).  A pageable C also works -- the library then stages the
     # copy-back through pinned slots -- but measured 0.45 s per call (fresh pages
     # touched every call) against 1.1 s instead of 2.4 s for the first call.
-    out = torch.empty((m, n), dtype=odt, pin_memory=True)
+    out = torch.empty((m, n), dtype=odt, pin_memory=not pageable_out)
     diag = torch.zeros(nat.DIAG_LEN, dtype=torch.int64, device=dev)
     nat.call("crtg_gemm_complex_host", prec, mode, m, n, k, ha.data_ptr(), ha.stride(0),
              hb.data_ptr(), hb.stride(0), out.data_ptr(), out.stride(0),
