@@ -1,5 +1,5 @@
 """Wall time of emulate_gemm_complex on plain numpy operands (the CLI's path):
-page-locking in place + staircase streaming + result in pinned host memory.
+staircase streaming through pinned staging rings, result in plain numpy memory.
 
     python tools/numpy_e2e.py [m n k N]
 """
