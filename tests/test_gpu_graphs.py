@@ -33,9 +33,11 @@ def _run(crt, A, B, C, cfg, ws):
 def test_replay_reads_current_operands(crt, mode):
     dev = torch.device("cuda", 0)
     m, k, n, N = 96, 200, 80, 14
-    a0 = orc.gen_matrix(m, k, 0.5, 1, "double")
-    b0 = orc.gen_matrix(k, n, 0.5, 2, "double")
-    a1 = orc.gen_matrix(m, k, 1.0, 3, "double")
+    # the reference generator returns Fortran-ordered arrays; run_complex takes
+    # row-major device operands (the public API makes that copy)
+    a0 = np.ascontiguousarray(orc.gen_matrix(m, k, 0.5, 1, "double"))
+    b0 = np.ascontiguousarray(orc.gen_matrix(k, n, 0.5, 2, "double"))
+    a1 = np.ascontiguousarray(orc.gen_matrix(m, k, 1.0, 3, "double"))
     A = torch.from_numpy(a0).to(dev)
     B = torch.from_numpy(b0).to(dev)
     C = torch.empty((m, n), dtype=torch.complex128, device=dev)
@@ -57,8 +59,8 @@ def test_replay_reads_current_operands(crt, mode):
 def test_replay_reports_domain_errors(crt):
     dev = torch.device("cuda", 0)
     m, k, n = 64, 128, 64
-    A = torch.from_numpy(orc.gen_matrix(m, k, 0.5, 1, "double")).to(dev)
-    B = torch.from_numpy(orc.gen_matrix(k, n, 0.5, 2, "double")).to(dev)
+    A = torch.from_numpy(np.ascontiguousarray(orc.gen_matrix(m, k, 0.5, 1, "double"))).to(dev)
+    B = torch.from_numpy(np.ascontiguousarray(orc.gen_matrix(k, n, 0.5, 2, "double"))).to(dev)
     C = torch.empty((m, n), dtype=torch.complex128, device=dev)
     cfg = crt.EmuConfig(domain="complex", num_moduli=14)
     from paper_2512_08321_b200 import _native as nat
