@@ -128,6 +128,12 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k,
  *  - Per-thread, per-device auxiliary streams: one fork stream for B's chain on
  *    small products and two copy-engine streams of crtg_gemm_complex_host.  They
  *    are joined to the caller's stream with events before the call returns.
+ *  - Per-thread cache of up to 16 instantiated CUDA graphs of small complex
+ *    products (m*n*k <= ~2048^3, one column block), keyed by every argument of
+ *    crtg_gemm_complex (pointers included): the second identical call captures
+ *    its launch sequence, later ones replay it.  Kept until process exit;
+ *    CRTG_GRAPHS=0 disables it.  A replay re-reads the operands, so in-place
+ *    updates between calls are seen (tests/test_gpu_graphs.py).
  *  - crtg_gemm_complex_host with PAGEABLE A / B / C only: a per-thread ring of
  *    3 pinned staging slots, each one streamed piece (~1/16 of an operand; 256
  *    MiB at 16384^2 complex128).  Freed at thread exit or by
