@@ -469,3 +469,32 @@ def test_host_pinned_and_staged_paths_agree(crt):
     pinned = crt.emulate_gemm_complex(ta, tb, cfg)                     # pinned: direct
     dev = crt.emulate_gemm_complex(ta.cuda(), tb.cuda(), cfg)
     assert staged.tobytes() == pinned.numpy().tobytes() == dev.cpu().numpy().tobytes()
+
+
+# ------------------------------------------------------- every modulus count
+@pytest.mark.parametrize("prec", ["double", "single"])
+@pytest.mark.parametrize("N", list(range(1, 21)))
+def test_every_modulus_count_fast(crt, prec, N):
+    """Each N has its own CRT kernel instantiation (k_crt_n<N>, two CTAs per SM
+    above 16) and its own mix of Karatsuba / split moduli: all 20 counts, both
+    precisions, against the oracle at a shape with ragged rows and K (reference
+    emulate.py:193-240)."""
+    a = orc.gen_matrix(37, 300, 1.0, 100 + N, prec)
+    b = orc.gen_matrix(300, 45, 1.0, 200 + N, prec)
+    cfg = crt.EmuConfig(precision=prec, domain="complex", mode="fast", num_moduli=N)
+    got = crt.emulate_gemm_complex(a, b, cfg)
+    want = orc.emulate_complex(a, b, N, "fast", prec)
+    assert got.dtype == want.dtype and got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("N", [2, 5, 9, 11, 18, 19])
+def test_modulus_counts_accurate_large_tiles(crt, N):
+    """Accurate mode and a product large enough for the 256x256-tile GEMM and
+    several residue tiles per CTA, for modulus counts the goldens skip."""
+    a = orc.gen_matrix(300, 1100, 2.0, 300 + N, "double")
+    b = orc.gen_matrix(1100, 260, 2.0, 400 + N, "double")
+    for mode in ("fast", "accurate"):
+        cfg = crt.EmuConfig(precision="double", domain="complex", mode=mode, num_moduli=N)
+        got = crt.emulate_gemm_complex(a, b, cfg)
+        want = orc.emulate_complex(a, b, N, mode, "double")
+        assert got.tobytes() == want.tobytes(), mode
