@@ -34,14 +34,20 @@ __device__ __forceinline__ void int_parts(double q, uint64_t& M, int& s) {
   }
 }
 
+// v = 2^90 + q as three 32-bit words for an integer-valued |q| < 2^90:
+// q = +-M 2^s with M < 2^53 and s <= 37, so M 2^s = hi 2^64 + lo with hi < 2^26;
+// the negative case is the two's-complement difference 2^90 - (hi:lo)
 __device__ __forceinline__ Val3 split_wide(double q) {
   uint64_t M;
   int s;
   int_parts(q, M, s);
-  const unsigned __int128 mag = (unsigned __int128)M << s;
-  const unsigned __int128 base = (unsigned __int128)1 << 90;
-  const unsigned __int128 v = (q < 0.0) ? base - mag : base + mag;
-  return {uint32_t(v), uint32_t(v >> 32), uint32_t(v >> 64)};
+  const uint64_t lo = M << s;
+  const uint32_t hi = s > 11 ? uint32_t(M >> (64 - s)) : 0u;
+  const uint64_t nlo = 0ull - lo;
+  const uint32_t nhi = (1u << 26) - hi - (lo != 0 ? 1u : 0u);
+  const bool neg = q < 0.0;
+  const uint64_t w01 = neg ? nlo : lo;
+  return {uint32_t(w01), uint32_t(w01 >> 32), neg ? nhi : hi + (1u << 26)};
 }
 
 // explicit single-instruction integer ops (keeps ptxas from re-associating the
