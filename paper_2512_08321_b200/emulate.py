@@ -19,6 +19,7 @@ Lower-level GPU parity hooks mirror the reference's stage functions:
 from __future__ import annotations
 
 import ctypes
+import threading
 import os
 from dataclasses import dataclass
 
@@ -86,6 +87,38 @@ def _to_device_matrix(x, name: str, dev, complex_out: bool = True):
 
 def _workspace(nbytes: int, dev) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+
+
+# Small products reuse one workspace + diagnostics buffer per (thread, device,
+# stream): stream order makes reuse safe, it saves two allocations per call and
+# keeps the buffer addresses stable, which is what lets the library replay its
+# captured CUDA graph (api.cu).  Larger workspaces are allocated per call.
+_SMALL_WS_BYTES = 256 << 20
+_tls = threading.local()
+_ws_size_cache: dict = {}
+
+
+def _small_buffers(need: int, dev, stream: int):
+    cache = getattr(_tls, "bufs", None)
+    if cache is None:
+        cache = _tls.bufs = {}
+    key = (dev.index, stream)
+    ent = cache.get(key)
+    if ent is None or ent[0].numel() < need:
+        ent = (torch.empty(max(need, 1 << 20), dtype=torch.uint8, device=dev),
+               torch.empty(nat.DIAG_LEN, dtype=torch.int64, device=dev))
+        cache[key] = ent
+    return ent
+
+
+def _workspace_size(lib, prec, mode, m, n, k, nmod, n_block) -> int:
+    key = (prec, mode, m, n, k, nmod, n_block)
+    v = _ws_size_cache.get(key)
+    if v is None:
+        if len(_ws_size_cache) > 4096:
+            _ws_size_cache.clear()
+        v = _ws_size_cache[key] = int(lib.crtg_workspace_size(prec, mode, m, n, k, nmod, n_block))
+    return v
 
 
 # ----------------------------------------------------------------------------
@@ -271,14 +304,20 @@ def run_complex(at: torch.Tensor, bt: torch.Tensor, cfg: EmuConfig,
         prec |= 16  # CRTG_IN_C64
     mode = nat.FAST if cfg.mode == "fast" else nat.ACCURATE
     lib = nat.load()
-    need = lib.crtg_workspace_size(prec, mode, m, n, k, nmod, cfg.n_block)
+    need = _workspace_size(lib, prec, mode, m, n, k, nmod, cfg.n_block)
+    stream = _stream_ptr(dev)
+    diag = None
     if ws is None or ws.numel() < need:
-        ws = _workspace(need, dev)
+        if need <= _SMALL_WS_BYTES:
+            ws, diag = _small_buffers(need, dev, stream)
+        else:
+            ws = _workspace(need, dev)
     odt = torch.complex64 if cfg.precision == "single" else torch.complex128
     if out is None:
         out = torch.empty((m, n), dtype=odt, device=dev)
     # crtg_gemm_complex zeroes the counters on the stream itself
-    diag = torch.empty(nat.DIAG_LEN, dtype=torch.int64, device=dev)
+    if diag is None:
+        diag = torch.empty(nat.DIAG_LEN, dtype=torch.int64, device=dev)
     mu = torch.empty(m, dtype=torch.int32, device=dev) if return_exponents else None
     nu = torch.empty(n, dtype=torch.int32, device=dev) if return_exponents else None
     nat.call("crtg_gemm_complex", prec, mode, m, n, k, at.data_ptr(), at.stride(0),
@@ -286,7 +325,7 @@ def run_complex(at: torch.Tensor, bt: torch.Tensor, cfg: EmuConfig,
              ctypes.byref(consts), cfg.n_block, ws.data_ptr(), ws.numel(),
              mu.data_ptr() if mu is not None else None,
              nu.data_ptr() if nu is not None else None,
-             diag.data_ptr(), 1 if sync_check else 0, _stream_ptr(dev))
+             diag.data_ptr(), 1 if sync_check else 0, stream)
     if diagnostics is not None:
         d = diag.cpu().tolist()
         for key, idx in (("clamped_mu", nat.DIAG_CLAMPED_MU), ("clamped_nu", nat.DIAG_CLAMPED_NU)):
