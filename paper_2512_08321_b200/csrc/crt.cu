@@ -327,7 +327,7 @@ __device__ __forceinline__ double raw_byte_to_f64(uint32_t w, int q) {
 #endif
 }
 
-template <int N, bool SINGLE>
+template <int N, bool SINGLE, bool REAL>
 __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
     k_crt_n(int64_t m, int64_t n, const int8_t* __restrict__ e_re, const int8_t* __restrict__ e_im,
             int64_t e_plane, int64_t e_ld, const int32_t* __restrict__ mu,
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
   const int64_t j0 = jq * 4;
   for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
     const int8_t* pr = e_re + i * e_ld + j0;
-    const int8_t* pi = e_im + i * e_ld + j0;
+    const int8_t* pi = REAL ? pr : e_im + i * e_ld + j0;  // no imaginary plane (real path)
     const bool aligned =
         ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(pi) | uintptr_t(e_plane)) &
          3) == 0 &&
@@ -349,13 +349,13 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
 #pragma unroll
       for (int l = 0; l < N; ++l) {
         wr[l] = __ldg(reinterpret_cast<const uint32_t*>(pr + l * e_plane));
-        wi[l] = __ldg(reinterpret_cast<const uint32_t*>(pi + l * e_plane));
+        wi[l] = REAL ? 0u : __ldg(reinterpret_cast<const uint32_t*>(pi + l * e_plane));
       }
     } else {
 #pragma unroll
       for (int l = 0; l < N; ++l) {
         wr[l] = load_word(pr + l * e_plane, false, j0, n);
-        wi[l] = load_word(pi + l * e_plane, false, j0, n);
+        wi[l] = REAL ? 0u : load_word(pi + l * e_plane, false, j0, n);
       }
     }
     if (N & 1) wr[N + (N & 1) - 1] = wi[N + (N & 1) - 1] = 0u;
@@ -376,10 +376,12 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
         tr[t][1] = dp2a_hi(hp, r01, tr[t][1]);
         tr[t][2] = dp2a_lo(hp, r23, tr[t][2]);
         tr[t][3] = dp2a_hi(hp, r23, tr[t][3]);
-        ti[t][0] = dp2a_lo(hp, i01, ti[t][0]);
-        ti[t][1] = dp2a_hi(hp, i01, ti[t][1]);
-        ti[t][2] = dp2a_lo(hp, i23, ti[t][2]);
-        ti[t][3] = dp2a_hi(hp, i23, ti[t][3]);
+        if (!REAL) {
+          ti[t][0] = dp2a_lo(hp, i01, ti[t][0]);
+          ti[t][1] = dp2a_hi(hp, i01, ti[t][1]);
+          ti[t][2] = dp2a_lo(hp, i23, ti[t][2]);
+          ti[t][3] = dp2a_hi(hp, i23, ti[t][3]);
+        }
       }
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, raw_byte_to_f64(wr[l + b], q)));
-          s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, raw_byte_to_f64(wi[l + b], q)));
+          if (!REAL) s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, raw_byte_to_f64(wi[l + b], q)));
         }
       }
     }
@@ -402,7 +404,15 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
       const double s1r = __dmul_rn(double(ir), dc.hi_scale);  // exact
       const double s1i = __dmul_rn(double(ii), dc.hi_scale);
       const int ex = -mi - nu[j];
-      if (SINGLE) {
+      if (REAL) {
+        // emulate_gemm_real: inverse_scale of the reduced real value, one cast
+        if (SINGLE)
+          reinterpret_cast<float*>(C)[i * ldc + j] =
+              __double2float_rn(ldexp_rn(reduce_single_fast(__dadd_rn(s1r, s2r[q]), dc), ex));
+        else
+          reinterpret_cast<double*>(C)[i * ldc + j] =
+              ldexp_rn(reduce_double_fast(s1r, s2r[q], dc), ex);
+      } else if (SINGLE) {
         const double cr = reduce_single_fast(__dadd_rn(s1r, s2r[q]), dc);
         const double ci = reduce_single_fast(__dadd_rn(s1i, s2i[q]), dc);
         const float re = __double2float_rn(ldexp_rn(cr, ex));
@@ -438,13 +448,16 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
   const dim3 grid(gx, unsigned(gy));
   const bool limbs = dc.hi_scale != 0.0;
 #if CRTG_CRT_TEMPLATED
-  if (!real && limbs && dc.n >= 1 && dc.n <= CRTG_MAX_MODULI) {
-#define CRTG_CRT_N(NN)                                                                      \
-  case NN:                                                                                  \
-    if (single)                                                                             \
-      k_crt_n<NN, true><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc); \
-    else                                                                                    \
-      k_crt_n<NN, false><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc); \
+  if (limbs && dc.n >= 1 && dc.n <= CRTG_MAX_MODULI) {
+#define CRTG_CRT_NR(NN, S, R) \
+  k_crt_n<NN, S, R><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
+#define CRTG_CRT_N(NN)                                                      \
+  case NN:                                                              \
+    if (real) {                                                         \
+      if (single) CRTG_CRT_NR(NN, true, true); else CRTG_CRT_NR(NN, false, true);   \
+    } else {                                                            \
+      if (single) CRTG_CRT_NR(NN, true, false); else CRTG_CRT_NR(NN, false, false); \
+    }                                                                   \
     break;
     switch (dc.n) {
       CRTG_CRT_N(1) CRTG_CRT_N(2) CRTG_CRT_N(3) CRTG_CRT_N(4) CRTG_CRT_N(5)
@@ -453,6 +466,7 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
       CRTG_CRT_N(16) CRTG_CRT_N(17) CRTG_CRT_N(18) CRTG_CRT_N(19) CRTG_CRT_N(20)
     }
 #undef CRTG_CRT_N
+#undef CRTG_CRT_NR
     return launched(1);
   }
 #endif
