@@ -53,6 +53,14 @@ std::atomic<uint64_t> g_launches{0};
 
 void crtg::note_launches(int n) { g_launches += uint64_t(n); }
 
+bool crtg::pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("CRTG_PDL");
+    return !(v && *v && std::atoi(v) == 0);
+  }();
+  return on;
+}
+
 namespace {
 std::mutex g_prof_mu;
 bool g_prof_on = false;
@@ -148,16 +156,23 @@ cudaStream_t fork_stream() {
   thread_local std::map<int, cudaStream_t> streams;
   auto it = streams.find(dev);
   if (it != streams.end()) return it->second;
+  // highest priority: B's chain (column statistics -> residues of B) is the
+  // longer of the two and the block scheduler should not queue it behind A's
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
   cudaStream_t st = nullptr;
-  cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi);
   streams[dev] = st;
   return st;
 }
 
-bool fork_wanted(int64_t m_pad, int64_t n_pad, int64_t n, int64_t nb) {
+// graphed: the launch sequence is being captured (replays pay nothing for the
+// extra events, so the fork pays below 1024^2 too)
+bool fork_wanted(int64_t m_pad, int64_t n_pad, int64_t n, int64_t nb, bool graphed) {
   static const bool on = env_int("CRTG_FORK", 1) != 0;
   const int64_t out = m_pad * n_pad;
-  return on && nb >= n && out >= int64_t(1024) * 1024 && out <= int64_t(4096) * 4096;
+  return on && nb >= n && (graphed || out >= int64_t(1024) * 1024) &&
+         out <= int64_t(4096) * 4096;
 }
 
 struct Events {
@@ -621,16 +636,19 @@ int run_scaling(const Plan& P, int precision, int mode, const void* A, int64_t l
   PwTree tree{};
   if (mode == CRTG_FAST) {
     if (int e = device_tree(P.k, tree)) return e;
+    // B's column statistics first: on a forked stream they head the longer
+    // chain (statistics -> residues of B), and launched after A's row
+    // statistics their few CTAs found every SM taken (1024^3: started 12 us late)
     {
-      StageTimer timer(CRTG_STAGE_SCALING, s);
-      CRTG_TRY(launch_row_stats(single ? E_C64 : E_C128, true, A, lda, P.m, P.k, tree, dc.p_fast, dc.delta, mu,
-                                rowabs, diag, s),
-               "row stats");
+      StageTimer timer(CRTG_STAGE_SCALING, side);
+      CRTG_TRY(launch_col_fast(single ? E_C64 : E_C128, B, ldb, P.k, P.n, colabs,
+                               at<double>(ws, P.colsq), dc.p_fast, dc.delta, nu, diag, side),
+               "col sumsq");
     }
-    StageTimer timer(CRTG_STAGE_SCALING, side);
-    CRTG_TRY(launch_col_fast(single ? E_C64 : E_C128, B, ldb, P.k, P.n, colabs, at<double>(ws, P.colsq), dc.p_fast,
-                             dc.delta, nu, diag, side),
-             "col sumsq");
+    StageTimer timer(CRTG_STAGE_SCALING, s);
+    CRTG_TRY(launch_row_stats(single ? E_C64 : E_C128, true, A, lda, P.m, P.k, tree, dc.p_fast,
+                              dc.delta, mu, rowabs, diag, s),
+             "row stats");
     return CRTG_OK;
   }
   // accurate mode (scaling.py:229-274)
@@ -739,15 +757,25 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
   return CRTG_OK;
 }
 
+// Read back the device counters of a synchronous call.  The destination is
+// page-locked, one per host thread (a pageable one is a staged copy); only
+// synchronous calls write it, each right before its own stream synchronisation.
 int check_diag(const unsigned long long* diag_dev, cudaStream_t s) {
-  unsigned long long h[CRTG_DIAG_LEN];
-  CRTG_TRY(cudaMemcpyAsync(h, diag_dev, sizeof(h), cudaMemcpyDeviceToHost, s), "diag copy");
+  thread_local unsigned long long* h = [] {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 8 * CRTG_DIAG_LEN, cudaHostAllocPortable) != cudaSuccess) p = nullptr;
+    return static_cast<unsigned long long*>(p);
+  }();
+  unsigned long long hs[CRTG_DIAG_LEN];
+  unsigned long long* hd = h ? h : hs;
+  CRTG_TRY(cudaMemcpyAsync(hd, diag_dev, 8 * CRTG_DIAG_LEN, cudaMemcpyDeviceToHost, s),
+           "diag copy");
   CRTG_TRY(cudaStreamSynchronize(s), "sync");
-  if (h[CRTG_DIAG_NONFINITE_A]) return fail(CRTG_ERR_DOMAIN, "A contains non-finite entries");
-  if (h[CRTG_DIAG_NONFINITE_B]) return fail(CRTG_ERR_DOMAIN, "B contains non-finite entries");
-  if (h[CRTG_DIAG_OVERFLOW_A] || h[CRTG_DIAG_OVERFLOW_B])
+  if (hd[CRTG_DIAG_NONFINITE_A]) return fail(CRTG_ERR_DOMAIN, "A contains non-finite entries");
+  if (hd[CRTG_DIAG_NONFINITE_B]) return fail(CRTG_ERR_DOMAIN, "B contains non-finite entries");
+  if (hd[CRTG_DIAG_OVERFLOW_A] || hd[CRTG_DIAG_OVERFLOW_B])
     return fail(CRTG_ERR_DOMAIN, "scaled magnitudes exceed the quantization budget");
-  if (h[CRTG_DIAG_INT32_OVERFLOW])
+  if (hd[CRTG_DIAG_INT32_OVERFLOW])
     return fail(CRTG_ERR_ARITH, "dot product exceeds the 32-bit accumulator");
   return CRTG_OK;
 }
@@ -818,12 +846,12 @@ namespace {
 int enqueue_complex(const Plan& P, int precision, int mode, const void* A, int64_t lda,
                     const void* B, int64_t ldb, void* C, int64_t ldc, const DevConsts& dc,
                     void* ws, int32_t* mu_out, int32_t* nu_out, unsigned long long* dg,
-                    cudaStream_t s) {
+                    cudaStream_t s, bool graphed = false) {
   CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
   Events E;
   cudaStream_t side = side_stream(s);
   // B's chain (column statistics, residues of block 0) on `aux`
-  const bool forked = side == s && fork_wanted(P.m_pad, P.n_pad, P.n, P.nb);
+  const bool forked = side == s && fork_wanted(P.m_pad, P.n_pad, P.n, P.nb, graphed);
   cudaStream_t aux = forked ? fork_stream() : side;
   cudaEvent_t ev0 = E.get();
   CRTG_TRY(cudaEventRecord(ev0, s), "record");
@@ -958,7 +986,7 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
     cudaStream_t cs = capture_stream();
     CRTG_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "capture");
     const int e = enqueue_complex(P, precision, mode, A, lda, B, ldb, C, ldc, dc, ws, mu_out,
-                                  nu_out, dg, cs);
+                                  nu_out, dg, cs, true);
     cudaGraph_t graph = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
     if (e) {
@@ -966,7 +994,8 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
       return e;
     }
     CRTG_TRY(int(ec), "end capture");
-    const cudaError_t ei = cudaGraphInstantiate(&hit->exec, graph, 0);
+    const cudaError_t ei =
+        cudaGraphInstantiate(&hit->exec, graph, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(graph);
     CRTG_TRY(int(ei), "graph instantiate");
     hit->kernels = int(crtg_launch_count() - before);

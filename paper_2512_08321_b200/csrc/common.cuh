@@ -26,6 +26,53 @@ inline int launched(int n) {
   return int(cudaGetLastError());
 }
 
+// Programmatic dependent launch.  The pipeline kernels (statistics, residues,
+// GEMM, CRT) are launched with launch_k, which lets the next kernel of the
+// stream be scheduled while this one still runs; every such kernel starts with
+// pdl_begin(): griddepcontrol.wait returns once the grids it depends on have
+// completed and their memory is visible (a no-op for a normal launch), so no
+// global load or store of the kernel can overtake its predecessor, and the
+// trigger then lets its own successor launch and park at that wait.  What is
+// saved is the launch latency between dependent kernels (small products run
+// ~6 of them back to back).  CRTG_PDL=0 launches normally.
+bool pdl_enabled();
+
+template <typename... K, typename... A>
+inline cudaError_t launch_k(void (*kern)(K...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t s, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  unsigned na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  // carry the stream's priority into the launch (and so into a captured graph
+  // node: the small-product graphs run B's longer chain on a high-priority fork)
+  int prio = 0;
+  if (cudaStreamGetPriority(s, &prio) == cudaSuccess && prio != 0) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na++].val.priority = prio;
+  }
+  cfg.attrs = na ? attr : nullptr;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<A&&>(args)...);
+}
+
+#ifndef CRTG_PDL_TRIGGER
+#define CRTG_PDL_TRIGGER 0
+#endif
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#if CRTG_PDL_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
 constexpr int kBlockRows = 128;
 constexpr int kBlockK = 128;                    // bytes
 constexpr int kBlockBytes = kBlockRows * kBlockK;  // 16 KiB

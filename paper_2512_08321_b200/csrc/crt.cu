@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(256, CRTG_CRT_MINB) k_crt(int64_t m, int64_t n
                                              const int32_t* __restrict__ nu,
                                              const __grid_constant__ DevConsts dc, void* C,
                                              int64_t ldc) {
+  pdl_begin();
   // 2-D: x = quads of 4 columns, y strides over rows (no division per element)
   const int64_t nq = (n + 3) >> 2;
   const int64_t jq = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
             int64_t e_plane, int64_t e_ld, const int32_t* __restrict__ mu,
             const int32_t* __restrict__ nu, const __grid_constant__ DevConsts dc, void* C,
             int64_t ldc) {
+  pdl_begin();
   const int64_t nq = (n + 3) >> 2;
   const int64_t jq = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (jq >= nq) return;
@@ -450,7 +452,7 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
 #if CRTG_CRT_TEMPLATED
   if (limbs && dc.n >= 1 && dc.n <= CRTG_MAX_MODULI) {
 #define CRTG_CRT_NR(NN, S, R) \
-  k_crt_n<NN, S, R><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
+  launch_k(k_crt_n<NN, S, R>, grid, 256, 0, s, m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
 #define CRTG_CRT_N(NN)                                                      \
   case NN:                                                              \
     if (real) {                                                         \
@@ -471,7 +473,7 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
   }
 #endif
 #define CRTG_CRT(S, L, R) \
-  k_crt<S, L, R><<<grid, 256, 0, s>>>(m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
+  launch_k(k_crt<S, L, R>, grid, 256, 0, s, m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
   if (real) {
     if (single) { if (limbs) CRTG_CRT(true, true, true); else CRTG_CRT(true, false, true); }
     else { if (limbs) CRTG_CRT(false, true, true); else CRTG_CRT(false, false, true); }

@@ -164,6 +164,119 @@ __device__ __forceinline__ void split_phase(const GemmArgs& g, uint32_t taddr, i
   }
 }
 
+// The same two epilogues with the per-column state in SHARED memory (word i of
+// this thread at st[i * stride]) so that the chunk loop is NOT unrolled: one
+// phase is then ~250 instructions that stay in the instruction cache, where the
+// fully unrolled register-state form is ~1000 straight-line instructions per
+// phase and variant (10.5K in all) and short-K tiles, whose epilogue is not
+// hidden behind long K loops, stalled on instruction fetch (ncu at 1024^3:
+// `no_instruction` the top stall reason).  Used by the 128 x 256 kernel.
+template <int NCH, bool POW2>
+__device__ __forceinline__ void karatsuba_phase_sm(const GemmArgs& g, uint32_t taddr, int s, int l,
+                                                   int row, bool row_ok, int col_base,
+                                                   const ModConst& mc, uint32_t* st, int stride) {
+  int8_t* dst_base = nullptr;
+  if (s == 1) dst_base = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  if (s == 2) dst_base = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  const uint32_t bias = uint32_t(mc.bias), bias_h = mc.bias_h, h = mc.h;
+#pragma unroll 1
+  for (int c = 0; c < NCH; ++c) {
+    uint32_t cv[32];
+    tmem_ld32(taddr + c * 32, cv);
+    uint32_t* sc = st + c * 8 * stride;
+    uint32_t sw[8];
+    if (s != 0) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sw[w] = sc[w * stride];
+    }
+    tmem_wait_ld();
+    uint32_t out[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint32_t a[4], b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t x = cv[4 * w + j];
+        if (s == 0) {
+          a[j] = ep_red<POW2>(x + bias, mc);
+        } else {
+          const uint32_t prev = __byte_perm(sw[w], 0, 0x4440 + j);
+          if (s == 1) {
+            a[j] = ep_red<POW2>(prev - x + bias_h, mc) - h;
+            b[j] = ep_red<POW2>(prev + x + bias, mc);
+          } else {
+            a[j] = ep_red<POW2>(x - prev + bias_h, mc) - h;
+          }
+        }
+      }
+      if (s == 0) {
+        sc[w * stride] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
+      } else {
+        out[w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
+        if (s == 1) sc[w * stride] = ep_pack_bytes(b[0], b[1], b[2], b[3]);
+      }
+    }
+    if (s != 0 && row_ok) {
+      uint4* d4 = reinterpret_cast<uint4*>(dst_base + c * 32);
+      d4[0] = make_uint4(out[0], out[1], out[2], out[3]);
+      d4[1] = make_uint4(out[4], out[5], out[6], out[7]);
+    }
+  }
+}
+
+template <int NCH>
+__device__ __forceinline__ void split_phase_sm(const GemmArgs& g, uint32_t taddr, int s, int l,
+                                               int row, bool row_ok, int col_base,
+                                               const ModConst& mc, uint32_t* st, int stride) {
+  int8_t* dre = g.e_re + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  int8_t* dim = g.e_im + (int64_t)l * g.e_plane + (int64_t)row * g.e_ld + col_base;
+  const uint32_t bias = uint32_t(mc.bias), h = mc.h, p = uint32_t(mc.p);
+  const uint32_t inv2 = mc.inv2, inv2j = mc.inv2j;
+#pragma unroll 1
+  for (int c = 0; c < NCH; ++c) {
+    uint32_t cv[32];
+    tmem_ld32(taddr + c * 32, cv);
+    uint32_t* sc = st + c * 8 * stride;
+    uint32_t sw[8];
+    if (s != 0) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sw[w] = sc[w * stride];
+    }
+    tmem_wait_ld();
+    uint32_t ore[8], oim[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      uint32_t a[4], b[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t x = cv[4 * w + j];
+        if (s == 0) {
+          a[j] = ep_red<false>(x + bias, mc);
+        } else {
+          const uint32_t xm = __byte_perm(sw[w], 0, 0x4440 + j);
+          const uint32_t ym = ep_red<false>(x + bias, mc);
+          a[j] = ep_red<false>((xm + ym) * inv2 + h, mc) - h;
+          b[j] = ep_red<false>((xm + p - ym) * inv2j + h, mc) - h;
+        }
+      }
+      if (s == 0) {
+        sc[w * stride] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
+      } else {
+        ore[w] = ep_pack_bytes(a[0], a[1], a[2], a[3]);
+        oim[w] = ep_pack_bytes(b[0], b[1], b[2], b[3]);
+      }
+    }
+    if (s != 0 && row_ok) {
+      uint4* r4 = reinterpret_cast<uint4*>(dre + c * 32);
+      r4[0] = make_uint4(ore[0], ore[1], ore[2], ore[3]);
+      r4[1] = make_uint4(ore[4], ore[5], ore[6], ore[7]);
+      uint4* i4 = reinterpret_cast<uint4*>(dim + c * 32);
+      i4[0] = make_uint4(oim[0], oim[1], oim[2], oim[3]);
+      i4[1] = make_uint4(oim[4], oim[5], oim[6], oim[7]);
+    }
+  }
+}
+
 // segments (K loops) of one output tile: the Karatsuba / split count of its
 // modulus, or the launch's fixed count (RAW, REAL)
 template <int MODE>
@@ -246,6 +359,19 @@ __device__ __forceinline__ void epilogue_phase(const GemmArgs& g, uint32_t taddr
     karatsuba_phase<NCH, true>(g, taddr, s, l, row, row_ok, col_base, mc, st);
   else
     karatsuba_phase<NCH, false>(g, taddr, s, l, row, row_ok, col_base, mc, st);
+}
+
+template <int NCH>
+__device__ __forceinline__ void karatsuba_epilogue_sm(const GemmArgs& g, uint32_t taddr, int s,
+                                                      int l, int row, bool row_ok, int col_base,
+                                                      const ModConst& mc, uint32_t* st,
+                                                      int stride) {
+  if (mc.nphase == 2)
+    split_phase_sm<NCH>(g, taddr, s, l, row, row_ok, col_base, mc, st, stride);
+  else if (mc.is_pow2)
+    karatsuba_phase_sm<NCH, true>(g, taddr, s, l, row, row_ok, col_base, mc, st, stride);
+  else
+    karatsuba_phase_sm<NCH, false>(g, taddr, s, l, row, row_ok, col_base, mc, st, stride);
 }
 
 }  // namespace crtg

@@ -42,6 +42,12 @@ constexpr int kTmemCols = 512;
 constexpr int kEpiThreads = 256;            // 8 epilogue warps
 constexpr int kThreads = 128 + kEpiThreads;  // producer, MMA, TMEM alloc, spare + epilogue
 constexpr int kGroupM = 16;  // rasterisation: 16 row tiles share each column sweep
+// Karatsuba / split epilogue state in shared memory (gemm_epilogue.cuh
+// karatsuba_phase_sm): 32 words per epilogue thread behind the operand ring
+#ifndef CRTG_EPI_SMEM
+#define CRTG_EPI_SMEM 1
+#endif
+constexpr uint32_t kStateBytes = CRTG_EPI_SMEM ? kEpiThreads * 32 * 4 : 0;
 
 struct Seg {
   int a_plane, b_plane, buf, accumulate;
@@ -71,6 +77,14 @@ __device__ __forceinline__ void decode_tile(int t, const GemmArgs& g, int& l, in
   tn = in / gm + g.nt0;
 }
 
+// unit of a persistent CTA in round r: boustrophedon over the rounds (round r
+// covers units [r G, (r + 1) G); odd rounds in reverse CTA order), so a CTA
+// that got an early unit of a round gets a late one of the next
+__device__ __forceinline__ int unit_of(int r) {
+  const int G = int(gridDim.x), b = int(blockIdx.x);
+  return r * G + ((r & 1) ? G - 1 - b : b);
+}
+
 }  // namespace
 
 template <int MODE>
@@ -81,6 +95,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
   __shared__ __align__(8) uint64_t tfull_bar[2];
   __shared__ __align__(8) uint64_t tempty_bar[2];
   __shared__ uint32_t tmem_slot;
+  __shared__ int8_t lord[CRTG_MAX_MODULI];  // processing order of the moduli
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -97,21 +112,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
       mbar_init(smem_u32(&tempty_bar[b]), kEpiThreads);
     }
     fence_mbar_init();
+    // Karatsuba: the three-product moduli first, the two-product (split) ones
+    // last, so that with the snake order below the CTAs that run one unit more
+    // than others run cheap ones (1024^3 N=14: 448 units on 148 CTAs, longest
+    // CTA 12 -> 10 products)
+    int o = 0;
+    for (int pass = 0; pass < 2; ++pass)
+      for (int l = 0; l < g.nl; ++l)
+        if (MODE != EPI_KARATSUBA ? pass == 0 : (g.mc[l].nphase == 2) == (pass == 1))
+          lord[o++] = int8_t(l);
   }
   if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(&tmem_slot));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  pdl_begin();  // barriers and TMEM are set up; operands are read from here on
 
   const int total = g.nl * g.mt * g.nt;
 
   if (warp == 0 && lane == 0) {
     // ---------------- producer ----------------
     uint32_t stage = 0, phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int r = 0; r * int(gridDim.x) < total; ++r) {
+      const int t = unit_of(r);
+      if (t >= total) continue;
       int l, tm, tn;
       decode_tile(t, g, l, tm, tn);
+      l = lord[l];
       const int nseg = MODE == EPI_BOUND ? 2 : tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const Seg sg = seg_of<MODE>(s);
@@ -135,9 +163,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
     const uint32_t idesc = idesc_i8(128, 256);
     const uint32_t idesc_u = idesc & ~((1u << 7) | (1u << 10));
     uint32_t stage = 0, phase = 0, gslot = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int r = 0; r * int(gridDim.x) < total; ++r) {
+      const int t = unit_of(r);
+      if (t >= total) continue;
       int l, tm, tn;
       decode_tile(t, g, l, tm, tn);
+      l = lord[l];
       const int nseg = MODE == EPI_BOUND ? 2 : tile_segments<MODE>(g, l);
       if (MODE == EPI_BOUND) {
         const uint32_t par = ((gslot >> 1) & 1) ^ 1;
@@ -188,11 +219,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
     const uint32_t lane_addr = tmem + (uint32_t(32 * q) << 16) + uint32_t(128 * half);
     uint32_t gslot = 0;
     uint32_t st[32];  // packed per-column state across the three Karatsuba phases
+    uint32_t* sst = reinterpret_cast<uint32_t*>(smem_raw + (smem_base - smem_u32(smem_raw)) +
+                                                kStages * kStageBytes) +
+                    (threadIdx.x - 128);
 #pragma unroll
     for (int i = 0; i < 32; ++i) st[i] = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int r = 0; r * int(gridDim.x) < total; ++r) {
+      const int t = unit_of(r);
+      if (t >= total) continue;
       int l, tm, tn;
       decode_tile(t, g, l, tm, tn);
+      l = lord[l];
       const int row = tm * 128 + 32 * q + lane;
       const bool row_ok = row < g.m;
       const int col_base = tn * 256 + 128 * half;
@@ -232,7 +269,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
         const uint32_t buf = gslot & 1;
         mbar_wait_warp(smem_u32(&tfull_bar[buf]), (gslot >> 1) & 1);
         tc_fence_after();
-        epilogue_phase<MODE, 4>(g, lane_addr + buf * 256, s, l, row, row_ok, col_base, mc, st);
+        if (MODE == EPI_KARATSUBA && CRTG_EPI_SMEM)
+          karatsuba_epilogue_sm<4>(g, lane_addr + buf * 256, s, l, row, row_ok, col_base, mc, sst,
+                                   kEpiThreads);
+        else
+          epilogue_phase<MODE, 4>(g, lane_addr + buf * 256, s, l, row, row_ok, col_base, mc, st);
         tc_fence_before();
         mbar_arrive(smem_u32(&tempty_bar[buf]));
         ++gslot;
@@ -334,6 +375,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
+  pdl_begin();
   const int total = g.nl * (g.mt >> 1) * g.nt;
 
   if (warp == 0 && lane == 0) {
@@ -433,14 +475,14 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
   }
 }
 
-size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + 1024; }
+size_t gemm_smem_bytes() { return size_t(kStages) * kStageBytes + kStateBytes + 1024; }
 
 template <int MODE>
 int launch_wide_mode(const GemmArgs& g, int grid, size_t smem, cudaStream_t stream) {
   const cudaError_t err = cudaFuncSetAttribute(
       k_gemm_w<MODE, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   if (err != cudaSuccess) return int(err);
-  k_gemm_w<MODE, 8><<<grid, 128 + 32 * 8, smem, stream>>>(g);
+  launch_k(k_gemm_w<MODE, 8>, grid, 128 + 32 * 8, smem, stream, g);
   return launched(1);
 }
 
@@ -466,25 +508,25 @@ int launch_gemm(int mode, const GemmArgs& g, int num_sms, cudaStream_t stream) {
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_KARATSUBA>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (err != cudaSuccess) return int(err);
-      k_gemm_i8<EPI_KARATSUBA><<<grid, kThreads, smem, stream>>>(g);
+      launch_k(k_gemm_i8<EPI_KARATSUBA>, grid, kThreads, smem, stream, g);
       break;
     case EPI_RAW:
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_RAW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem));
       if (err != cudaSuccess) return int(err);
-      k_gemm_i8<EPI_RAW><<<grid, kThreads, smem, stream>>>(g);
+      launch_k(k_gemm_i8<EPI_RAW>, grid, kThreads, smem, stream, g);
       break;
     case EPI_REAL:
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_REAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(smem));
       if (err != cudaSuccess) return int(err);
-      k_gemm_i8<EPI_REAL><<<grid, kThreads, smem, stream>>>(g);
+      launch_k(k_gemm_i8<EPI_REAL>, grid, kThreads, smem, stream, g);
       break;
     default:
       err = cudaFuncSetAttribute(k_gemm_i8<EPI_BOUND>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (err != cudaSuccess) return int(err);
-      k_gemm_i8<EPI_BOUND><<<grid, kThreads, smem, stream>>>(g);
+      launch_k(k_gemm_i8<EPI_BOUND>, grid, kThreads, smem, stream, g);
       break;
   }
   return launched(1);

@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
                                                   int8_t* __restrict__ out, int64_t plane_bytes,
                                                   int64_t rb_count,
                                                   unsigned long long* __restrict__ overflow) {
+  pdl_begin();
   __shared__ __align__(16) uint8_t stage[3][kTileRows * 128];
   const int kb = blockIdx.x;
   const int r0 = blockIdx.y * kTileRows;
@@ -216,19 +217,12 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
                                              int8_t* __restrict__ out, int64_t plane_bytes,
                                              int64_t goff, int soff, int cq, int cs,
                                              uint8_t (*stage)[kResRows * 128]) {
-  // unrolled over the modulus index: each modulus's constants become immediate
-  // constant-bank operands instead of per-iteration LDC loads
-  // small operands: blockIdx.y of gridDim.y CTAs share a tile, each taking the
-  // moduli l == blockIdx.y (mod gridDim.y)
+  // large launches: unrolled over the modulus index, so each modulus's
+  // constants become immediate constant-bank operands instead of per-iteration
+  // LDC loads.  Small launches (MSPLIT): blockIdx.y of gridDim.y CTAs share a
+  // tile, each taking the moduli l == blockIdx.y (mod gridDim.y)
   int it = 0;  // moduli processed by this CTA (smem stage buffer parity)
-#if CRTG_RES_UNROLL
-#pragma unroll
-  for (int l = 0; l < CRTG_MAX_MODULI; ++l) {
-    if (l >= dc.n) break;
-#else
-  for (int l = 0; l < dc.n; ++l) {
-#endif
-    if (MSPLIT && l % int(gridDim.y) != int(blockIdx.y)) continue;
+  auto one = [&](int l) {
     const ResConst c = rcs[l];
     uint32_t w[3][2];
     residue_words<FORM, SYM>(vr, vi, c, w);
@@ -256,6 +250,24 @@ __device__ __forceinline__ void store_moduli(const Val3 (&vr)[8], const Val3 (&v
         reinterpret_cast<uint4*>(base + 2 * plane_bytes)[cs] =
             reinterpret_cast<const uint4*>(sb[2])[cs];
     }
+  };
+  if constexpr (MSPLIT) {
+    // small operands (and the moduli-split launches): a rolled loop, constants
+    // by uniform loads -- the unrolled form is ~20K instructions and latency-bound
+    // small launches stalled on instruction fetch (ncu at 1024^2: no_instruction
+    // the top stall); large launches keep the unrolled loop (rolled: A 5.4 -> 5.8 ms)
+#pragma unroll 1
+    for (int l = int(blockIdx.y); l < dc.n; l += int(gridDim.y)) one(l);
+  } else {
+#if CRTG_RES_UNROLL
+#pragma unroll
+    for (int l = 0; l < CRTG_MAX_MODULI; ++l) {
+      if (l >= dc.n) break;
+      one(l);
+    }
+#else
+    for (int l = 0; l < dc.n; ++l) one(l);
+#endif
   }
   if (OPERAND != 0) __syncthreads();  // the next tile reuses the buffers
 }
@@ -278,6 +290,7 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
                                                   int64_t rb_count,
                                                   unsigned long long* __restrict__ overflow,
                                                   int n_kb, int n_rt, int row_base) {
+  pdl_begin();
   // B of the complex pipeline (TIN): the tile's 128 K x 16 columns of B are
   // transposed on the way IN (coalesced 256-byte rows into a swizzled shared
   // tile, then each thread reads its column's 8 consecutive K), so its planes
@@ -493,16 +506,24 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
     const int msplit = (max_ctas > 0 || tiles >= 2 * nsm_r)
                            ? 1
                            : int(std::min<int64_t>(dc.n, (2 * nsm_r + tiles - 1) / tiles));
+    // small launches take the rolled-loop instantiation (MS): up to 2048^2
+    // operands (<= 4096 tiles; 1024^3 N=14 136 vs 151 us per product, 2048^3
+    // -3%, 4096^3 and up neutral to slower; CRTG_RES_ROLLED_TILES overrides)
+    static const int64_t rolled_tiles = [] {
+      const char* v = std::getenv("CRTG_RES_ROLLED_TILES");
+      return v && *v ? int64_t(std::atoll(v)) : int64_t(4096);
+    }();
+    const bool ms = msplit > 1 || (max_ctas == 0 && tiles <= rolled_tiles);
     const dim3 grid(grid1, unsigned(std::max(1, msplit)));
     // symmetric residues for the real path and the parity hook (dc.sym), the
     // 128-offset representative in the complex pipeline
 #define CRTG_RES_LAUNCH(R, S, M)                                                              \
-  k_residues<T, OP, R, S, M><<<grid, 256, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),      \
+  launch_k(k_residues<T, OP, R, S, M>, grid, 256, 0, s, static_cast<const T*>(X), ldx, int(rows),      \
                                                   int(kdim), col0, exps, dc, out, plane_bytes,   \
                                                   rb_count, overflow, n_kb, n_rt, int(row_base))
     if (REAL || dc.sym) {
-      if (msplit > 1) CRTG_RES_LAUNCH(REAL, true, true); else CRTG_RES_LAUNCH(REAL, true, false);
-    } else if (msplit > 1) {
+      if (ms) CRTG_RES_LAUNCH(REAL, true, true); else CRTG_RES_LAUNCH(REAL, true, false);
+    } else if (ms) {
       CRTG_RES_LAUNCH(false, false, true);
     } else {
       CRTG_RES_LAUNCH(false, false, false);
@@ -511,7 +532,7 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
   } else {
   // cover every padded row of the plane so the GEMM reads zeros there
   dim3 grid(unsigned((kdim + 127) / 128), unsigned(rb_count * 128 / kTileRows));
-  k_pack<T, OP, KIND, REAL><<<grid, kThreads, 0, s>>>(static_cast<const T*>(X), ldx, int(rows),
+  launch_k(k_pack<T, OP, KIND, REAL>, grid, kThreads, 0, s, static_cast<const T*>(X), ldx, int(rows),
                                                 int(kdim), col0, exps, dc, out, plane_bytes,
                                                 rb_count, overflow);
   }

@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(256) k_row_stats(const T* __restrict__ A, int6
                                                    int fast, int32_t* __restrict__ mu,
                                                    double* __restrict__ rowabs,
                                                    unsigned long long* __restrict__ diag) {
+  pdl_begin();
   extern __shared__ double vals[];  // [2][nleaves + nnodes]
   __shared__ double red[8];
   const int64_t i = blockIdx.x;
@@ -270,6 +271,7 @@ __global__ void __launch_bounds__(128) k_col_absmax(const T* __restrict__ B, int
                                                     int n, int rows_per_chunk,
                                                     double* __restrict__ colabs,
                                                     unsigned long long* __restrict__ diag) {
+  pdl_begin();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int h0 = blockIdx.y * rows_per_chunk;
   const int h1 = min(k, h0 + rows_per_chunk);
@@ -297,6 +299,7 @@ template <typename T, bool REAL>
 __global__ void __launch_bounds__(128) k_col_sumsq(const T* __restrict__ B, int64_t ldb, int k,
                                                    int n, const double* __restrict__ colabs,
                                                    double* __restrict__ colsq) {
+  pdl_begin();
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int j = int(t >> 1), part = int(t & 1);
   if (j >= n) return;
@@ -359,6 +362,7 @@ __global__ void __launch_bounds__(128) k_col_stats(const T* __restrict__ B, int6
                                                    int32_t* __restrict__ nu,
                                                    double* __restrict__ colabs,
                                                    unsigned long long* __restrict__ diag) {
+  pdl_begin();
   constexpr int kParts = REAL ? 1 : 2;
   constexpr int kCols = 32 / kParts;            // columns per CTA
   constexpr int kSeg = 32 * int(sizeof(T));     // bytes per row segment
@@ -463,6 +467,7 @@ template <typename T, bool REAL>
 __global__ void k_col_fallback(const T* __restrict__ B, int64_t ldb, int k, int n, float p_fast,
                                float delta, const double* __restrict__ colabs,
                                int32_t* __restrict__ nu, unsigned long long* __restrict__ diag) {
+  pdl_begin();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n || nu[j] != kNuPending) return;
   const double mx = colabs[j];
@@ -482,6 +487,7 @@ __global__ void k_col_fallback(const T* __restrict__ B, int64_t ldb, int k, int 
 __global__ void k_col_finalize(int n, const double* __restrict__ colabs,
                                const double* __restrict__ colsq, float p_fast, float delta,
                                int32_t* __restrict__ nu, unsigned long long* __restrict__ diag) {
+  pdl_begin();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const double mx = colabs[j];
@@ -491,6 +497,7 @@ __global__ void k_col_finalize(int n, const double* __restrict__ colabs,
 }
 
 __global__ void k_bar(const double* __restrict__ absval, int64_t count, int32_t* __restrict__ bar) {
+  pdl_begin();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
   const double v = absval[i];
@@ -502,6 +509,7 @@ __global__ void k_accurate_exps(const int32_t* __restrict__ maxb, const double* 
                                 const int32_t* __restrict__ bar, int64_t count, float p_accu,
                                 float delta, int32_t* __restrict__ out,
                                 unsigned long long* __restrict__ counter) {
+  pdl_begin();
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
   double mv = double(maxb[i]);
@@ -540,7 +548,7 @@ int launch_row_stats(int elem, bool fast, const void* A, int64_t lda, int64_t m,
   CRTG_ELEM_DISPATCH(elem, {
     cudaFuncSetAttribute(k_row_stats<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem > 48 * 1024 ? smem : 48 * 1024));
-    k_row_stats<T, R><<<unsigned(m), 256, smem, s>>>(static_cast<const T*>(A), lda, int(k), tree,
+    launch_k(k_row_stats<T, R>, unsigned(m), 256, smem, s, static_cast<const T*>(A), lda, int(k), tree,
                                                      p_fast, delta, fast, mu, rowabs, diag);
   })
   return launched(1);
@@ -557,7 +565,7 @@ int launch_col_absmax(int elem, const void* B, int64_t ldb, int64_t k, int64_t n
       int(std::min<int64_t>(1024, std::max<int64_t>(16, round_up((k + chunks - 1) / chunks, 16))));
   dim3 grid(unsigned(xb), unsigned((k + rows_per_chunk - 1) / rows_per_chunk));
   CRTG_ELEM_DISPATCH(elem, {
-    k_col_absmax<T, R><<<grid, 128, 0, s>>>(static_cast<const T*>(B), ldb, int(k), int(n),
+    launch_k(k_col_absmax<T, R>, grid, 128, 0, s, static_cast<const T*>(B), ldb, int(k), int(n),
                                             rows_per_chunk, colabs, diag);
   })
   return launched(1);
@@ -576,10 +584,10 @@ int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n, 
     CRTG_TRY_L(launch_col_absmax(elem, B, ldb, k, n, colabs, diag, s));
     const unsigned grid = unsigned((2 * n + 127) / 128);
     CRTG_ELEM_DISPATCH(elem, {
-      k_col_sumsq<T, R><<<grid, 128, 0, s>>>(static_cast<const T*>(B), ldb, int(k), int(n), colabs,
+      launch_k(k_col_sumsq<T, R>, grid, 128, 0, s, static_cast<const T*>(B), ldb, int(k), int(n), colabs,
                                              colsq);
     })
-    k_col_finalize<<<unsigned((n + 127) / 128), 128, 0, s>>>(int(n), colabs, colsq, p_fast, delta,
+    launch_k(k_col_finalize, unsigned((n + 127) / 128), 128, 0, s, int(n), colabs, colsq, p_fast, delta,
                                                               nu, diag);
     return launched(2);
   }
@@ -588,9 +596,9 @@ int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n, 
     constexpr int cols = 32 / parts;
     const size_t smem = size_t(kColS) * kColR * 32 * sizeof(T);
     cudaFuncSetAttribute(k_col_stats<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    k_col_stats<T, R><<<unsigned((n + cols - 1) / cols), 128, smem, s>>>(
+    launch_k(k_col_stats<T, R>, unsigned((n + cols - 1) / cols), 128, smem, s,
         static_cast<const T*>(B), ldb, int(k), int(n), p_fast, delta, nu, colabs, diag);
-    k_col_fallback<T, R><<<unsigned((n + 127) / 128), 128, 0, s>>>(
+    launch_k(k_col_fallback<T, R>, unsigned((n + 127) / 128), 128, 0, s,
         static_cast<const T*>(B), ldb, int(k), int(n), p_fast, delta, colabs, nu, diag);
   })
   return launched(2);
@@ -598,7 +606,7 @@ int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n, 
 
 int launch_bar(const double* absval, int64_t count, int32_t* bar, cudaStream_t s) {
   if (count <= 0) return 0;
-  k_bar<<<unsigned((count + 255) / 256), 256, 0, s>>>(absval, count, bar);
+  launch_k(k_bar, unsigned((count + 255) / 256), 256, 0, s, absval, count, bar);
   return launched(1);
 }
 
@@ -606,7 +614,7 @@ int launch_accurate_exps(const int32_t* maxb, const double* absval, const int32_
                          int64_t count, float p_accu, float delta, int32_t* out,
                          unsigned long long* clamp_counter, cudaStream_t s) {
   if (count <= 0) return 0;
-  k_accurate_exps<<<unsigned((count + 255) / 256), 256, 0, s>>>(maxb, absval, bar, count, p_accu,
+  launch_k(k_accurate_exps, unsigned((count + 255) / 256), 256, 0, s, maxb, absval, bar, count, p_accu,
                                                                  delta, out, clamp_counter);
   return launched(1);
 }
