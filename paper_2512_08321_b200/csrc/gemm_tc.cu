@@ -322,6 +322,10 @@ constexpr int kWGroupM = 8;  // 256-row tiles per column sweep
 #ifndef CRTG_MOD_INNER
 #define CRTG_MOD_INNER 0
 #endif
+// boustrophedon unit order with the three-product moduli first (as k_gemm_i8)
+#ifndef CRTG_W_SNAKE
+#define CRTG_W_SNAKE 1
+#endif
 
 __device__ __forceinline__ void decode_tile_w(int t, const GemmArgs& g, int& l, int& tm2,
                                               int& tn) {
@@ -356,6 +360,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
   __shared__ __align__(8) uint64_t empty_bar[kWStages];
   __shared__ __align__(8) uint64_t tfull_bar, tempty_bar;
   __shared__ uint32_t tmem_slot;
+  __shared__ int8_t lord[CRTG_MAX_MODULI];  // processing order of the moduli (CRTG_W_SNAKE)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -369,6 +374,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
     mbar_init(smem_u32(&tfull_bar), 1);
     mbar_init(smem_u32(&tempty_bar), 32 * EW);
     fence_mbar_init();
+    int o = 0;  // three-product moduli first (see k_gemm_i8)
+    for (int pass = 0; pass < 2; ++pass)
+      for (int l = 0; l < g.nl; ++l)
+        if (!CRTG_W_SNAKE || MODE != EPI_KARATSUBA ? pass == 0
+                                                    : (g.mc[l].nphase == 2) == (pass == 1))
+          lord[o++] = int8_t(l);
   }
   if (warp == 2) tmem_alloc<kTmemCols>(smem_u32(&tmem_slot));
   tc_fence_before();
@@ -381,9 +392,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
   if (warp == 0 && lane == 0) {
     // ---------------- producer: A rows [256 tm2, +256) and B rows [256 tn, +256) ----------------
     uint32_t stage = 0, phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int r = 0; r * int(gridDim.x) < total; ++r) {
+      const int t = CRTG_W_SNAKE ? unit_of(r) : r * int(gridDim.x) + int(blockIdx.x);
+      if (t >= total) continue;
       int l, tm2, tn;
       decode_tile_w(t, g, l, tm2, tn);
+      l = lord[l];
       const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         const int8_t* a = g.a + (int64_t)(l * g.planes_per_l + s) * g.a_plane;
@@ -403,9 +417,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
     // ---------------- MMA issuer: two M=128 MMAs per K step share the B tile ----------------
     const uint32_t idesc = idesc_i8(128, 256);
     uint32_t stage = 0, phase = 0, gslot = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int r = 0; r * int(gridDim.x) < total; ++r) {
+      const int t = CRTG_W_SNAKE ? unit_of(r) : r * int(gridDim.x) + int(blockIdx.x);
+      if (t >= total) continue;
       int l, tm2, tn;
       decode_tile_w(t, g, l, tm2, tn);
+      l = lord[l];
       const int nseg = tile_segments<MODE>(g, l);
       for (int s = 0; s < nseg; ++s) {
         mbar_wait(smem_u32(&tempty_bar), (gslot & 1) ^ 1);  // epilogue drained both halves
@@ -448,9 +465,12 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
     uint32_t st[NCH * 8];
 #pragma unroll
     for (int i = 0; i < NCH * 8; ++i) st[i] = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int r = 0; r * int(gridDim.x) < total; ++r) {
+      const int t = CRTG_W_SNAKE ? unit_of(r) : r * int(gridDim.x) + int(blockIdx.x);
+      if (t >= total) continue;
       int l, tm2, tn;
       decode_tile_w(t, g, l, tm2, tn);
+      l = lord[l];
       const int row = tm2 * 256 + 128 * half + 32 * q + lane;
       const bool row_ok = row < g.m;
       const int col_base = tn * 256 + 32 * NCH * colh;
