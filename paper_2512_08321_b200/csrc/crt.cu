@@ -9,6 +9,8 @@
 //   inverse_scale    emulate.py:135-144   ldexp(C', -mu_i - nu_j), one cast
 //   assembly         emulate.py:239-240   (re + 1j*im): real = re + (0*im - 0),
 //                                          imag = 0 + (0 + im), in the output type
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -328,61 +330,73 @@ __device__ __forceinline__ double raw_byte_to_f64(uint32_t w, int q) {
 #endif
 }
 
-template <int N, bool SINGLE, bool REAL>
-__global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
+// Q: output columns per thread (4; 2 for small grids, where 4 left a third of
+// a wave as the tail: 1024^2 was 2.3 waves)
+template <int N, bool SINGLE, bool REAL, int Q = 4>
+__global__ void __launch_bounds__(256, N > 16 ? 2 : (Q == 2 ? 4 : CRTG_CRT_MINB))
     k_crt_n(int64_t m, int64_t n, const int8_t* __restrict__ e_re, const int8_t* __restrict__ e_im,
             int64_t e_plane, int64_t e_ld, const int32_t* __restrict__ mu,
             const int32_t* __restrict__ nu, const __grid_constant__ DevConsts dc, void* C,
             int64_t ldc) {
+  static_assert(Q == 4 || Q == 2, "4 or 2 columns per thread");
   pdl_begin();
-  const int64_t nq = (n + 3) >> 2;
+  const int64_t nq = (n + Q - 1) / Q;
   const int64_t jq = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (jq >= nq) return;
-  const int64_t j0 = jq * 4;
+  const int64_t j0 = jq * Q;
   for (int64_t i = blockIdx.y; i < m; i += gridDim.y) {
     const int8_t* pr = e_re + i * e_ld + j0;
     const int8_t* pi = REAL ? pr : e_im + i * e_ld + j0;  // no imaginary plane (real path)
     const bool aligned =
         ((reinterpret_cast<uintptr_t>(pr) | reinterpret_cast<uintptr_t>(pi) | uintptr_t(e_plane)) &
-         3) == 0 &&
-        j0 + 4 <= n;
+         (Q - 1)) == 0 &&
+        j0 + Q <= n;
     uint32_t wr[N + (N & 1)], wi[N + (N & 1)];
     if (aligned) {
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        wr[l] = __ldg(reinterpret_cast<const uint32_t*>(pr + l * e_plane));
-        wi[l] = REAL ? 0u : __ldg(reinterpret_cast<const uint32_t*>(pi + l * e_plane));
+        if (Q == 4) {
+          wr[l] = __ldg(reinterpret_cast<const uint32_t*>(pr + l * e_plane));
+          wi[l] = REAL ? 0u : __ldg(reinterpret_cast<const uint32_t*>(pi + l * e_plane));
+        } else {
+          wr[l] = __ldg(reinterpret_cast<const uint16_t*>(pr + l * e_plane));
+          wi[l] = REAL ? 0u : __ldg(reinterpret_cast<const uint16_t*>(pi + l * e_plane));
+        }
       }
     } else {
 #pragma unroll
       for (int l = 0; l < N; ++l) {
-        wr[l] = load_word(pr + l * e_plane, false, j0, n);
-        wi[l] = REAL ? 0u : load_word(pi + l * e_plane, false, j0, n);
+        wr[l] = load_word(pr + l * e_plane, false, j0, Q == 4 ? n : min(n, j0 + Q));
+        wi[l] = REAL ? 0u : load_word(pi + l * e_plane, false, j0, Q == 4 ? n : min(n, j0 + Q));
       }
     }
     if (N & 1) wr[N + (N & 1) - 1] = wi[N + (N & 1) - 1] = 0u;
     // per modulus pair: S1 as exact integer limb sums (two moduli per dp2a), then
     // S2 -- the rounded f64 sequence of crt.py:239-240, l ascending, no FMA
-    int32_t tr[3][4] = {}, ti[3][4] = {};
-    double s2r[4] = {0, 0, 0, 0}, s2i[4] = {0, 0, 0, 0};
+    int32_t tr[3][Q] = {}, ti[3][Q] = {};
+    double s2r[Q] = {}, s2i[Q] = {};
 #pragma unroll
     for (int l = 0; l < N; l += 2) {
       const uint32_t r01 = __byte_perm(wr[l], wr[l + 1], 0x5140);
-      const uint32_t r23 = __byte_perm(wr[l], wr[l + 1], 0x7362);
       const uint32_t i01 = __byte_perm(wi[l], wi[l + 1], 0x5140);
-      const uint32_t i23 = __byte_perm(wi[l], wi[l + 1], 0x7362);
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         const uint32_t hp = dc.limb_pair[l >> 1][t];
         tr[t][0] = dp2a_lo(hp, r01, tr[t][0]);
         tr[t][1] = dp2a_hi(hp, r01, tr[t][1]);
-        tr[t][2] = dp2a_lo(hp, r23, tr[t][2]);
-        tr[t][3] = dp2a_hi(hp, r23, tr[t][3]);
         if (!REAL) {
           ti[t][0] = dp2a_lo(hp, i01, ti[t][0]);
           ti[t][1] = dp2a_hi(hp, i01, ti[t][1]);
-          ti[t][2] = dp2a_lo(hp, i23, ti[t][2]);
-          ti[t][3] = dp2a_hi(hp, i23, ti[t][3]);
+        }
+        if (Q == 4) {
+          const uint32_t r23 = __byte_perm(wr[l], wr[l + 1], 0x7362);
+          const uint32_t i23 = __byte_perm(wi[l], wi[l + 1], 0x7362);
+          tr[t][Q - 2] = dp2a_lo(hp, r23, tr[t][Q - 2]);
+          tr[t][Q - 1] = dp2a_hi(hp, r23, tr[t][Q - 1]);
+          if (!REAL) {
+            ti[t][Q - 2] = dp2a_lo(hp, i23, ti[t][Q - 2]);
+            ti[t][Q - 1] = dp2a_hi(hp, i23, ti[t][Q - 1]);
+          }
         }
       }
 #pragma unroll
@@ -390,7 +404,7 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
         if (l + b >= N) break;
         const double cl = dc.coeff_lo[l + b];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < Q; ++q) {
           s2r[q] = __dadd_rn(s2r[q], __dmul_rn(cl, raw_byte_to_f64(wr[l + b], q)));
           if (!REAL) s2i[q] = __dadd_rn(s2i[q], __dmul_rn(cl, raw_byte_to_f64(wi[l + b], q)));
         }
@@ -398,7 +412,7 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : CRTG_CRT_MINB)
     }
     const int32_t mi = mu[i];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < Q; ++q) {
       const int64_t j = j0 + q;
       if (j >= n) break;
       const int64_t ir = (int64_t(tr[2][q]) << 32) + (int64_t(tr[1][q]) << 16) + tr[0][q];
@@ -441,24 +455,34 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
                const int8_t* e_im, int64_t e_plane, int64_t e_ld, const int32_t* mu,
                const int32_t* nu, const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s,
                int max_ctas) {
-  const int64_t nq = (n + 3) / 4;
+  const bool limbs = dc.hi_scale != 0.0;
+  // few threads (small outputs): two columns per thread, so the grid is ~5 waves
+  // instead of ~2.3 with a one-third tail (1024^2); complex pipeline only
+  static const int64_t q2_max = [] {
+    const char* v = std::getenv("CRTG_CRT_Q2_THREADS");
+    return v && *v ? int64_t(std::atoll(v)) : int64_t(148) * 768 * 4;
+  }();
+  const bool q2 = CRTG_CRT_TEMPLATED && limbs && !real && max_ctas == 0 &&
+                  m * ((n + 3) / 4) <= q2_max;
+  const int64_t nq = q2 ? (n + 1) / 2 : (n + 3) / 4;
   if (m <= 0 || nq <= 0) return 0;
   const unsigned gx = unsigned((nq + 255) / 256);
   int64_t gy = std::min<int64_t>(m, 65535);
   // max_ctas (side-stream runs beside the GEMM): cap the total CTA count
   if (max_ctas > 0) gy = std::max<int64_t>(1, std::min<int64_t>(gy, max_ctas / int64_t(gx)));
   const dim3 grid(gx, unsigned(gy));
-  const bool limbs = dc.hi_scale != 0.0;
 #if CRTG_CRT_TEMPLATED
   if (limbs && dc.n >= 1 && dc.n <= CRTG_MAX_MODULI) {
-#define CRTG_CRT_NR(NN, S, R) \
-  launch_k(k_crt_n<NN, S, R>, grid, 256, 0, s, m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
+#define CRTG_CRT_NR(NN, S, R, Q) \
+  launch_k(k_crt_n<NN, S, R, Q>, grid, 256, 0, s, m, n, e_re, e_im, e_plane, e_ld, mu, nu, dc, C, ldc)
 #define CRTG_CRT_N(NN)                                                      \
   case NN:                                                              \
     if (real) {                                                         \
-      if (single) CRTG_CRT_NR(NN, true, true); else CRTG_CRT_NR(NN, false, true);   \
+      if (single) CRTG_CRT_NR(NN, true, true, 4); else CRTG_CRT_NR(NN, false, true, 4);   \
+    } else if (q2) {                                                    \
+      if (single) CRTG_CRT_NR(NN, true, false, 2); else CRTG_CRT_NR(NN, false, false, 2); \
     } else {                                                            \
-      if (single) CRTG_CRT_NR(NN, true, false); else CRTG_CRT_NR(NN, false, false); \
+      if (single) CRTG_CRT_NR(NN, true, false, 4); else CRTG_CRT_NR(NN, false, false, 4); \
     }                                                                   \
     break;
     switch (dc.n) {
