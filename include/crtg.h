@@ -125,9 +125,12 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k,
  *  - Immutable per-(device, k) pairwise-sum tree of the fast-mode row
  *    statistics (numpy's summation order), uploaded once with cudaMalloc and
  *    kept for the process lifetime (16 * (k / 64 + 4) bytes: 16 KB at k = 65536).
- *  - Per-thread, per-device auxiliary streams: one fork stream for B's chain on
- *    small products and two copy-engine streams of crtg_gemm_complex_host.  They
- *    are joined to the caller's stream with events before the call returns.
+ *  - Per-thread, per-device auxiliary streams: one fork stream (highest
+ *    priority) for B's chain on small products and two copy-engine streams of
+ *    crtg_gemm_complex_host.  They are joined to the caller's stream with
+ *    events before the call returns.
+ *  - Per-thread 64-byte page-locked buffer that synchronous calls read their
+ *    device counters back into (sync_check = 1), right before synchronising.
  *  - Per-thread cache of up to 16 instantiated CUDA graphs of small complex
  *    products (m*n*k <= ~2048^3, one column block), keyed by every argument of
  *    crtg_gemm_complex (pointers included): the second identical call captures
