@@ -330,34 +330,47 @@ ResConst make_res(int p, uint32_t off) {
 // split = true: moduli with a square root of -1 use the 2-product form (the
 // production pipeline); false keeps the reference's [re, im, re+im] planes for
 // every modulus (the crtg_residues parity hook unpacks them)
-DevConsts make_dev_uncached(const crtg_consts& K, bool split);
+DevConsts make_dev_uncached(const crtg_consts& K, bool split, bool uns);
+
+// The complex pipeline's residues as UNSIGNED bytes t in [0, p) with u8 x u8
+// tcgen05 products (instead of the signed t - 128): same e-planes, but the
+// tensor cores draw less power on them (ZGEMM 16384^3: K3 -1.7%, DESIGN.md
+// section 3).  The epilogue's single biased reduction needs every product below
+// 2^30, i.e. (p - 1)^2 k_pad < 2^30: k_pad <= 16384; longer K keeps the signed
+// encoding (|product| <= 128^2 k <= 2^30 up to k = 65536).  CRTG_U8=0 disables.
+bool unsigned_residues(int64_t k) {
+  static const bool on = env_int("CRTG_U8", 1) != 0;
+  return on && round_up(k, 128) <= 16384;
+}
 
 // the constant tables take ~0.1 ms of host integer arithmetic to build (modular
 // inverses, powers, square roots of -1); small calls would pay that every time,
 // so the last few (constants, split) pairs are cached per thread
-DevConsts make_dev(const crtg_consts& K, bool split = true) {
+DevConsts make_dev(const crtg_consts& K, bool split = true, bool uns = false) {
   struct Entry {
     crtg_consts key;
-    bool split;
+    bool split, uns;
     DevConsts val;
   };
   static thread_local std::vector<Entry> cache;
   for (const auto& e : cache)
-    if (e.split == split && std::memcmp(&e.key, &K, sizeof(K)) == 0) return e.val;
+    if (e.split == split && e.uns == uns && std::memcmp(&e.key, &K, sizeof(K)) == 0) return e.val;
   if (cache.size() >= 8) cache.erase(cache.begin());
-  cache.push_back({K, split, make_dev_uncached(K, split)});
+  cache.push_back({K, split, uns, make_dev_uncached(K, split, uns)});
   return cache.back().val;
 }
 
-DevConsts make_dev_uncached(const crtg_consts& K, bool split) {
+DevConsts make_dev_uncached(const crtg_consts& K, bool split, bool uns) {
   DevConsts d{};
   d.n = K.num_moduli;
+  d.uns = uns ? 1 : 0;
   for (int l = 0; l < d.n; ++l) {
     const int p = K.moduli[l];
     d.mc[l] = make_mod(p);
     const ModConst& mc = d.mc[l];
     d.rc[l] = make_res(p, uint32_t(p / 2));
-    d.rx[l] = make_res(p, 128u);
+    d.rx[l] = make_res(p, uns ? 0u : 128u);
+    d.rx[l].xor_mask = uns ? 0u : 0x80808080u;
     if (split && split_enabled()) {
       make_split(d.mc[l], d.rc[l], p);
       make_split(d.mc[l], d.rx[l], p);
@@ -734,6 +747,7 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
     g.e_ld = P.nb_pad;
     g.e_plane = m * P.nb_pad;
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
+    g.uns = dc.uns;
     {
       StageTimer timer(CRTG_STAGE_GEMM, s);
       CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
@@ -942,7 +956,7 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
                                 : at<unsigned long long>(ws, P.diag);
-  const DevConsts dc = make_dev(*K);
+  const DevConsts dc = make_dev(*K, true, unsigned_residues(k));
   if (!graph_wanted(P, s)) {
     if (int e = enqueue_complex(P, precision, mode, A, lda, B, ldb, C, ldc, dc, ws, mu_out, nu_out,
                                 dg, s))
@@ -1244,7 +1258,7 @@ extern "C" int crtg_gemm_complex_exps(int precision, int64_t m, int64_t n, int64
   unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
                                 : at<unsigned long long>(ws, P.diag);
   CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
-  const DevConsts dc = make_dev(*K);
+  const DevConsts dc = make_dev(*K, true, unsigned_residues(k));
   Events E;
   cudaStream_t side = side_stream(s);
   cudaEvent_t ev0 = E.get();
@@ -1502,7 +1516,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
   char* dC = dB + r(size_t(k) * n * esz);  // m x n, row-major (ld n)
   unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
                                 : at<unsigned long long>(ws, P.diag);
-  const DevConsts dc = make_dev(*K);
+  const DevConsts dc = make_dev(*K, true, unsigned_residues(k));
   Events E;
   cudaEvent_t ev0 = E.get();
   CRTG_TRY(cudaMemsetAsync(dg, 0, 8 * CRTG_DIAG_LEN, s), "memset");
@@ -1756,6 +1770,7 @@ extern "C" int crtg_gemm_complex_host(int precision, int mode, int64_t m, int64_
     g.e_ld = P.n_pad;
     g.e_plane = m * P.n_pad;
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
+    g.uns = dc.uns;
     {
       StageTimer timer(CRTG_STAGE_GEMM, s);
       CRTG_TRY(run_gemm(EPI_KARATSUBA, g, s), "karatsuba gemm");
@@ -2010,6 +2025,7 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
     g.e_plane = m * P.nb_pad;
     g.overflow = dg + CRTG_DIAG_INT32_OVERFLOW;
     for (int l = 0; l < N; ++l) g.mc[l] = dc.mc[l];
+    g.uns = dc.uns;
     {
       StageTimer timer(CRTG_STAGE_GEMM, s);
       CRTG_TRY(run_gemm(EPI_REAL, g, s), "real gemm");

@@ -139,6 +139,7 @@ struct ResConst {
   // sum_i limb_i(im) (j c_i mod p) + kU, congruent to re + j im + off (V: p - j)
   uint32_t uw0123, uw45, vw0123, vw45;  // byte tables of j c_i, (p - j) c_i mod p
   uint32_t ku31, ku63, kuw, kv31, kv63, kvw;  // (off - (1 + j) 2^31|63|90) mod p, V likewise
+  uint32_t xor_mask;  // stored byte = t ^ mask: 0x80 per byte (off = 128, signed t - 128) or 0
 };
 
 struct DevConsts {
@@ -147,6 +148,7 @@ struct DevConsts {
   ResConst rc[CRTG_MAX_MODULI];  // symmetric representative
   ResConst rx[CRTG_MAX_MODULI];  // 128-offset representative (complex pipeline)
   int32_t sym;                   // 1: the complex pipeline stores symmetric residues too
+  int32_t uns;                   // 1: rx holds unsigned residues t in [0, p) (off = 0; u8 GEMM)
   double coeff_hi[CRTG_MAX_MODULI];
   double coeff_lo[CRTG_MAX_MODULI];
   double p_hi, p_lo;

@@ -31,6 +31,7 @@ struct GemmArgs {
   int32_t* col_max;  // BOUND: [nt*256]
   unsigned long long* overflow;  // REAL: int32 accumulator overflow (kernel.py:33-34)
   int group_m;       // raster: row tiles per column sweep (0 -> 16)
+  int uns;           // KARATSUBA: operands are unsigned residues in [0, p) (u8 x u8)
   ModConst mc[CRTG_MAX_MODULI];
 };
 

@@ -156,7 +156,8 @@ __device__ __forceinline__ uint32_t res_uv(const Val3& vr, const Val3& vi, const
   return mod_small(u, c);
 }
 
-// 4 values t_i in [0,p) -> packed int8 (t_i - off)
+// 4 values t_i in [0,p) -> packed bytes: SYM, the symmetric t_i - off; else
+// the bytes of t_i xor `off` (a per-byte mask: 0x80 -> signed t - 128, 0 -> t)
 template <bool SYM>
 __device__ __forceinline__ uint32_t pack_t(uint32_t a, uint32_t b, uint32_t c, uint32_t d,
                                            uint32_t off) {
@@ -165,8 +166,9 @@ __device__ __forceinline__ uint32_t pack_t(uint32_t a, uint32_t b, uint32_t c, u
     const uint32_t hi = __byte_perm(c - off, d - off, 0x0040);
     return __byte_perm(lo, hi, 0x5410);
   }
-  // off = 128: (t - 128) mod 256 == t ^ 0x80 for t < 256
-  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410) ^ 0x80808080u;
+  // off = 128: (t - 128) mod 256 == t ^ 0x80 for t < 256 (signed bytes); off = 0:
+  // t itself (unsigned bytes, mask 0)
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410) ^ off;
 }
 
 // planes of one modulus: [re, im, re+im] (Karatsuba), or [U, V] = [re + j im,
@@ -185,8 +187,8 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
         tu[j] = res_uv<FORM>(re[4 * half + j], im[4 * half + j], c, 0);
         tv[j] = res_uv<FORM>(re[4 * half + j], im[4 * half + j], c, 1);
       }
-      w[0][half] = pack_t<SYM>(tu[0], tu[1], tu[2], tu[3], c.off);
-      w[1][half] = pack_t<SYM>(tv[0], tv[1], tv[2], tv[3], c.off);
+      w[0][half] = pack_t<SYM>(tu[0], tu[1], tu[2], tu[3], SYM ? c.off : c.xor_mask);
+      w[1][half] = pack_t<SYM>(tv[0], tv[1], tv[2], tv[3], SYM ? c.off : c.xor_mask);
     } else {
       uint32_t tr[4], ti[4], ts[4];
 #pragma unroll
@@ -203,9 +205,9 @@ __device__ __forceinline__ void residue_words(const Val3 (&re)[8], const Val3 (&
         const uint32_t y = min(x, x + c.neg_p);
         ts[j] = min(y, y + c.neg_p);
       }
-      w[0][half] = pack_t<SYM>(tr[0], tr[1], tr[2], tr[3], c.off);
-      w[1][half] = pack_t<SYM>(ti[0], ti[1], ti[2], ti[3], c.off);
-      w[2][half] = pack_t<SYM>(ts[0], ts[1], ts[2], ts[3], c.off);
+      w[0][half] = pack_t<SYM>(tr[0], tr[1], tr[2], tr[3], SYM ? c.off : c.xor_mask);
+      w[1][half] = pack_t<SYM>(ti[0], ti[1], ti[2], ti[3], SYM ? c.off : c.xor_mask);
+      w[2][half] = pack_t<SYM>(ts[0], ts[1], ts[2], ts[3], SYM ? c.off : c.xor_mask);
     }
   }
 }
