@@ -1896,7 +1896,7 @@ extern "C" int crtg_gemm_real(int precision, int mode, int64_t m, int64_t n, int
   const bool single = (precision & CRTG_SINGLE) != 0;
   unsigned long long* dg = diag ? reinterpret_cast<unsigned long long*>(diag)
                                 : at<unsigned long long>(ws, P.diag);
-  const DevConsts dc = make_dev(*K);
+  const DevConsts dc = make_dev(*K, true, unsigned_residues(k));
   int32_t* mu = at<int32_t>(ws, P.mu);
   int32_t* nu = at<int32_t>(ws, P.nu);
   double* rowabs = at<double>(ws, P.rowabs);

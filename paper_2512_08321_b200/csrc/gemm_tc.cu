@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_i8(const __grid_constant__
     // [0, p) (g.uns) and the accurate-mode X = (R+I)(R'+I') bytes of the bound product
     const uint32_t idesc_s = idesc_i8(128, 256);
     const uint32_t idesc_u = idesc_s & ~((1u << 7) | (1u << 10));
-    const uint32_t idesc = MODE == EPI_KARATSUBA && g.uns ? idesc_u : idesc_s;
+    const uint32_t idesc = (MODE == EPI_KARATSUBA || MODE == EPI_REAL) && g.uns ? idesc_u : idesc_s;
     uint32_t stage = 0, phase = 0, gslot = 0;
     for (int r = 0; r * int(gridDim.x) < total; ++r) {
       const int t = unit_of(r);
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(128 + 32 * EW, 1) k_gemm_w(const __grid_consta
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer: two M=128 MMAs per K step share the B tile ----------------
     // Karatsuba / split on unsigned residue bytes in [0, p): bits 7 / 10 clear
-    const uint32_t idesc = MODE == EPI_KARATSUBA && g.uns
+    const uint32_t idesc = (MODE == EPI_KARATSUBA || MODE == EPI_REAL) && g.uns
                                ? (idesc_i8(128, 256) & ~((1u << 7) | (1u << 10)))
                                : idesc_i8(128, 256);
     uint32_t stage = 0, phase = 0, gslot = 0;

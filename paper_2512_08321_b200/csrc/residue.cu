@@ -423,7 +423,9 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
     // one plane per modulus (emulate_gemm_real: no imaginary part / Karatsuba sum)
     for (int l = 0; l < dc.n; ++l) {
       if (MS && l % int(gridDim.y) != int(blockIdx.y)) continue;
-      const ResConst c = dc.rc[l];
+      // symmetric residues, or (dc.uns, k <= 16384) t in [0, p): rx has off = 0,
+      // so pack_t<true> stores the bytes of t
+      const ResConst c = dc.uns ? dc.rx[l] : dc.rc[l];
       uint32_t w0, w1;
       if (huge) {
         w0 = pack_real<3>(vr, 0, c);
