@@ -1110,8 +1110,9 @@ __global__ void k_mod_sum(const int8_t* __restrict__ x, const int8_t* __restrict
   out[i] = int8_t(to_sym(r, mc));
 }
 
-// split-modulus planes x + c y (U: c = j, V: c = p - j) in the pipeline's
-// 128-offset representative ((v + 128) mod p) - 128 in [-128, p - 129]
+// split-modulus planes x + c y (U: c = j, V: c = p - j) in the 128-offset
+// representative ((v + 128) mod p) - 128 in [-128, p - 129] (signed operands:
+// crtg_complex_gemm_mod's GEMM runs with g.uns = 0)
 __global__ void k_mod_lin(const int8_t* __restrict__ x, const int8_t* __restrict__ y, int c,
                           int64_t count, ModConst mc, int8_t* __restrict__ out) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;

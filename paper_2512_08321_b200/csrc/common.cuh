@@ -115,7 +115,8 @@ struct ModConst {
 };
 
 // Residue-kernel constants for one modulus and one stored representative
-// (off = floor(p/2): the symmetric residue t - off; off = 128: t ^ 0x80).
+// (off = floor(p/2): the symmetric residue t - off; off = 128: t ^ 0x80; off = 0:
+// t itself, the unsigned pipeline encoding).
 // A value a' is read as 16-bit limbs of v = a' + 2^31 (two limbs), a' + 2^63
 // (four) or 2^90 + a' (six); u = sum_i limb_i * (2^(16 i) mod p) + k is congruent to a' + off and
 // below 2^27, so one magic reduction gives t = (a' + off) mod p.
@@ -146,7 +147,7 @@ struct DevConsts {
   int32_t n;
   ModConst mc[CRTG_MAX_MODULI];
   ResConst rc[CRTG_MAX_MODULI];  // symmetric representative
-  ResConst rx[CRTG_MAX_MODULI];  // 128-offset representative (complex pipeline)
+  ResConst rx[CRTG_MAX_MODULI];  // pipeline representative: unsigned t (uns) or 128-offset
   int32_t sym;                   // 1: the complex pipeline stores symmetric residues too
   int32_t uns;                   // 1: rx holds unsigned residues t in [0, p) (off = 0; u8 GEMM)
   double coeff_hi[CRTG_MAX_MODULI];

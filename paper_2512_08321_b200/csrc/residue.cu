@@ -118,12 +118,15 @@ __global__ void __launch_bounds__(kThreads) k_pack(const T* __restrict__ X, int6
 // is a coalesced 16-byte write of a contiguous 2 KiB run of the packed plane.
 //
 // Stored representative.  SYM = true writes the reference's symmetric residue
-// (crt.py:136-151; the crtg_residues parity hook and the real path, whose
-// int32 overflow check depends on it).  SYM = false (the complex pipeline)
-// writes (a' + 128 mod p) - 128 in [-128, p - 129]: congruent to a', so every
-// modular product and e-plane is unchanged, |value| <= 128 keeps the Karatsuba
-// and split sums within the epilogue's 2^30 bias for k <= 2^16, and the byte is
-// t ^ 0x80 -- one LOP per four values instead of four subtractions.
+// (crt.py:136-151; the crtg_residues parity hook, and the real path for
+// k > 16384, whose int32 overflow check depends on it).  SYM = false (the
+// complex pipeline) writes, for k <= 16384 (DevConsts::uns), the unsigned
+// residue t = a' mod p in [0, p) -- the GEMM then runs u8 x u8 products, which
+// draw less power, and (p - 1)^2 k < 2^30 keeps every sum inside the
+// epilogue's single biased reduction -- and for longer K the signed
+// (a' + 128 mod p) - 128 in [-128, p - 129] (byte t ^ 0x80, |value| <= 128
+// keeps k 128^2 <= 2^30 up to k = 2^16).  Both are congruent to a', so every
+// modular product and e-plane is unchanged.
 // ---------------------------------------------------------------------------
 constexpr int kResRows = 16;
 #ifndef CRTG_RES_MINB
@@ -302,7 +305,8 @@ __global__ void __launch_bounds__(256, CRTG_RES_MINB) k_residues(const T* __rest
   constexpr int kStageBytes = TIN ? 128 * 16 * 2 * int(sizeof(T)) : 6 * kResRows * 128;
   __shared__ __align__(16) uint8_t smem_buf[kStageBytes];
   uint8_t (*stage)[kResRows * 128] = reinterpret_cast<uint8_t (*)[kResRows * 128]>(smem_buf);
-  // representative of the stored residues: the symmetric (rc) or the 128-offset (rx) tables
+  // representative of the stored residues: the symmetric (rc) or the pipeline's
+  // unsigned / 128-offset (rx) tables
   const ResConst* rcs = SYM ? dc.rc : dc.rx;
   // grid-stride over (K block, 16-row tile): a full grid when launched alone, one
   // CTA per SM when it runs beside the persistent GEMM (side stream)
@@ -520,7 +524,7 @@ void launch_one(const void* X, int64_t ldx, int64_t rows, int64_t kdim, int64_t 
     const bool ms = msplit > 1 || (max_ctas == 0 && tiles <= rolled_tiles);
     const dim3 grid(grid1, unsigned(std::max(1, msplit)));
     // symmetric residues for the real path and the parity hook (dc.sym), the
-    // 128-offset representative in the complex pipeline
+    // unsigned (k <= 16384) or 128-offset representative in the complex pipeline
 #define CRTG_RES_LAUNCH(R, S, M)                                                              \
   launch_k(k_residues<T, OP, R, S, M>, grid, 256, 0, s, static_cast<const T*>(X), ldx, int(rows),      \
                                                   int(kdim), col0, exps, dc, out, plane_bytes,   \
