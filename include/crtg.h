@@ -129,8 +129,10 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k,
  *    priority) for B's chain on small products and two copy-engine streams of
  *    crtg_gemm_complex_host.  They are joined to the caller's stream with
  *    events before the call returns.
- *  - Per-thread 64-byte page-locked buffer that synchronous calls read their
- *    device counters back into (sync_check = 1), right before synchronising.
+ *  - Per-thread 64-byte page-locked buffers that synchronous calls read their
+ *    device counters back into (sync_check = 1), right before synchronising:
+ *    one filled by a copy, and one device-mapped that the captured graphs of
+ *    synchronous small products write from their last kernel.
  *  - Per-thread cache of up to 16 instantiated CUDA graphs of small complex
  *    products (m*n*k <= ~2048^3, one column block), keyed by every argument of
  *    crtg_gemm_complex (pointers included): the second identical call captures

@@ -774,6 +774,8 @@ int run_pipeline(const Plan& P, int precision, const void* A, int64_t lda, const
 // Read back the device counters of a synchronous call.  The destination is
 // page-locked, one per host thread (a pageable one is a staged copy); only
 // synchronous calls write it, each right before its own stream synchronisation.
+int eval_diag(const volatile unsigned long long* hd);
+
 int check_diag(const unsigned long long* diag_dev, cudaStream_t s) {
   thread_local unsigned long long* h = [] {
     void* p = nullptr;
@@ -785,6 +787,42 @@ int check_diag(const unsigned long long* diag_dev, cudaStream_t s) {
   CRTG_TRY(cudaMemcpyAsync(hd, diag_dev, 8 * CRTG_DIAG_LEN, cudaMemcpyDeviceToHost, s),
            "diag copy");
   CRTG_TRY(cudaStreamSynchronize(s), "sync");
+  return eval_diag(hd);
+}
+
+// Synchronous small products replay a graph that ends with k_diag_out, which
+// stores the counters straight into this page-locked, device-mapped buffer of
+// the calling thread (no separate copy after the graph).  Only synchronous
+// calls write it, each followed by its own stream synchronisation.
+struct MappedDiag {
+  unsigned long long* h = nullptr;
+  unsigned long long* d = nullptr;
+};
+MappedDiag mapped_diag() {
+  thread_local MappedDiag m = [] {
+    MappedDiag r;
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 8 * CRTG_DIAG_LEN, cudaHostAllocPortable | cudaHostAllocMapped) ==
+        cudaSuccess) {
+      void* dp = nullptr;
+      if (cudaHostGetDevicePointer(&dp, p, 0) == cudaSuccess) {
+        r.h = static_cast<unsigned long long*>(p);
+        r.d = static_cast<unsigned long long*>(dp);
+      } else {
+        cudaFreeHost(p);
+      }
+    }
+    return r;
+  }();
+  return m;
+}
+
+__global__ void k_diag_out(const unsigned long long* __restrict__ dg,
+                           unsigned long long* __restrict__ out) {
+  if (threadIdx.x < CRTG_DIAG_LEN) out[threadIdx.x] = dg[threadIdx.x];
+}
+
+int eval_diag(const volatile unsigned long long* hd) {
   if (hd[CRTG_DIAG_NONFINITE_A]) return fail(CRTG_ERR_DOMAIN, "A contains non-finite entries");
   if (hd[CRTG_DIAG_NONFINITE_B]) return fail(CRTG_ERR_DOMAIN, "B contains non-finite entries");
   if (hd[CRTG_DIAG_OVERFLOW_A] || hd[CRTG_DIAG_OVERFLOW_B])
@@ -901,6 +939,7 @@ struct GraphKey {
   size_t ws_bytes;
   int32_t *mu_out, *nu_out;
   unsigned long long* dg;
+  int sync;  // synchronous: the graph ends with k_diag_out into mapped_diag()
   crtg_consts K;
   bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
 };
@@ -972,6 +1011,8 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
   key.n_block = n_block;
   key.A = A; key.B = B; key.C = C; key.ws = ws; key.ws_bytes = ws_bytes;
   key.mu_out = mu_out; key.nu_out = nu_out; key.dg = dg;
+  const MappedDiag md = sync_check ? mapped_diag() : MappedDiag{};
+  key.sync = md.d ? 1 : 0;
   std::memcpy(&key.K, K, sizeof(crtg_consts));
   static thread_local std::vector<GraphEntry> cache;
   static thread_local uint64_t tick = 0;
@@ -999,8 +1040,12 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
     const uint64_t before = crtg_launch_count();
     cudaStream_t cs = capture_stream();
     CRTG_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "capture");
-    const int e = enqueue_complex(P, precision, mode, A, lda, B, ldb, C, ldc, dc, ws, mu_out,
-                                  nu_out, dg, cs, true);
+    int e = enqueue_complex(P, precision, mode, A, lda, B, ldb, C, ldc, dc, ws, mu_out, nu_out,
+                            dg, cs, true);
+    if (!e && key.sync) {
+      k_diag_out<<<1, 32, 0, cs>>>(dg, md.d);
+      e = cuda_check(launched(1), "diag out");
+    }
     cudaGraph_t graph = nullptr;
     const cudaError_t ec = cudaStreamEndCapture(cs, &graph);
     if (e) {
@@ -1018,6 +1063,10 @@ int crtg_gemm_complex(int precision, int mode, int64_t m, int64_t n, int64_t k, 
   if (hit->exec) {
     CRTG_TRY(cudaGraphLaunch(hit->exec, s), "graph launch");
     note_launches(hit->kernels);
+    if (key.sync) {
+      CRTG_TRY(cudaStreamSynchronize(s), "sync");
+      return eval_diag(md.h);
+    }
   } else if (int e = enqueue_complex(P, precision, mode, A, lda, B, ldb, C, ldc, dc, ws, mu_out,
                                      nu_out, dg, s)) {
     return e;
