@@ -108,6 +108,8 @@ def load(path: str | None = None) -> ctypes.CDLL:
     CRTG_LIB=/path/to/libcrtg.so selects another build of the same library
     (A/B timing of kernel variants, tools/ab.py)."""
     global _lib
+    if _lib is not None and path is None:  # hot path: no lock once loaded
+        return _lib
     with _lock:
         if _lib is not None:
             return _lib

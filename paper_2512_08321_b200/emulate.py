@@ -51,15 +51,28 @@ class ScalingVectors:
 # ----------------------------------------------------------------------------
 # device plumbing
 # ----------------------------------------------------------------------------
+_cuda_seen = False
+
+
 def _device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise nat.NativeError("no CUDA device: the B200 emulation has no CPU path")
+    global _cuda_seen
+    if not _cuda_seen:
+        if not torch.cuda.is_available():
+            raise nat.NativeError("no CUDA device: the B200 emulation has no CPU path")
+        _cuda_seen = True
     dev = torch.device("cuda", torch.cuda.current_device())
     nat.check_device(dev.index)
     return dev
 
 
+# the raw handle of the current stream without building a torch Stream object
+# (a few microseconds per call on small products)
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_ptr(dev) -> int:
+    if _raw_stream is not None:
+        return _raw_stream(dev.index)
     return torch.cuda.current_stream(dev).cuda_stream
 
 
@@ -75,7 +88,9 @@ def _to_device_matrix(x, name: str, dev, complex_out: bool = True):
             t = t.to(torch.complex128)
         if complex_out and t.dtype not in (torch.complex64, torch.complex128):
             t = t.to(torch.complex128)
-        return t.to(dev).contiguous(), True
+        if not (t.is_cuda and t.get_device() == dev.index):
+            t = t.to(dev)
+        return (t if t.is_contiguous() else t.contiguous()), True
     arr = np.asarray(x)
     if arr.ndim != 2:
         raise DimensionError(f"{name} must be 2-D")
