@@ -26,6 +26,13 @@
 #ifndef CRTG_CRT_TEMPLATED
 #define CRTG_CRT_TEMPLATED 1
 #endif
+// CTAs per SM of the two-column form (N <= 16 / N > 16)
+#ifndef CRTG_CRT_Q2_MINB
+#define CRTG_CRT_Q2_MINB 4
+#endif
+#ifndef CRTG_CRT_Q2_MINB_WIDE
+#define CRTG_CRT_Q2_MINB_WIDE 3
+#endif
 #ifndef CRTG_CRT_BATCH
 #define CRTG_CRT_BATCH 8
 #endif
@@ -330,10 +337,23 @@ __device__ __forceinline__ double raw_byte_to_f64(uint32_t w, int q) {
 #endif
 }
 
+// numpy's re + 1j*im for finite re, im (emulate.py:239-240):
+//   real = re + (0*im - 0), imag = 0 + (0 + im).
+// 0*im - 0 is a zero carrying im's sign, so real == re except that re = -0 with
+// im's sign bit clear gives +0; imag == im except that -0 gives +0 (= im + 0).
+// Integer select + one DADD instead of five FP64-pipe ops.
+__device__ __forceinline__ double2 assemble_f64(double re, double im) {
+  const long long rb = __double_as_longlong(re), ib = __double_as_longlong(im);
+  double2 o;
+  o.x = __longlong_as_double((rb == (long long)0x8000000000000000ull && ib >= 0) ? 0ll : rb);
+  o.y = __dadd_rn(im, 0.0);
+  return o;
+}
+
 // Q: output columns per thread (4; 2 for small grids, where 4 left a third of
 // a wave as the tail: 1024^2 was 2.3 waves)
 template <int N, bool SINGLE, bool REAL, int Q = 4>
-__global__ void __launch_bounds__(256, N > 16 ? 2 : (Q == 2 ? 4 : CRTG_CRT_MINB))
+__global__ void __launch_bounds__(256, N > 16 ? (Q == 2 ? CRTG_CRT_Q2_MINB_WIDE : 2) : (Q == 2 ? CRTG_CRT_Q2_MINB : CRTG_CRT_MINB))
     k_crt_n(int64_t m, int64_t n, const int8_t* __restrict__ e_re, const int8_t* __restrict__ e_im,
             int64_t e_plane, int64_t e_ld, const int32_t* __restrict__ mu,
             const int32_t* __restrict__ nu, const __grid_constant__ DevConsts dc, void* C,
@@ -440,10 +460,7 @@ __global__ void __launch_bounds__(256, N > 16 ? 2 : (Q == 2 ? 4 : CRTG_CRT_MINB)
       } else {
         const double re = ldexp_rn(reduce_double_fast(s1r, s2r[q], dc), ex);
         const double im = ldexp_rn(reduce_double_fast(s1i, s2i[q], dc), ex);
-        double2 o;
-        o.x = __dadd_rn(re, __dsub_rn(__dmul_rn(0.0, im), 0.0));
-        o.y = __dadd_rn(0.0, __dadd_rn(0.0, im));
-        reinterpret_cast<double2*>(C)[i * ldc + j] = o;
+        reinterpret_cast<double2*>(C)[i * ldc + j] = assemble_f64(re, im);
       }
     }
   }
@@ -456,11 +473,15 @@ int launch_crt(bool single, bool real, int64_t m, int64_t n, const int8_t* e_re,
                const int32_t* nu, const DevConsts& dc, void* C, int64_t ldc, cudaStream_t s,
                int max_ctas) {
   const bool limbs = dc.hi_scale != 0.0;
-  // few threads (small outputs): two columns per thread, so the grid is ~5 waves
-  // instead of ~2.3 with a one-third tail (1024^2); complex pipeline only
+  // complex pipeline: two columns per thread at 4 CTAs/SM (3 above 16 moduli),
+  // 64 registers, no spills -- twice the resident warps of the 4-column form
+  // (80 registers at 3 CTAs/SM) hide the FP64 dependency chains: 16384^3 N=15
+  // CRT stage 5.33 -> 5.12 ms per step; small grids (1024^2: ~5 waves instead
+  // of ~2.3 with a one-third tail) gain too.  CRTG_CRT_Q2_THREADS caps the
+  // 4-column thread count that still takes the 2-column form (0: never).
   static const int64_t q2_max = [] {
     const char* v = std::getenv("CRTG_CRT_Q2_THREADS");
-    return v && *v ? int64_t(std::atoll(v)) : int64_t(148) * 768 * 4;
+    return v && *v ? int64_t(std::atoll(v)) : INT64_MAX;
   }();
   const bool q2 = CRTG_CRT_TEMPLATED && limbs && !real && max_ctas == 0 &&
                   m * ((n + 3) / 4) <= q2_max;
