@@ -356,6 +356,28 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Unsigned key of |x| for the order-free column statistics: float -> the bits of
+// |x|; double -> the high word of |x| with bit 0 also set when the low word is
+// nonzero.  Zero <-> key 0, inf / nan <-> key >= the exponent mask, and for
+// every x with a nonzero key, the double whose high word is the key has x's
+// ilogb and the same comparisons against 2^500 / 2^-511 as |x| (so absmax and
+// the smallest nonzero |x| derive from max / min keys), except key 1: a nonzero
+// |x| < 2^-1042, whose exponent lies in the low word (unscaled_ok rejects it).
+template <typename T>
+__device__ __forceinline__ uint32_t abs_key(const T* p) {
+  if constexpr (sizeof(T) == 8) {
+    const uint2 w = *reinterpret_cast<const uint2*>(p);
+    return (w.y & 0x7FFFFFFFu) | min(w.x, 1u);
+  } else {
+    return __float_as_uint(*p) & 0x7FFFFFFFu;
+  }
+}
+template <typename T>
+__device__ __forceinline__ double key_value(uint32_t key) {
+  if constexpr (sizeof(T) == 8) return __hiloint2double(int(key), 0);
+  else return double(__uint_as_float(key));
+}
+
 template <typename T, bool REAL>
 __global__ void __launch_bounds__(128) k_col_stats(const T* __restrict__ B, int64_t ldb, int k,
                                                    int n, float p_fast, float delta,
@@ -375,8 +397,24 @@ __global__ void __launch_bounds__(128) k_col_stats(const T* __restrict__ B, int6
   const int nst = (k + kColR - 1) / kColR;
   const uint32_t ring_u32 = smem_u32(ring);
 
+  // full stages of full segments (every stage but the last, every CTA but the
+  // last column strip): thread t always copies chunk t % kChunks of rows
+  // t / kChunks + i * (128 / kChunks), so the addresses advance by constants
+  // (~3 instructions per 16-byte copy instead of ~28 for the general form)
+  constexpr int kRowStep = 128 / kChunks;  // rows between one thread's copies
+  static_assert(128 % kChunks == 0 && kColR % kRowStep == 0, "copy pattern");
+  const bool full_seg = valid == kSeg && blockDim.x == 128;
+  const int my_q = threadIdx.x % kChunks, my_r = threadIdx.x / kChunks;
+  const char* my_src = base + int64_t(my_r) * row_bytes + 16 * my_q;
+  const uint32_t my_dst = ring_u32 + my_r * kSeg + 16 * my_q;
   auto issue = [&](int st) {
-    if (st < nst) {
+    if (st < nst && full_seg && (st + 1) * kColR <= k) {
+      const char* src = my_src + int64_t(st) * kColR * row_bytes;
+      const uint32_t dst = my_dst + (st % kColS) * (kColR * kSeg);
+#pragma unroll
+      for (int i = 0; i < kColR / kRowStep; ++i)
+        cp_async16(dst + i * kRowStep * kSeg, src + int64_t(i) * kRowStep * row_bytes, 16);
+    } else if (st < nst) {
       const uint32_t dst0 = ring_u32 + (st % kColS) * (kColR * kSeg);
       for (int c = threadIdx.x; c < kColR * kChunks; c += blockDim.x) {
         const int r = c / kChunks, q = c % kChunks;
@@ -395,10 +433,11 @@ __global__ void __launch_bounds__(128) k_col_stats(const T* __restrict__ B, int6
   // order) and nothing else, so each row costs it one load, one DMUL and the
   // DADD on the chain; warps 1-3 take the order-free statistics (absmax,
   // smallest nonzero, finiteness) of the same stage rows in parallel
-  __shared__ double red_mx[3][32], red_mn[3][32];
-  __shared__ int red_bad[3][32];
-  double sum = 0.0, mx = 0.0, mn = INFINITY;
-  int bad = 0;
+  // order-free statistics as unsigned integer keys of |x| (see abs_key):
+  // max key -> absmax exponent / finiteness, min of (key - 1) -> smallest nonzero
+  __shared__ uint32_t red_mx[3][32], red_mn[3][32];
+  double sum = 0.0;
+  uint32_t kmx = 0u, kmn = 0xFFFFFFFFu;
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   for (int st = 0; st < nst; ++st) {
@@ -421,37 +460,40 @@ __global__ void __launch_bounds__(128) k_col_stats(const T* __restrict__ B, int6
         }
       }
     } else {
+#pragma unroll 4
       for (int r = warp - 1; r < nr; r += 3) {
-        const double x = double(seg[r * 32 + lane]);
-        const double ax = fabs(x);
-        bad |= !isfinite(x);
-        mx = fmax(mx, ax);
-        mn = fmin(mn, ax != 0.0 ? ax : INFINITY);
+        const uint32_t key = abs_key(seg + r * 32 + lane);
+        kmx = max(kmx, key);
+        kmn = min(kmn, key - 1u);  // 0 (zero) wraps to the largest key
       }
     }
     __syncthreads();
   }
   if (warp > 0) {
-    red_mx[warp - 1][lane] = mx;
-    red_mn[warp - 1][lane] = mn;
-    red_bad[warp - 1][lane] = bad;
+    red_mx[warp - 1][lane] = kmx;
+    red_mn[warp - 1][lane] = kmn;
   }
   __syncthreads();
   if (warp > 0) return;
-  mx = fmax(fmax(red_mx[0][lane], red_mx[1][lane]), red_mx[2][lane]);
-  mn = fmin(fmin(red_mn[0][lane], red_mn[1][lane]), red_mn[2][lane]);
-  bad = red_bad[0][lane] | red_bad[1][lane] | red_bad[2][lane];
+  kmx = max(max(red_mx[0][lane], red_mx[1][lane]), red_mx[2][lane]);
+  kmn = min(min(red_mn[0][lane], red_mn[1][lane]), red_mn[2][lane]);
+  const bool bad = kmx >= (sizeof(T) == 8 ? 0x7FF00000u : 0x7F800000u);  // inf / nan
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicAdd(diag + CRTG_DIAG_NONFINITE_B, 1ull);
   double other = 0.0;
   if (!REAL) {  // lanes (2c, 2c+1) = (re, im) of column c
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, 1));
+    kmx = max(kmx, __shfl_xor_sync(0xffffffffu, kmx, 1));
+    kmn = min(kmn, __shfl_xor_sync(0xffffffffu, kmn, 1));
     other = __shfl_xor_sync(0xffffffffu, sum, 1);
   }
   const int j = j0 + (REAL ? lane : lane >> 1);
   if (j >= n || (!REAL && (lane & 1))) return;
-  colabs[j] = mx;
-  if (!unscaled_ok(mx, mn)) {
+  const double mx = key_value<T>(kmx);
+  const double mn = kmn == 0xFFFFFFFFu ? INFINITY : key_value<T>(kmn + 1u);
+  // key 1 (double): every nonzero |x| < 2^-1042, its exponent is not in the key
+  // -> the fallback recomputes the exact absmax (colabs = -1)
+  const bool inexact = sizeof(T) == 8 && kmx == 1u;
+  colabs[j] = inexact ? -1.0 : mx;
+  if (inexact || !unscaled_ok(mx, mn)) {
     nu[j] = kNuPending;
     return;
   }
@@ -470,10 +512,17 @@ __global__ void k_col_fallback(const T* __restrict__ B, int64_t ldb, int k, int 
   pdl_begin();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n || nu[j] != kNuPending) return;
-  const double mx = colabs[j];
-  const Pow2 sc = make_pow2(mx == 0.0 ? 0 : -ilogb(mx));
   const T* p = B + (REAL ? 1 : 2) * int64_t(j);
   const int64_t stride = (REAL ? 1 : 2) * ldb;
+  double mx = colabs[j];
+  if (mx < 0.0) {  // k_col_stats' key could not carry the exponent: exact absmax
+    mx = 0.0;
+    for (int h = 0; h < k; ++h) {
+      mx = fmax(mx, fabs(double(p[h * stride])));
+      if (!REAL) mx = fmax(mx, fabs(double(p[h * stride + 1])));
+    }
+  }
+  const Pow2 sc = make_pow2(mx == 0.0 ? 0 : -ilogb(mx));
   double sr = 0.0, si = 0.0;
   for (int h = 0; h < k; ++h) {
     sr = __dadd_rn(sr, sq(sc, double(p[h * stride])));

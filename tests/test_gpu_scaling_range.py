@@ -100,3 +100,46 @@ def test_unaligned_leading_dimension_path(crt):
     got = crt.emulate_gemm_complex(torch.from_numpy(a).cuda(), bt, cfg).cpu().numpy()
     want = orc.emulate_complex(a, full[:, :11], 8, "fast", "single")
     assert got.tobytes() == want.tobytes()
+
+
+def key_edge_columns(k, n, seed):
+    """Columns at the edges of k_col_stats' integer keys (high word of |x|, bit 0
+    set for a nonzero low word): equal high words with different low words,
+    2^500 exactly and one ulp above, 2^-511 exactly and one ulp below, columns
+    whose nonzeros are all below 2^-1042 (key 1: exponent only in the low
+    word), a lone NaN-free huge value, and ordinary columns in between."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((k, n)) + 1j * rng.standard_normal((k, n))
+    ulp_up = lambda v: np.nextafter(v, np.inf)  # noqa: E731
+    ulp_dn = lambda v: np.nextafter(v, 0.0)  # noqa: E731
+    x[:, 0] = 2.0 ** 500
+    x[7, 1] = ulp_up(2.0 ** 500)
+    x[:, 1] = np.where(np.arange(k) == 7, x[7, 1], 1.0)
+    x[:, 2] = 2.0 ** -511
+    x[3, 2] = 1.0
+    x[:, 3] = 1.0
+    x[5, 3] = ulp_dn(2.0 ** -511)
+    x[:, 4] = 0.0
+    x[::7, 4] = 2.0 ** -1060
+    x[1, 4] = 2.0 ** -1065 + 2.0 ** -1070
+    x[:, 5] = 0.0
+    x[9, 5] = 5e-324 * 3
+    x[:, 6] = (1.0 + 2.0 ** -40) * (1 + 1j)  # high words equal, low words differ
+    x[11, 6] = 1.0 + 2.0 ** -52
+    x[:, 8] = x[:, 8].real * 2.0 ** -1030 + 1j * x[:, 8].imag * 2.0 ** -1010  # subnormal mix
+    x[:, 9] = 0.0
+    x[0, 9] = 1j * 2.0 ** -1050
+    return x
+
+
+@pytest.mark.parametrize("k,n", [(200, 40), (64, 16), (1000, 33)])
+def test_col_stats_key_edges(crt, k, n):
+    b = key_edge_columns(k, n, k + n)
+    a = np.random.default_rng(1).standard_normal((5, k)) + 0j
+    ms = crt.select_moduli(14)
+    diag, odiag = {}, {}
+    sv = crt.fast_scaling(a, b, ms, None, diag)
+    mu, nu = orc.exponents(a, b, 14, "fast", odiag)
+    assert np.array_equal(sv.nu_exp, nu)
+    assert np.array_equal(sv.mu_exp, mu)
+    assert diag.get("clamped_nu", 0) == odiag.get("clamped_nu", 0)
