@@ -329,8 +329,8 @@ __global__ void __launch_bounds__(128) k_col_sumsq(const T* __restrict__ B, int6
 // Fast-mode column statistics in ONE pass (k_col_stats): per column j of B (and
 // per part) the sequential numpy axis-0 chain of UNSCALED squares, the absmax,
 // the smallest nonzero |x| and finiteness; then the exponent in-kernel when
-// unscaled_ok, else nu[j] = kNuPending and k_col_fallback re-runs that column's
-// chains scaled.  Memory-level parallelism comes from a cp.async ring: a CTA
+// unscaled_ok, else the chain lanes re-run that column's chains scaled from B
+// (the reference's two-pass form; no second launch).  Memory-level parallelism comes from a cp.async ring: a CTA
 // owns 32 components (16 complex columns x (re, im), or 32 real columns) = one
 // 256-byte (128 for float) segment per row of B, and keeps kColS stages of
 // kColR rows in flight while warp 0 runs the 32 chains out of shared memory —
@@ -344,7 +344,6 @@ __global__ void __launch_bounds__(128) k_col_sumsq(const T* __restrict__ B, int6
 #endif
 constexpr int kColR = CRTG_COL_R;  // rows per stage
 constexpr int kColS = 4;           // stages
-constexpr int32_t kNuPending = INT32_MIN;
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
@@ -486,50 +485,47 @@ __global__ void __launch_bounds__(128) k_col_stats(const T* __restrict__ B, int6
     other = __shfl_xor_sync(0xffffffffu, sum, 1);
   }
   const int j = j0 + (REAL ? lane : lane >> 1);
-  if (j >= n || (!REAL && (lane & 1))) return;
-  const double mx = key_value<T>(kmx);
+  const bool live = j < n;  // both lanes of a column pair agree
+  double mx = key_value<T>(kmx);
   const double mn = kmn == 0xFFFFFFFFu ? INFINITY : key_value<T>(kmn + 1u);
   // key 1 (double): every nonzero |x| < 2^-1042, its exponent is not in the key
-  // -> the fallback recomputes the exact absmax (colabs = -1)
   const bool inexact = sizeof(T) == 8 && kmx == 1u;
-  colabs[j] = inexact ? -1.0 : mx;
-  if (inexact || !unscaled_ok(mx, mn)) {
-    nu[j] = kNuPending;
-    return;
-  }
-  const bool zero = mx == 0.0;
-  const Pow2 sc = make_pow2(zero ? 0 : -ilogb(mx));
-  double sumsq = __dadd_rn(__dadd_rn(0.0, unscale_sq(sum, sc)), unscale_sq(other, sc));
-  if (zero) sumsq = 1.0;
-  nu[j] = fast_exponent(mx, sumsq, p_fast, delta, diag + CRTG_DIAG_CLAMPED_NU);
-}
-
-// the two-pass form for the columns k_col_stats could not take unscaled
-template <typename T, bool REAL>
-__global__ void k_col_fallback(const T* __restrict__ B, int64_t ldb, int k, int n, float p_fast,
-                               float delta, const double* __restrict__ colabs,
-                               int32_t* __restrict__ nu, unsigned long long* __restrict__ diag) {
-  pdl_begin();
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n || nu[j] != kNuPending) return;
-  const T* p = B + (REAL ? 1 : 2) * int64_t(j);
-  const int64_t stride = (REAL ? 1 : 2) * ldb;
-  double mx = colabs[j];
-  if (mx < 0.0) {  // k_col_stats' key could not carry the exponent: exact absmax
-    mx = 0.0;
-    for (int h = 0; h < k; ++h) {
-      mx = fmax(mx, fabs(double(p[h * stride])));
-      if (!REAL) mx = fmax(mx, fabs(double(p[h * stride + 1])));
+  const bool pend = live && (inexact || !unscaled_ok(mx, mn));
+  double s_re = sum, s_im = other;
+  if (__any_sync(0xffffffffu, pend)) {
+    // rare: the reference's two-pass form for this column, right here (each lane
+    // its own part: the exact absmax when the key could not carry it, then the
+    // sequential chain of scaled squares re-read from B)
+    const T* p = B + int64_t(j) * kParts + (REAL ? 0 : (lane & 1));
+    const int64_t stride = int64_t(kParts) * ldb;
+    if (pend && inexact) {
+      double a = 0.0;
+      for (int h = 0; h < k; ++h) a = fmax(a, fabs(double(p[h * stride])));
+      mx = a;
+    }
+    if (!REAL) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    double sc_sum = 0.0;
+    if (pend) {
+      const Pow2 sc = make_pow2(mx == 0.0 ? 0 : -ilogb(mx));
+      for (int h = 0; h < k; ++h) sc_sum = __dadd_rn(sc_sum, sq(sc, double(p[h * stride])));
+    }
+    const double sc_other = REAL ? 0.0 : __shfl_xor_sync(0xffffffffu, sc_sum, 1);
+    if (pend) {
+      s_re = sc_sum;
+      s_im = sc_other;
     }
   }
-  const Pow2 sc = make_pow2(mx == 0.0 ? 0 : -ilogb(mx));
-  double sr = 0.0, si = 0.0;
-  for (int h = 0; h < k; ++h) {
-    sr = __dadd_rn(sr, sq(sc, double(p[h * stride])));
-    if (!REAL) si = __dadd_rn(si, sq(sc, double(p[h * stride + 1])));
+  if (!live || (!REAL && (lane & 1))) return;
+  colabs[j] = mx;
+  const bool zero = mx == 0.0;
+  double sumsq;
+  if (pend) {
+    sumsq = __dadd_rn(__dadd_rn(0.0, s_re), s_im);  // already scaled
+  } else {
+    const Pow2 sc = make_pow2(zero ? 0 : -ilogb(mx));
+    sumsq = __dadd_rn(__dadd_rn(0.0, unscale_sq(s_re, sc)), unscale_sq(s_im, sc));
   }
-  double sumsq = __dadd_rn(__dadd_rn(0.0, sr), si);
-  if (mx == 0.0) sumsq = 1.0;
+  if (zero) sumsq = 1.0;
   nu[j] = fast_exponent(mx, sumsq, p_fast, delta, diag + CRTG_DIAG_CLAMPED_NU);
 }
 
@@ -644,13 +640,15 @@ int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n, 
     constexpr int parts = R ? 1 : 2;
     constexpr int cols = 32 / parts;
     const size_t smem = size_t(kColS) * kColR * 32 * sizeof(T);
-    cudaFuncSetAttribute(k_col_stats<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    static const bool attr = [&] {
+      return cudaFuncSetAttribute(k_col_stats<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)) == cudaSuccess;
+    }();
+    (void)attr;
     launch_k(k_col_stats<T, R>, unsigned((n + cols - 1) / cols), 128, smem, s,
         static_cast<const T*>(B), ldb, int(k), int(n), p_fast, delta, nu, colabs, diag);
-    launch_k(k_col_fallback<T, R>, unsigned((n + 127) / 128), 128, 0, s,
-        static_cast<const T*>(B), ldb, int(k), int(n), p_fast, delta, colabs, nu, diag);
   })
-  return launched(2);
+  return launched(1);
 }
 
 int launch_bar(const double* absval, int64_t count, int32_t* bar, cudaStream_t s) {
