@@ -10,6 +10,8 @@
 // contiguous row is numpy's pairwise sum (8-accumulator leaves <= 128 elements,
 // recursive halving at n/2 rounded down to a multiple of 8, initial value 0);
 // np.sum(axis=0) is a sequential column sweep.
+#include <atomic>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -640,11 +642,15 @@ int launch_col_fast(int elem, const void* B, int64_t ldb, int64_t k, int64_t n, 
     constexpr int parts = R ? 1 : 2;
     constexpr int cols = 32 / parts;
     const size_t smem = size_t(kColS) * kColR * 32 * sizeof(T);
-    static const bool attr = [&] {
-      return cudaFuncSetAttribute(k_col_stats<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(smem)) == cudaSuccess;
-    }();
-    (void)attr;
+    // the attribute is per device: set once per (instantiation, device)
+    static std::atomic<unsigned long long> attr_set{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set.load(std::memory_order_relaxed) & bit) &&
+        cudaFuncSetAttribute(k_col_stats<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem)) == cudaSuccess)
+      attr_set.fetch_or(bit, std::memory_order_relaxed);
     launch_k(k_col_stats<T, R>, unsigned((n + cols - 1) / cols), 128, smem, s,
         static_cast<const T*>(B), ldb, int(k), int(n), p_fast, delta, nu, colabs, diag);
   })
