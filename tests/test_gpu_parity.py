@@ -498,3 +498,29 @@ def test_modulus_counts_accurate_large_tiles(crt, N):
         got = crt.emulate_gemm_complex(a, b, cfg)
         want = orc.emulate_complex(a, b, N, mode, "double")
         assert got.tobytes() == want.tobytes(), mode
+
+
+def _fuzz_cases(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(count):
+        m, n, k = (int(x) for x in rng.integers(1, 700, 3))
+        out.append((i, m, n, k, int(rng.integers(1, 21)), ["fast", "accurate"][i % 2],
+                    ["double", "single"][(i // 2) % 2], float(rng.choice([0.5, 1.0, 2.0, 4.0]))))
+    return out
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(24, 2026), ids=lambda c: f"fuzz{c[0]}")
+def test_random_shapes_modes_precisions(crt, case):
+    """Seeded sweep over ragged shapes (every extent 1..699, so partial residue
+    tiles, partial 128/256-row GEMM tiles and odd CRT column counts), modulus
+    counts 1..20, both modes, both precisions and exponent spreads phi, each
+    compared bit for bit with the oracle (reference emulate.py:193-240)."""
+    i, m, n, k, N, mode, prec, phi = case
+    a = orc.gen_matrix(m, k, phi, 1000 + i, prec)
+    b = orc.gen_matrix(k, n, phi, 2000 + i, prec)
+    cfg = crt.EmuConfig(precision=prec, domain="complex", mode=mode, num_moduli=N)
+    got = crt.emulate_gemm_complex(a, b, cfg)
+    want = orc.emulate_complex(a, b, N, mode, prec)
+    assert got.dtype == want.dtype and got.shape == want.shape
+    assert got.tobytes() == want.tobytes(), f"{int(np.count_nonzero(got != want))} mismatches"

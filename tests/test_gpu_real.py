@@ -155,3 +155,23 @@ def test_real_torch_inputs(crt):
     assert got.is_cuda and got.dtype == torch.float64
     want = orc.emulate_real(a.cpu().numpy(), b.cpu().numpy(), 15)
     assert got.cpu().numpy().tobytes() == want.tobytes()
+
+
+def _fuzz_real(count, seed):
+    rng = np.random.default_rng(seed)
+    return [(i, *(int(x) for x in rng.integers(1, 700, 3)), int(rng.integers(1, 21)),
+             ["fast", "accurate"][i % 2], ["double", "single"][(i // 2) % 2],
+             float(rng.choice([0.5, 2.0, 4.0]))) for i in range(count)]
+
+
+@pytest.mark.parametrize("case", _fuzz_real(16, 2027), ids=lambda c: f"fuzz{c[0]}")
+def test_real_random_shapes(crt, case):
+    """Seeded ragged shapes, modulus counts, modes and precisions for the real
+    pipeline (EPI_REAL, reference emulate.py:169-190) against the oracle."""
+    i, m, n, k, N, mode, prec, phi = case
+    a = orc.gen_matrix(m, k, phi, 3000 + i, prec, domain="real")
+    b = orc.gen_matrix(k, n, phi, 4000 + i, prec, domain="real")
+    cfg = crt.EmuConfig(precision=prec, domain="real", mode=mode, num_moduli=N)
+    got = crt.emulate_gemm_real(a, b, cfg)
+    want = orc.emulate_real(a, b, N, mode, prec)
+    assert got.dtype == want.dtype and got.tobytes() == want.tobytes()
